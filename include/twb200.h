@@ -1,0 +1,312 @@
+/*
+ * twb200.h — C ABI of libtwb200, the B200 engine for the Revati/timewarp hot path
+ * (arXiv 2601.00397): batch-duration prediction, Timekeeper min-advance, and the
+ * lockstep discrete-event loop, evaluated in bulk over many serving configs.
+ *
+ * Conventions (all entry points):
+ *   - every data pointer is a DEVICE pointer allocated by the caller (the library
+ *     never allocates except the small scratch noted per call); sizes are element
+ *     counts unless the name says bytes;
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream) and is stream-ordered; calls never synchronize;
+ *   - return 0 on success, otherwise a TW_E* code; tw_last_error() gives text.
+ *     Per-element domain errors (EmptyBatch, NegativeDuration, TableMiss) are NOT
+ *     call failures: they are written as negative codes into the output arrays,
+ *     and the Python shim re-raises the reference's exception classes.
+ *   - reentrant; one host thread per device is the intended use.
+ *
+ * The reference is pure Python; the boundary a maintainer binds is its plugin
+ * surface (see INTEGRATION.md for the ctypes stubs):
+ *   predictor plugin   pkg/src/timewarp/predictor.py:100-266 (predict(batch, hw) -> ns)
+ *   Timekeeper core    pkg/src/timewarp/timekeeper.py:68-366 (BarrierCore.handle/_resolve)
+ *   event loop         pkg/src/timewarp/oracle.py:49-180     (simulate / _plan)
+ */
+#ifndef TWB200_H
+#define TWB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TWB200_ABI_VERSION 1
+
+/* ---- call status codes ---------------------------------------------------- */
+#define TW_OK 0
+#define TW_EINVAL 1    /* bad argument (null pointer, size, malformed blob) */
+#define TW_ECUDA 2     /* CUDA launch/runtime error */
+#define TW_ENOSMEM 3   /* predictor blob or per-warp state exceeds shared memory */
+
+/* ---- per-element prediction codes (negative int64 in out_ns) -------------- */
+#define TW_PRED_EMPTY_BATCH (-1)      /* predictor.py:95-97   EmptyBatch       */
+#define TW_PRED_NEGATIVE (-2)         /* predictor.py:143-145 NegativeDuration */
+#define TW_PRED_TABLE_MISS (-3)       /* predictor.py:240-242 TableMiss        */
+#define TW_PRED_BAD_DESC (-4)         /* desc_id out of range (host bug)       */
+
+/* ---- predictor set ("pset") blob ------------------------------------------ */
+/* One contiguous, 16-byte aligned byte blob holding every predictor a sweep uses:
+ *   tw_pset_header | tw_pred_desc[n_desc] | table pool
+ * A table (kind TABLE) occupies, at byte offset `table_off` from the blob start:
+ *   int32 paxis[np] (sorted, unique) | int32 daxis[nd] (sorted, unique) |
+ *   (pad to 8) | int64 grid_us[np*nd] (row-major [p][d]; TW_TABLE_HOLE = no row)
+ * The blob is built on host (paper_2601_00397_b200/predictor.py::PredictorSet) and
+ * staged whole into shared memory by each CTA with one cp.async.bulk (TMA). */
+#define TW_PSET_MAGIC 0x54534550u /* "PEST" little-endian */
+#define TW_PRED_CONSTANT 0        /* predictor.py:100-111 */
+#define TW_PRED_LINEAR 1          /* predictor.py:114-146 */
+#define TW_PRED_TABLE 2           /* predictor.py:149-242 */
+#define TW_TABLE_HOLE (-1)
+
+typedef struct tw_pset_header {
+  uint32_t magic;
+  uint32_t version;
+  int32_t n_desc;
+  int32_t total_bytes; /* whole blob, multiple of 16 */
+} tw_pset_header;      /* 16 B */
+
+typedef struct tw_pred_desc {
+  int32_t kind;                /* TW_PRED_* */
+  int32_t allow_extrapolation; /* TABLE: nearest-row fallback (predictor.py:238-239) */
+  int64_t constant_us;         /* CONSTANT: duration_us (>= 0, checked on host) */
+  double base_us;              /* LINEAR coefficients, applied left to right:     */
+  double per_prefill_token_us; /* ((base + kp*P) + kd*D) + kc*C, each op rounded  */
+  double per_decode_us;        /* in fp64, no FMA (predictor.py:137-142)          */
+  double per_context_token_us;
+  int32_t table_off; /* TABLE: byte offset of paxis from blob start */
+  int32_t np;        /* TABLE: prefill-axis length */
+  int32_t nd;        /* TABLE: decode-axis length  */
+  int32_t pad;
+} tw_pred_desc; /* 64 B */
+
+/* ---- bulk predictor (kernel 2 of the north star) -------------------------- */
+/* out_ns[i] = predict(features i) in ns (multiple of 1000) or a TW_PRED_* code.
+ * Features are the reference's BatchComposition totals (predictor.py:69-84):
+ * P = total_prefill_tokens, D = num_decodes, C = total_context; a batch is empty
+ * iff it has no slots, which the feature-only entry point encodes as
+ * P == 0 && D == 0 && C < 0 (C = -1 marks "no slots": predictor.py:83-84). */
+int tw_predict_features(const void* pset, int64_t pset_bytes, const int32_t* P,
+                        const int32_t* D, const int64_t* C, const int32_t* desc_id,
+                        int64_t n, int64_t* out_ns, void* stream);
+
+/* Fused batch-feature extraction + prediction over CSR batches (kernels 1+2).
+ * Batch b owns slots [batch_off[b], batch_off[b+1]); a slot is a PrefillChunk
+ * (slot_tok >= 0: chunk_tokens, slot_ctx: context_len_before) or a DecodeSlot
+ * (slot_tok == -1, slot_ctx: context_len) — predictor.py:47-61.
+ * feat_out (optional, may be NULL) receives int64 {P, D, C} per batch. */
+int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batch_off,
+                       const int32_t* slot_tok, const int32_t* slot_ctx,
+                       const int32_t* desc_id, int64_t n_batches, int64_t* feat_out,
+                       int64_t* out_ns, void* stream);
+
+/* ---- Timekeeper (kernel 3): BarrierCore op-stream replay ------------------ */
+/* One op stream per Timekeeper instance ("config"); every stream is replayed
+ * by one warp with the BarrierCore state machine (timekeeper.py:131-366) on a
+ * FakeClock (pkg/tests/_support.py:25-38). Actors are identified by their
+ * registration index (client ids "actor1", "observer2", ... map to 0, 1, ...). */
+#define TW_OP_REGISTER_ACTOR 0    /* arg ignored                              */
+#define TW_OP_REGISTER_OBSERVER 1
+#define TW_OP_SEAL 2
+#define TW_OP_JUMP 3              /* client, arg = absolute target ns          */
+#define TW_OP_ENTER 4             /* client, group (small int), arg = expected */
+#define TW_OP_DEREGISTER 5        /* client                                    */
+#define TW_OP_ADVANCE_CLOCK 6     /* arg = ns the FakeClock moves forward      */
+#define TW_OP_BAD_CLIENT 7        /* any op naming an unknown client id        */
+
+/* ack codes written per op (errors.py:12-45, wire.py MalformedBody) */
+#define TW_ACK_OK 0
+#define TW_ACK_REGISTRATION_SEALED 1
+#define TW_ACK_NO_ACTORS 2
+#define TW_ACK_UNKNOWN_CLIENT 3
+#define TW_ACK_INVALID_STATE 4
+#define TW_ACK_ROLE_VIOLATION 5
+#define TW_ACK_INVALID_DELTA 6
+#define TW_ACK_EXPECTED_MISMATCH 7
+#define TW_ACK_TOO_MANY 8 /* > TW_TK_MAX_CLIENTS clients or groups (engine limit) */
+
+#define TW_TK_MAX_CLIENTS 32
+#define TW_TK_MAX_GROUPS 32
+
+typedef struct tw_tk_op {
+  int64_t arg;
+  int32_t type;   /* TW_OP_* */
+  int16_t client; /* registration index */
+  int16_t group;  /* collective group index */
+} tw_tk_op;       /* 16 B */
+
+typedef struct tw_tk_event {
+  int64_t offset_ns; /* CLOCK_UPDATE offset, or COLLECTIVE_RELEASE group  */
+  int64_t seq;       /* CLOCK_UPDATE seq, or release generation           */
+  int64_t wall_ns;   /* FakeClock stamp                                   */
+  int32_t kind;      /* 0 = CLOCK_UPDATE (incl. suppressed), 1 = RELEASE  */
+  int32_t op_index;  /* op that triggered it                              */
+} tw_tk_event;       /* 32 B */
+
+typedef struct tw_tk_final {
+  int64_t offset_ns;
+  int64_t seq;
+  int64_t wall_ns;
+  int64_t rounds;     /* resolves */
+  int64_t broadcasts; /* CLOCK_UPDATEs (including suppressed ones) */
+  int64_t n_events;   /* total events produced (may exceed capacity) */
+  int32_t status;     /* 0 ok, 1 event buffer overflow, 2 engine limit hit */
+  int32_t pad;
+  int64_t pad2;
+} tw_tk_final; /* 64 B */
+
+/* Streams are CSR: stream s owns ops [op_off[s], op_off[s+1]); its events go to
+ * ev[ev_off[s] ..  ev_off[s+1]) (capacity; excess counted, not written).
+ * wall0_ns[s]: FakeClock start; cooldown_ns[s]: BarrierCore cooldown (>= 0);
+ * suppress[s]: suppress_broadcasts flag. ack: one int32 per op. */
+int tw_tk_replay(const tw_tk_op* ops, const int64_t* op_off, int32_t n_streams,
+                 const int64_t* wall0_ns, const int64_t* cooldown_ns,
+                 const uint8_t* suppress, int32_t* ack, tw_tk_event* ev,
+                 const int64_t* ev_off, tw_tk_final* fin, void* stream);
+
+/* Bulk min-advance (the _try_resolve/_resolve arithmetic, timekeeper.py:318-366)
+ * for C independent Timekeepers with A actor slots each, one round:
+ * pending[c*A + a] = requested target or INT64_MAX (no request / not eligible);
+ * eligible_mask[c] bit a = actor a is active and not exempt. A round resolves
+ * iff sealed (assumed) and every eligible actor has a pending target. State
+ * arrays (offset/seq/wall/last_bcast; last_bcast = INT64_MIN means None) are
+ * updated in place; broadcast[c] = 1 when a CLOCK_UPDATE is emitted, 0 when the
+ * round resolved silently, -1 when it did not resolve. Pending entries of
+ * resolved configs are reset to INT64_MAX (pending.clear()). Requires A <= 32. */
+int tw_tk_resolve(int64_t* pending, const uint32_t* eligible_mask, int32_t n_cfg,
+                  int32_t A, int64_t cooldown_ns, int64_t* offset_ns, int64_t* seq,
+                  int64_t* wall_ns, int64_t* last_bcast_ns, int8_t* broadcast,
+                  void* stream);
+
+/* ---- lockstep event loop (kernel 4): oracle.simulate over many configs ---- */
+#define TW_POLICY_MIXED 0               /* engine.py:46-48 */
+#define TW_POLICY_PREFILL_PRIORITIZED 1
+
+#define TW_SIM_TIMEKEEPER 1u /* flags: drive virtual time through per-config BarrierCore rounds */
+
+typedef struct tw_sim_cfg {
+  /* EngineConfig (engine.py:98-133) */
+  int32_t chunk_size;
+  int32_t max_batch_tokens;
+  int32_t max_running;
+  int32_t kv_block_tokens;
+  int32_t kv_capacity_blocks;
+  int32_t workers_per_replica; /* TP */
+  int32_t pp_stages;           /* PP */
+  int32_t policy;              /* TW_POLICY_* */
+  int32_t pred_id;             /* descriptor index in the pset */
+  int32_t workload_id;         /* index into the workload CSR */
+  int64_t epoch_ns;            /* simulate(epoch_ns=...) (oracle.py:53) */
+  int64_t tk_cooldown_ns;      /* Timekeeper cooldown J for the actor grid */
+  uint32_t flags;              /* TW_SIM_* */
+  int32_t pad;
+} tw_sim_cfg; /* 64 B */
+
+/* status codes per config */
+#define TW_SIM_OK 0
+#define TW_SIM_STALLED_ACTIVE 1  /* oracle.py:184-188 */
+#define TW_SIM_STALLED_KV 2      /* oracle.py:189-193 */
+#define TW_SIM_PRED_ERROR 3      /* predictor raised; pred_code holds TW_PRED_* */
+#define TW_SIM_CAPACITY 4        /* max_running exceeds the launch's slot capacity */
+#define TW_SIM_BAD_CONFIG 5      /* EngineConfig validation failed (engine.py:109-120) */
+#define TW_SIM_EVENT_OVERFLOW 6  /* flag bit (status |= 1<<8) when the dump was truncated */
+
+typedef struct tw_sim_result {
+  int64_t final_now_ns; /* virtual time when the loop drained (max FINISHED ts) */
+  int64_t steps;        /* non-empty batches = predictions */
+  int64_t events;       /* token events emitted */
+  uint64_t digest;      /* order-sensitive digest of the event stream (tw_event_hash) */
+  int64_t tk_seq;       /* Timekeeper CLOCK_UPDATE count (TW_SIM_TIMEKEEPER) */
+  int64_t tk_offset_ns; /* final Timekeeper offset */
+  int64_t tk_wall_ns;   /* final FakeClock wall */
+  int32_t status;       /* TW_SIM_* (+ overflow bit) */
+  int32_t pred_code;    /* TW_PRED_* when status == TW_SIM_PRED_ERROR */
+} tw_sim_result;        /* 64 B */
+
+/* event kinds (engine.py:57-60) and the dump record */
+#define TW_EV_FIRST_TOKEN 0
+#define TW_EV_OUTPUT_TOKEN 1
+#define TW_EV_FINISHED 2
+typedef struct tw_event {
+  int64_t ts_ns;
+  int32_t step;
+  int32_t req_kind; /* (request index << 2) | kind */
+} tw_event;         /* 16 B */
+
+/* Workloads are CSR over requests already sorted stably by offset (oracle.py:60):
+ * workload w owns requests [wl_off[w], wl_off[w+1]).
+ * order: permutation of config ids (largest estimated cost first) that the
+ * persistent CTAs pull from a device work counter; may be NULL (identity).
+ * req_first_ns / req_finish_ns (optional): per (config, request) FIRST_TOKEN and
+ * FINISHED timestamps at [req_base[c] + i]; unset entries are left untouched.
+ * ev / ev_off (optional): audited configs get their full event stream in
+ * ev[ev_off[c] .. ev_off[c+1]). slot_capacity: per-warp active-list capacity,
+ * normally max(max_running) over the configs (configs above it finish with
+ * TW_SIM_CAPACITY; at most 4096). scratch: >= 16 bytes of device memory, zeroed by
+ * the call (work counter). */
+int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
+                int32_t n_cfg, const int32_t* order, const int64_t* wl_off,
+                const int64_t* req_offset_ns, const int32_t* req_prompt,
+                const int32_t* req_output, tw_sim_result* results,
+                const int64_t* req_base, int64_t* req_first_ns, int64_t* req_finish_ns,
+                const int64_t* ev_off, tw_event* ev, int32_t slot_capacity, void* scratch,
+                void* stream);
+
+/* Launch geometry the library picked for the last tw_sim_many on this thread
+ * (for the bench's roofline bookkeeping). */
+int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
+                       int32_t* slot_capacity);
+
+/* ---- misc ------------------------------------------------------------------ */
+int tw_abi_version(void);
+const char* tw_last_error(void);
+/* Number of kernel launches this thread has issued through the library. */
+int64_t tw_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+/* ---- the event digest, shared by the CUDA path and the oracle ------------- */
+/* digest = sum over events k (0-based, emission order) of tw_event_hash(k, ...)
+ * mod 2^64: position-bound, so any reordering, timestamp, step or kind change of
+ * any event changes it (w.h.p.). req = index in the stable-sorted arrivals. */
+#if defined(__CUDACC__)
+#define TW_HD __host__ __device__ __forceinline__
+#else
+#define TW_HD static inline
+#endif
+TW_HD uint64_t tw_mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+TW_HD uint64_t tw_event_hash(uint64_t k, uint64_t req, uint64_t kind, int64_t ts,
+                             int64_t step) {
+  uint64_t a = k * 0x9E3779B97F4A7C15ULL + req * 0xC2B2AE3D27D4EB4FULL + kind;
+  uint64_t b = tw_mix64(a ^ (uint64_t)ts);
+  return tw_mix64(b + (uint64_t)step);
+}
+
+#endif /* TWB200_H */
+
+/* layout checks (the Python mirrors in paper_2601_00397_b200/_lib.py assert the same) */
+#ifdef __cplusplus
+static_assert(sizeof(tw_pred_desc) == 64, "tw_pred_desc");
+static_assert(sizeof(tw_tk_op) == 16, "tw_tk_op");
+static_assert(sizeof(tw_tk_event) == 32, "tw_tk_event");
+static_assert(sizeof(tw_tk_final) == 64, "tw_tk_final");
+static_assert(sizeof(tw_sim_cfg) == 64, "tw_sim_cfg");
+static_assert(sizeof(tw_sim_result) == 64, "tw_sim_result");
+static_assert(sizeof(tw_event) == 16, "tw_event");
+#else
+_Static_assert(sizeof(tw_pred_desc) == 64, "tw_pred_desc");
+_Static_assert(sizeof(tw_tk_op) == 16, "tw_tk_op");
+_Static_assert(sizeof(tw_tk_event) == 32, "tw_tk_event");
+_Static_assert(sizeof(tw_tk_final) == 64, "tw_tk_final");
+_Static_assert(sizeof(tw_sim_cfg) == 64, "tw_sim_cfg");
+_Static_assert(sizeof(tw_sim_result) == 64, "tw_sim_result");
+_Static_assert(sizeof(tw_event) == 16, "tw_event");
+#endif

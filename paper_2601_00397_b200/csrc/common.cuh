@@ -1,0 +1,281 @@
+// common.cuh — device helpers shared by the libtwb200 kernels (sm_100a).
+//
+//  * pset staging: the whole predictor blob is copied global -> shared with ONE
+//    cp.async.bulk (TMA bulk-copy engine, SASS UBLKCP) completing on an mbarrier;
+//  * the exact-fp64 duration predictor (reference: predictor.py:100-242) in a
+//    scalar form (bulk kernel, one query per thread) and a warp-cooperative form
+//    (event loop, one query per warp: ballot-based axis bracketing);
+//  * int64 warp reductions.
+//
+// Bit-exactness contract: every fp64 op is an explicit _rn
+// intrinsic (no FMA contraction possible), ints convert exactly, rounding to whole
+// microseconds is half-to-even (__double2ll_rn), durations are int64 ns.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/twb200.h"
+
+namespace twb {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------------------
+// error / launch bookkeeping (abi.cu)
+// ------------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch();
+
+// ------------------------------------------------------------------------------
+// TMA bulk copy of the predictor blob into shared memory
+// ------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Copies `bytes` (multiple of 16, both addresses 16-B aligned) from global `src` to
+// shared `dst` using the bulk-copy (TMA) engine. Must be called by ALL threads of
+// the CTA; thread 0 issues, everyone waits on the mbarrier's phase 0.
+__device__ __forceinline__ void tma_stage_to_smem(void* dst, const void* src, uint32_t bytes,
+                                                  uint64_t* mbar) {
+  const uint32_t bar = smem_u32(mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    // chunks of <= 64 KiB keep each transfer well inside the tx-count range
+    uint32_t off = 0;
+    while (off < bytes) {
+      uint32_t n = bytes - off;
+      if (n > 65536u) n = 65536u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(static_cast<char*>(dst) + off)),
+          "l"(static_cast<const char*>(src) + off), "r"(n), "r"(bar)
+          : "memory");
+      off += n;
+    }
+  }
+  __syncthreads();
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------
+// predictor blob views
+// ------------------------------------------------------------------------------
+struct TableView {
+  const int32_t* pax;
+  const int32_t* dax;
+  const int64_t* grid;
+  int np, nd;
+};
+
+__device__ __forceinline__ const tw_pred_desc* pset_desc(const char* pset, int id) {
+  return reinterpret_cast<const tw_pred_desc*>(pset + sizeof(tw_pset_header)) + id;
+}
+__device__ __forceinline__ int pset_ndesc(const char* pset) {
+  return reinterpret_cast<const tw_pset_header*>(pset)->n_desc;
+}
+__device__ __forceinline__ TableView table_view(const char* pset, const tw_pred_desc* d) {
+  TableView t;
+  const char* base = pset + d->table_off;
+  t.pax = reinterpret_cast<const int32_t*>(base);
+  t.dax = t.pax + d->np;
+  uint32_t goff = (uint32_t)(d->np + d->nd) * 4u;
+  goff = (goff + 7u) & ~7u;
+  t.grid = reinterpret_cast<const int64_t*>(base + goff);
+  t.np = d->np;
+  t.nd = d->nd;
+  return t;
+}
+
+// Python round(float) -> int (half to even), then us -> ns.
+__device__ __forceinline__ int64_t us_to_ns_rn(double us) { return __double2ll_rn(us) * 1000; }
+
+// lerp with exact-int operands: Python evaluates (b-a)*(x-lo) exactly and the
+// int/int true division correctly rounded; equal to one __ddiv_rn while |num| < 2^53
+// (the host rejects tables that could exceed it).
+__device__ __forceinline__ double lerp_int(int64_t a, int64_t b, int64_t lo, int64_t hi, int64_t x) {
+  const int64_t num = (b - a) * (x - lo);
+  const double q = __ddiv_rn(__ll2double_rn(num), __ll2double_rn(hi - lo));
+  return __dadd_rn(__ll2double_rn(a), q);
+}
+__device__ __forceinline__ double lerp_dbl(double a, double b, int64_t lo, int64_t hi, int64_t x) {
+  const double diff = __dsub_rn(b, a);
+  const double prod = __dmul_rn(diff, __ll2double_rn(x - lo));
+  return __dadd_rn(a, __ddiv_rn(prod, __ll2double_rn(hi - lo)));
+}
+
+// Bilinear evaluation once both axes are bracketed (indices into the axes).
+// Returns TW_PRED_TABLE_MISS (as a sentinel) when a corner is a hole.
+__device__ __forceinline__ int64_t table_corners(const TableView& t, int p0, int p1, int d0, int d1,
+                                                 int64_t P, int64_t D) {
+  const int64_t c00 = t.grid[p0 * t.nd + d0];
+  const int64_t c10 = t.grid[p1 * t.nd + d0];
+  const int64_t c01 = t.grid[p0 * t.nd + d1];
+  const int64_t c11 = t.grid[p1 * t.nd + d1];
+  if (c00 == TW_TABLE_HOLE || c10 == TW_TABLE_HOLE || c01 == TW_TABLE_HOLE || c11 == TW_TABLE_HOLE)
+    return TW_PRED_TABLE_MISS;
+  const int64_t P0 = t.pax[p0], P1 = t.pax[p1], D0 = t.dax[d0], D1 = t.dax[d1];
+  double us;
+  if (P1 == P0) {
+    // level-1 lerps return the int corners (predictor.py:229-230); an exact hit
+    // (predictor.py:213-215) is the P1==P0, D1==D0 case
+    us = (D1 == D0) ? __ll2double_rn(c00) : lerp_int(c00, c01, D0, D1, D);
+  } else {
+    const double at_d0 = lerp_int(c00, c10, P0, P1, P);
+    const double at_d1 = lerp_int(c01, c11, P0, P1, P);
+    us = (D1 == D0) ? at_d0 : lerp_dbl(at_d0, at_d1, D0, D1, D);
+  }
+  return us_to_ns_rn(us);
+}
+
+// scalar bracket: lo = index of max axis <= v, hi = index of min axis >= v
+__device__ __forceinline__ bool bracket_scalar(const int32_t* axis, int n, int64_t v, int& lo, int& hi) {
+  if (v < axis[0] || v > axis[n - 1]) return false;
+  int a = 0, b = n - 1;  // invariant: axis[a] <= v, answer in [a, b]
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (axis[m] <= v) a = m; else b = m - 1;
+  }
+  lo = a;
+  hi = (axis[a] == v) ? a : a + 1;
+  return true;
+}
+
+// manhattan-nearest row, ties -> smallest (p, d) (predictor.py:205-207); scalar
+__device__ __forceinline__ int64_t table_nearest_scalar(const TableView& t, int64_t P, int64_t D) {
+  int64_t best = INT64_MAX, bv = 0;
+  for (int i = 0; i < t.np; i++) {
+    const int64_t dp = llabs((int64_t)t.pax[i] - P);
+    if (dp > best) continue;  // rows further in p alone cannot win (p ascending)
+    for (int j = 0; j < t.nd; j++) {
+      const int64_t v = t.grid[i * t.nd + j];
+      if (v == TW_TABLE_HOLE) continue;
+      const int64_t dist = dp + llabs((int64_t)t.dax[j] - D);
+      if (dist < best) {  // strict: first in (p, d) order wins ties
+        best = dist;
+        bv = v;
+      }
+    }
+  }
+  return bv * 1000;
+}
+
+// One prediction, scalar (bulk kernel). Not for empty batches.
+__device__ __forceinline__ int64_t predict_scalar(const char* pset, int id, int64_t P, int64_t D,
+                                                  int64_t C) {
+  if (id < 0 || id >= pset_ndesc(pset)) return TW_PRED_BAD_DESC;
+  const tw_pred_desc* d = pset_desc(pset, id);
+  if (d->kind == TW_PRED_CONSTANT) return d->constant_us * 1000;
+  if (d->kind == TW_PRED_LINEAR) {
+    double us = __dadd_rn(d->base_us, __dmul_rn(d->per_prefill_token_us, __ll2double_rn(P)));
+    us = __dadd_rn(us, __dmul_rn(d->per_decode_us, __ll2double_rn(D)));
+    us = __dadd_rn(us, __dmul_rn(d->per_context_token_us, __ll2double_rn(C)));
+    const int64_t q = __double2ll_rn(us);
+    return q < 0 ? (int64_t)TW_PRED_NEGATIVE : q * 1000;
+  }
+  if (d->kind != TW_PRED_TABLE) return TW_PRED_BAD_DESC;
+  const TableView t = table_view(pset, d);
+  int p0, p1, d0, d1;
+  if (bracket_scalar(t.pax, t.np, P, p0, p1) && bracket_scalar(t.dax, t.nd, D, d0, d1)) {
+    const int64_t r = table_corners(t, p0, p1, d0, d1, P, D);
+    if (r != TW_PRED_TABLE_MISS) return r;
+  }
+  if (d->allow_extrapolation) return table_nearest_scalar(t, P, D);
+  return TW_PRED_TABLE_MISS;
+}
+
+// ------------------------------------------------------------------------------
+// warp-cooperative prediction (event loop): all lanes get the same answer
+// ------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t w = __shfl_xor_sync(kFull, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// lo/hi bracket with lanes comparing 32 axis entries at a time (one LDS + ballot).
+__device__ __forceinline__ bool bracket_warp(const int32_t* axis, int n, int64_t v, int& lo, int& hi) {
+  const int lane = threadIdx.x & 31;
+  if (v < axis[0] || v > axis[n - 1]) return false;
+  int cnt_le = 0;  // number of axis entries <= v  (axis sorted ascending)
+  bool eq = false;
+  for (int b = 0; b < n; b += 32) {
+    const int i = b + lane;
+    const int64_t a = (i < n) ? (int64_t)axis[i] : INT64_MAX;
+    cnt_le += __popc(__ballot_sync(kFull, a <= v));
+    eq |= __any_sync(kFull, a == v);
+    if (b + 32 < n && (int64_t)axis[b + 31] > v) break;
+  }
+  lo = cnt_le - 1;
+  hi = eq ? lo : lo + 1;
+  return true;
+}
+
+__device__ __forceinline__ int64_t table_nearest_warp(const TableView& t, int64_t P, int64_t D) {
+  const int lane = threadIdx.x & 31;
+  // each lane scans cells lane, lane+32, ...; key = (dist, p-index, d-index) which is
+  // the reference's (dist, (p, d)) order because the axes are sorted ascending
+  int64_t best = INT64_MAX, bkey = INT64_MAX, bv = 0;
+  const int cells = t.np * t.nd;
+  for (int c = lane; c < cells; c += 32) {
+    const int64_t v = t.grid[c];
+    if (v == TW_TABLE_HOLE) continue;
+    const int i = c / t.nd, j = c - i * t.nd;
+    const int64_t dist = llabs((int64_t)t.pax[i] - P) + llabs((int64_t)t.dax[j] - D);
+    if (dist < best || (dist == best && c < bkey)) {
+      best = dist;
+      bkey = c;
+      bv = v;
+    }
+  }
+  const int64_t mind = warp_min_i64(best);
+  const int64_t k = warp_min_i64(best == mind ? bkey : INT64_MAX);
+  const unsigned who = __ballot_sync(kFull, best == mind && bkey == k);
+  return __shfl_sync(kFull, bv, __ffs(who) - 1) * 1000;
+}
+
+// Warp-uniform prediction for a non-empty batch; every lane must call.
+__device__ __forceinline__ int64_t predict_warp(const char* pset, int id, int64_t P, int64_t D,
+                                                int64_t C) {
+  if (id < 0 || id >= pset_ndesc(pset)) return TW_PRED_BAD_DESC;
+  const tw_pred_desc* d = pset_desc(pset, id);
+  if (d->kind != TW_PRED_TABLE) return predict_scalar(pset, id, P, D, C);
+  const TableView t = table_view(pset, d);
+  int p0, p1, d0, d1;
+  if (bracket_warp(t.pax, t.np, P, p0, p1) && bracket_warp(t.dax, t.nd, D, d0, d1)) {
+    const int64_t r = table_corners(t, p0, p1, d0, d1, P, D);
+    if (r != TW_PRED_TABLE_MISS) return r;
+  }
+  if (d->allow_extrapolation) return table_nearest_warp(t, P, D);
+  return TW_PRED_TABLE_MISS;
+}
+
+// FakeClock.sleep(wait_ns / 1e9) -> int(round(seconds * 1e9)) (pkg/tests/_support.py:33-34)
+__device__ __forceinline__ int64_t fake_sleep_ns(int64_t wait_ns) {
+  const double seconds = __ddiv_rn(__ll2double_rn(wait_ns), 1e9);
+  return __double2ll_rn(__dmul_rn(seconds, 1e9));
+}
+
+}  // namespace twb

@@ -1,0 +1,157 @@
+// predict.cu — bulk duration predictor (north-star kernels 1 and 2).
+//
+//   tw_predict_features : (P, D, C, desc_id) -> int64 ns        28 B / prediction
+//   tw_predict_batches  : CSR slots -> features -> int64 ns     8 B/slot + 20 B/batch
+//
+// Reference: predictor.py:64-84 (features), 100-242 (predict). HBM-bound gather
+// work: the predictor blob (descriptors + calibration tables, a few KB) is staged
+// once per CTA into shared memory by one TMA bulk copy; the query streams are read
+// with 16-byte vector loads marked evict-first, each thread handling 4 queries per
+// iteration for memory-level parallelism; grid = a multiple of the 148 SMs.
+#include "common.cuh"
+
+namespace twb {
+
+constexpr int kPredThreads = 256;
+
+struct PsetSmem {
+  static __device__ __forceinline__ char* stage(const void* pset, uint32_t bytes) {
+    extern __shared__ __align__(128) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    char* blob = smem + 128;
+    tma_stage_to_smem(blob, pset, bytes, bar);
+    return blob;
+  }
+};
+
+__device__ __forceinline__ int64_t predict_one(const char* ps, int32_t p, int32_t d, int64_t c,
+                                               int32_t id) {
+  if (p == 0 && d == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
+  return predict_scalar(ps, id, p, d, c);
+}
+
+__global__ void __launch_bounds__(kPredThreads) k_predict_features(
+    const void* __restrict__ pset, uint32_t pset_bytes, const int32_t* __restrict__ P,
+    const int32_t* __restrict__ D, const int64_t* __restrict__ C, const int32_t* __restrict__ id,
+    int64_t n, int64_t* __restrict__ out) {
+  const char* ps = PsetSmem::stage(pset, pset_bytes);
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // vector body: groups of 4 consecutive queries (all arrays 16-B aligned by contract)
+  const int64_t n4 = n >> 2;
+  for (int64_t g = tid; g < n4; g += nthreads) {
+    const int4 p4 = __ldcs(reinterpret_cast<const int4*>(P) + g);
+    const int4 d4 = __ldcs(reinterpret_cast<const int4*>(D) + g);
+    const int4 i4 = __ldcs(reinterpret_cast<const int4*>(id) + g);
+    const longlong2 c01 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g);
+    const longlong2 c23 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g + 1);
+    longlong2 o01, o23;
+    o01.x = predict_one(ps, p4.x, d4.x, c01.x, i4.x);
+    o01.y = predict_one(ps, p4.y, d4.y, c01.y, i4.y);
+    o23.x = predict_one(ps, p4.z, d4.z, c23.x, i4.z);
+    o23.y = predict_one(ps, p4.w, d4.w, c23.y, i4.w);
+    __stcs(reinterpret_cast<longlong2*>(out) + 2 * g, o01);
+    __stcs(reinterpret_cast<longlong2*>(out) + 2 * g + 1, o23);
+  }
+  for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, P[i], D[i], C[i], id[i]);
+}
+
+// Fused extraction + prediction. One thread per batch; its slots are a contiguous
+// run (CSR), so a warp reads one contiguous region and L1 merges the sectors.
+__global__ void __launch_bounds__(kPredThreads) k_predict_batches(
+    const void* __restrict__ pset, uint32_t pset_bytes, const int64_t* __restrict__ off,
+    const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx, const int32_t* __restrict__ id,
+    int64_t nb, int64_t* __restrict__ feat, int64_t* __restrict__ out) {
+  const char* ps = PsetSmem::stage(pset, pset_bytes);
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += nthreads) {
+    const int64_t s0 = off[b], s1 = off[b + 1];
+    int64_t Pt = 0, Dn = 0, Ct = 0;
+    for (int64_t s = s0; s < s1; s++) {
+      const int32_t t = __ldg(tok + s);
+      const int32_t c = __ldg(ctx + s);
+      if (t >= 0) Pt += t; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+      Ct += c;
+    }
+    if (feat) {
+      feat[3 * b] = Pt;
+      feat[3 * b + 1] = Dn;
+      feat[3 * b + 2] = Ct;
+    }
+    out[b] = (s1 == s0) ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(ps, id[b], Pt, Dn, Ct);
+  }
+}
+
+static int pred_grid(int64_t work, size_t smem, const void* fn) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPredThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (work + kPredThreads - 1) / kPredThreads;
+  int64_t cap = (int64_t)sms * per_sm;  // one full wave, persistent grid-stride
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+static int check_pset(const void* pset, int64_t bytes, size_t* smem) {
+  if (!pset || bytes < (int64_t)sizeof(tw_pset_header) || (bytes & 15) ||
+      (reinterpret_cast<uintptr_t>(pset) & 15)) {
+    set_error("pset: null, misaligned or size %lld not a multiple of 16", (long long)bytes);
+    return TW_EINVAL;
+  }
+  *smem = 128 + (size_t)bytes;
+  if (*smem > 200 * 1024) {
+    set_error("pset blob of %lld bytes exceeds the shared-memory staging budget", (long long)bytes);
+    return TW_ENOSMEM;
+  }
+  return TW_OK;
+}
+
+}  // namespace twb
+
+using namespace twb;
+
+extern "C" int tw_predict_features(const void* pset, int64_t pset_bytes, const int32_t* P,
+                                   const int32_t* D, const int64_t* C, const int32_t* desc_id,
+                                   int64_t n, int64_t* out_ns, void* stream) {
+  size_t smem;
+  int rc = check_pset(pset, pset_bytes, &smem);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!P || !D || !C || !desc_id || !out_ns))) {
+    set_error("tw_predict_features: bad arrays");
+    return TW_EINVAL;
+  }
+  if (((uintptr_t)P | (uintptr_t)D | (uintptr_t)C | (uintptr_t)desc_id | (uintptr_t)out_ns) & 15) {
+    set_error("tw_predict_features: arrays must be 16-byte aligned");
+    return TW_EINVAL;
+  }
+  if (n == 0) return TW_OK;
+  cudaFuncSetAttribute(k_predict_features, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = pred_grid((n + 3) / 4, smem, (const void*)k_predict_features);
+  k_predict_features<<<grid, kPredThreads, smem, (cudaStream_t)stream>>>(
+      pset, (uint32_t)pset_bytes, P, D, C, desc_id, n, out_ns);
+  count_launch();
+  return check_launch("tw_predict_features");
+}
+
+extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batch_off,
+                                  const int32_t* slot_tok, const int32_t* slot_ctx,
+                                  const int32_t* desc_id, int64_t n_batches, int64_t* feat_out,
+                                  int64_t* out_ns, void* stream) {
+  size_t smem;
+  int rc = check_pset(pset, pset_bytes, &smem);
+  if (rc) return rc;
+  if (n_batches < 0 || (n_batches > 0 && (!batch_off || !desc_id || !out_ns))) {
+    set_error("tw_predict_batches: bad arrays");
+    return TW_EINVAL;
+  }
+  if (n_batches == 0) return TW_OK;
+  cudaFuncSetAttribute(k_predict_batches, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = pred_grid(n_batches, smem, (const void*)k_predict_batches);
+  k_predict_batches<<<grid, kPredThreads, smem, (cudaStream_t)stream>>>(
+      pset, (uint32_t)pset_bytes, batch_off, slot_tok, slot_ctx, desc_id, n_batches, feat_out, out_ns);
+  count_launch();
+  return check_launch("tw_predict_batches");
+}

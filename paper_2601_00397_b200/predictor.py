@@ -1,0 +1,451 @@
+"""Batch runtime predictors, B200 edition — drop-in for ``timewarp.predictor``.
+
+Mirrors the reference plugin surface (pkg/src/timewarp/predictor.py:27-266): the
+same class names, constructor arguments, ``from_csv`` loader, exception classes
+and the duck-typed ``predict(batch, hw=None) -> int ns`` method, so the reference's
+own ``oracle.simulate`` and ``EmulatedEngine`` accept these objects unchanged.
+``predict`` accepts any object with ``prefill_chunks`` (``chunk_tokens``,
+``context_len_before``) and ``decodes`` (``context_len``) — including the
+reference's own ``BatchComposition``.
+
+Every prediction is computed by libtwb200's sm_100a kernels (exact fp64, half-even
+microsecond rounding, int64 ns): ``predict`` launches one fused extraction+predict
+kernel for a single batch, ``predict_many`` / :func:`predict_features` run the bulk
+kernels over millions of batches. There is no Python arithmetic fallback.
+
+A :class:`PredictorSet` packs any number of predictors into the one contiguous
+blob the kernels stage into shared memory with a TMA bulk copy (twb200.h).
+"""
+
+from __future__ import annotations
+
+import csv
+import logging
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (
+    PRED_DESC_DTYPE,
+    PSET_HEADER_DTYPE,
+    TW_PRED_BAD_DESC,
+    TW_PRED_CONSTANT,
+    TW_PRED_EMPTY_BATCH,
+    TW_PRED_LINEAR,
+    TW_PRED_NEGATIVE,
+    TW_PRED_TABLE,
+    TW_PRED_TABLE_MISS,
+    TW_PSET_MAGIC,
+    TW_TABLE_HOLE,
+)
+
+log = logging.getLogger(__name__)
+
+NS_PER_US = 1_000
+
+
+class PredictorError(Exception):
+    pass
+
+
+class EmptyBatch(PredictorError):
+    """Prediction requested for a batch with no work in it."""
+
+
+class NegativeDuration(PredictorError):
+    """Model parameters produced a duration below zero."""
+
+
+class TableMiss(PredictorError):
+    """Lookup key outside the calibrated range with extrapolation disabled."""
+
+
+class TableParseError(PredictorError):
+    """Calibration file is malformed."""
+
+
+@dataclass(frozen=True)
+class PrefillChunk:
+    request_id: str
+    chunk_tokens: int
+    context_len_before: int
+
+
+@dataclass(frozen=True)
+class DecodeSlot:
+    request_id: str
+    context_len: int
+
+
+@dataclass(frozen=True)
+class BatchComposition:
+    prefill_chunks: tuple = ()
+    decodes: tuple = ()
+
+    @property
+    def total_prefill_tokens(self) -> int:
+        return sum(c.chunk_tokens for c in self.prefill_chunks)
+
+    @property
+    def num_decodes(self) -> int:
+        return len(self.decodes)
+
+    @property
+    def total_context(self) -> int:
+        return sum(c.context_len_before for c in self.prefill_chunks) + sum(
+            d.context_len for d in self.decodes
+        )
+
+    def is_empty(self) -> bool:
+        return not self.prefill_chunks and not self.decodes
+
+
+@dataclass(frozen=True)
+class HardwareSpec:
+    name: str = "default"
+    parameters: dict = field(default_factory=dict)
+
+
+def raise_for_code(code: int, context: str = "") -> None:
+    """Map a kernel's per-element code to the reference exception (predictor.py:27-44)."""
+    if code >= 0:
+        return
+    if code == TW_PRED_EMPTY_BATCH:
+        raise EmptyBatch("cannot predict a duration for an empty batch")
+    if code == TW_PRED_NEGATIVE:
+        raise NegativeDuration(f"model produced a negative duration{context}")
+    if code == TW_PRED_TABLE_MISS:
+        raise TableMiss(f"no calibration for {context or 'this batch'} and extrapolation is disabled")
+    if code == TW_PRED_BAD_DESC:
+        raise PredictorError("predictor descriptor out of range")
+    raise PredictorError(f"unknown prediction code {code}")
+
+
+# ---------------------------------------------------------------------------------
+# predictor objects
+# ---------------------------------------------------------------------------------
+
+
+class _DevicePredictor:
+    """Shared plumbing: a one-predictor PredictorSet and the predict entry points."""
+
+    _pset: "PredictorSet | None" = None
+
+    def _descriptor(self) -> np.void:  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def _table(self):
+        return None
+
+    @property
+    def predictor_set(self) -> "PredictorSet":
+        if self._pset is None:
+            self._pset = PredictorSet([self])
+        return self._pset
+
+    def predict(self, batch, hw: HardwareSpec | None = None) -> int:
+        """Returns the predicted step duration in nanoseconds (one GPU launch)."""
+        out = self.predictor_set.predict_batches([batch], [0])
+        code = int(out[0])
+        if code < 0:
+            raise_for_code(code, _describe(batch))
+        return code
+
+    def predict_many(self, batches: Sequence, raise_errors: bool = True) -> np.ndarray:
+        """Bulk prediction over many batch compositions in one launch."""
+        out = self.predictor_set.predict_batches(batches, np.zeros(len(batches), np.int32))
+        if raise_errors and len(out) and out.min() < 0:
+            i = int(np.argmin(out))
+            raise_for_code(int(out[i]), _describe(batches[i]))
+        return out
+
+
+def _describe(batch) -> str:
+    try:
+        p = sum(c.chunk_tokens for c in batch.prefill_chunks)
+        d = len(batch.decodes)
+        return f" prefill={p} decodes={d}"
+    except Exception:  # pragma: no cover
+        return ""
+
+
+class ConstantPredictor(_DevicePredictor):
+    """Every non-empty batch takes the same fixed duration (predictor.py:100-111)."""
+
+    def __init__(self, duration_us: int) -> None:
+        if duration_us < 0:
+            raise NegativeDuration(f"constant duration {duration_us}us is negative")
+        self.duration_us = int(duration_us)
+        self._pset = None
+
+    def _descriptor(self):
+        d = np.zeros((), PRED_DESC_DTYPE)
+        d["kind"] = TW_PRED_CONSTANT
+        d["constant_us"] = self.duration_us
+        return d
+
+
+class LinearPredictor(_DevicePredictor):
+    """Affine cost model (predictor.py:114-146), evaluated in exact fp64 on device."""
+
+    def __init__(
+        self,
+        base_us: float,
+        per_prefill_token_us: float = 0.0,
+        per_decode_us: float = 0.0,
+        per_context_token_us: float = 0.0,
+    ) -> None:
+        self.base_us = base_us
+        self.per_prefill_token_us = per_prefill_token_us
+        self.per_decode_us = per_decode_us
+        self.per_context_token_us = per_context_token_us
+        self._pset = None
+
+    def _descriptor(self):
+        d = np.zeros((), PRED_DESC_DTYPE)
+        d["kind"] = TW_PRED_LINEAR
+        d["base_us"] = float(self.base_us)
+        d["per_prefill_token_us"] = float(self.per_prefill_token_us)
+        d["per_decode_us"] = float(self.per_decode_us)
+        d["per_context_token_us"] = float(self.per_context_token_us)
+        return d
+
+
+class TablePredictor(_DevicePredictor):
+    """Calibration-table lookup over (total_prefill_tokens, num_decodes) (predictor.py:149-242).
+
+    On device the rows become a dense [prefill-axis x decode-axis] int64 grid with
+    holes, so bracketing is an axis search and the four corners are direct loads.
+    """
+
+    def __init__(self, rows: dict, allow_extrapolation: bool = False) -> None:
+        if not rows:
+            raise TableParseError("calibration table has no rows")
+        self._rows = {(int(p), int(d)): int(v) for (p, d), v in dict(rows).items()}
+        self._prefill_axis = sorted({p for p, _ in self._rows})
+        self._decode_axis = sorted({d for _, d in self._rows})
+        self.allow_extrapolation = allow_extrapolation
+        for (p, d), v in self._rows.items():
+            if not (-(2**31) <= p < 2**31 and -(2**31) <= d < 2**31):
+                raise TableParseError(f"table key {(p, d)} outside the int32 range of the device grid")
+            if v < 0:
+                # The reference only rejects negatives in from_csv; the device grid
+                # reserves negative values for holes and error codes.
+                raise NegativeDuration(f"table value {v}us at {(p, d)} is negative")
+        # exactness of the int lerp numerator on device: |(b-a)*(x-lo)| < 2^53
+        vals = list(self._rows.values())
+        span = max(vals) - min(vals)
+        gap = max(
+            [b - a for a, b in zip(self._prefill_axis, self._prefill_axis[1:])]
+            + [b - a for a, b in zip(self._decode_axis, self._decode_axis[1:])]
+            + [1]
+        )
+        if span * gap >= 2**53:
+            raise TableParseError("table values x axis gaps exceed the exact fp64 range (2^53)")
+        self._pset = None
+
+    @classmethod
+    def from_csv(cls, path: str, allow_extrapolation: bool = False) -> "TablePredictor":
+        """Load ``total_prefill_tokens,num_decodes,duration_us`` rows (predictor.py:167-192)."""
+        rows: dict = {}
+        with open(path, newline="") as fh:
+            reader = csv.DictReader(fh)
+            expected = {"total_prefill_tokens", "num_decodes", "duration_us"}
+            if reader.fieldnames is None or not expected.issubset(reader.fieldnames):
+                raise TableParseError(
+                    f"{path}: header must contain {sorted(expected)}, got {reader.fieldnames}"
+                )
+            for lineno, row in enumerate(reader, start=2):
+                try:
+                    key = (int(row["total_prefill_tokens"]), int(row["num_decodes"]))
+                    duration = int(row["duration_us"])
+                except (TypeError, ValueError) as exc:
+                    raise TableParseError(f"{path}:{lineno}: {exc}") from None
+                if duration < 0:
+                    raise NegativeDuration(f"{path}:{lineno}: duration {duration}us is negative")
+                if key in rows:
+                    log.warning("calibration table %s: duplicate key %s, keeping last", path, key)
+                rows[key] = duration
+        return cls(rows, allow_extrapolation=allow_extrapolation)
+
+    def _descriptor(self):
+        d = np.zeros((), PRED_DESC_DTYPE)
+        d["kind"] = TW_PRED_TABLE
+        d["allow_extrapolation"] = int(bool(self.allow_extrapolation))
+        d["np"] = len(self._prefill_axis)
+        d["nd"] = len(self._decode_axis)
+        return d
+
+    def _table(self):
+        pax = np.asarray(self._prefill_axis, np.int32)
+        dax = np.asarray(self._decode_axis, np.int32)
+        grid = np.full((len(pax), len(dax)), TW_TABLE_HOLE, np.int64)
+        pi = {p: i for i, p in enumerate(self._prefill_axis)}
+        di = {d: i for i, d in enumerate(self._decode_axis)}
+        for (p, d), v in self._rows.items():
+            grid[pi[p], di[d]] = v
+        return pax, dax, grid
+
+
+def build_predictor(config: dict):
+    """Construct a predictor from its config document (predictor.py:245-266)."""
+    kind = config.get("kind")
+    if kind == "constant":
+        return ConstantPredictor(duration_us=config["duration_us"])
+    if kind == "linear":
+        return LinearPredictor(
+            base_us=config.get("base_us", 0.0),
+            per_prefill_token_us=config.get("per_prefill_token_us", 0.0),
+            per_decode_us=config.get("per_decode_us", 0.0),
+            per_context_token_us=config.get("per_context_token_us", 0.0),
+        )
+    if kind == "table":
+        return TablePredictor.from_csv(
+            config["path"], allow_extrapolation=config.get("allow_extrapolation", False)
+        )
+    raise PredictorError(f"unknown predictor kind {kind!r}")
+
+
+# ---------------------------------------------------------------------------------
+# predictor set blob + bulk entry points
+# ---------------------------------------------------------------------------------
+
+
+def _align(n: int, a: int) -> int:
+    return (n + a - 1) // a * a
+
+
+class PredictorSet:
+    """Many predictors packed into one device blob (layout: include/twb200.h)."""
+
+    def __init__(self, predictors: Iterable) -> None:
+        self.predictors = list(predictors)
+        if not self.predictors:
+            raise PredictorError("a predictor set needs at least one predictor")
+        n = len(self.predictors)
+        descs = np.zeros(n, PRED_DESC_DTYPE)
+        pool: list[bytes] = []
+        off = _align(PSET_HEADER_DTYPE.itemsize + n * PRED_DESC_DTYPE.itemsize, 16)
+        cursor = off
+        for i, p in enumerate(self.predictors):
+            descs[i] = p._descriptor()
+            tab = p._table()
+            if tab is not None:
+                pax, dax, grid = tab
+                axes = pax.tobytes() + dax.tobytes()
+                axes += b"\0" * (_align(len(axes), 8) - len(axes))
+                blob = axes + grid.tobytes()
+                blob += b"\0" * (_align(len(blob), 16) - len(blob))
+                descs[i]["table_off"] = cursor
+                pool.append(blob)
+                cursor += len(blob)
+        total = _align(cursor, 16)
+        hdr = np.zeros((), PSET_HEADER_DTYPE)
+        hdr["magic"] = TW_PSET_MAGIC
+        hdr["version"] = 1
+        hdr["n_desc"] = n
+        hdr["total_bytes"] = total
+        buf = bytearray(total)
+        buf[0:16] = hdr.tobytes()
+        buf[16 : 16 + descs.nbytes] = descs.tobytes()
+        pos = off
+        for blob in pool:
+            buf[pos : pos + len(blob)] = blob
+            pos += len(blob)
+        self.blob = np.frombuffer(bytes(buf), np.uint8)
+        self._dev: dict = {}
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.blob.size)
+
+    def device_blob(self, device=None):
+        from ._device import require_cuda, to_device
+
+        dev = require_cuda(device)
+        key = str(dev)
+        if key not in self._dev:
+            self._dev[key] = to_device(self.blob, dev)
+        return self._dev[key]
+
+    # -- bulk features -> ns --------------------------------------------------------
+    def predict_features(self, P, D, C, desc_id, device=None, stream=None):
+        """out[i] = ns for features (P, D, C) with descriptor desc_id (torch or numpy in).
+
+        Empty batches are encoded as P == D == 0 and C < 0 (twb200.h). Returns a CUDA
+        int64 tensor when given CUDA tensors, else a numpy array.
+        """
+        import torch
+
+        from ._device import require_cuda, stream_handle
+
+        dev = require_cuda(device)
+        host = not isinstance(P, torch.Tensor)
+
+        def dv(x, dt):
+            if isinstance(x, torch.Tensor):
+                return x.to(device=dev, dtype=dt).contiguous()
+            return torch.as_tensor(np.ascontiguousarray(x)).to(device=dev, dtype=dt)
+
+        Pt, Dt, Ct = dv(P, torch.int32), dv(D, torch.int32), dv(C, torch.int64)
+        It = dv(desc_id, torch.int32)
+        n = Pt.numel()
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+        blob = self.device_blob(dev)
+        rc = _lib.load().tw_predict_features(
+            blob.data_ptr(), self.nbytes, Pt.data_ptr(), Dt.data_ptr(), Ct.data_ptr(),
+            It.data_ptr(), n, out.data_ptr(), stream_handle(stream),
+        )
+        _lib.check(rc, "tw_predict_features")
+        return out.cpu().numpy() if host else out
+
+    # -- CSR batches -> features -> ns ------------------------------------------------
+    def predict_batches(self, batches: Sequence, desc_id, device=None, return_features=False):
+        """Fused feature extraction + prediction for reference-style batch objects."""
+        import torch
+
+        from ._device import require_cuda, stream_handle
+
+        dev = require_cuda(device)
+        off, tok, ctx = pack_batches(batches)
+        nb = len(batches)
+        t_off = torch.from_numpy(off).to(dev)
+        t_tok = torch.from_numpy(tok).to(dev)
+        t_ctx = torch.from_numpy(ctx).to(dev)
+        t_id = torch.as_tensor(np.ascontiguousarray(desc_id, np.int32)).to(dev)
+        out = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
+        feat = torch.empty(max(3 * nb, 3), dtype=torch.int64, device=dev) if return_features else None
+        blob = self.device_blob(dev)
+        rc = _lib.load().tw_predict_batches(
+            blob.data_ptr(), self.nbytes, t_off.data_ptr(), t_tok.data_ptr(), t_ctx.data_ptr(),
+            t_id.data_ptr(), nb, feat.data_ptr() if feat is not None else None, out.data_ptr(),
+            stream_handle(),
+        )
+        _lib.check(rc, "tw_predict_batches")
+        res = out[:nb].cpu().numpy()
+        if return_features:
+            return res, feat[: 3 * nb].cpu().numpy().reshape(nb, 3)
+        return res
+
+
+def pack_batches(batches: Sequence):
+    """Reference-style batches -> CSR (offsets int64, slot tokens int32, slot ctx int32).
+
+    Slot tokens: chunk_tokens for a PrefillChunk, -1 for a DecodeSlot (twb200.h).
+    """
+    off = np.zeros(len(batches) + 1, np.int64)
+    toks: list[int] = []
+    ctxs: list[int] = []
+    for i, b in enumerate(batches):
+        for c in b.prefill_chunks:
+            toks.append(int(c.chunk_tokens))
+            ctxs.append(int(c.context_len_before))
+        for d in b.decodes:
+            toks.append(-1)
+            ctxs.append(int(d.context_len))
+        off[i + 1] = len(toks)
+    tok = np.asarray(toks if toks else [0], np.int32)
+    ctx = np.asarray(ctxs if ctxs else [0], np.int32)
+    return off, tok, ctx

@@ -1,0 +1,362 @@
+"""Bulk emulation of many serving configurations — the B200 event loop's host side.
+
+Mirrors the reference's event-loop interfaces (pkg/src/timewarp/oracle.py:49-54 and
+pkg/src/timewarp/engine.py:46-133):
+
+* :func:`simulate` is a drop-in for ``timewarp.oracle.simulate``: same arguments,
+  same ``[{"request_id", "kind", "virtual_ts_ns", "step"}]`` result, raises
+  :class:`OracleStalled` on a stall — but the loop runs in libtwb200's sm_100a
+  kernel (one warp, full event dump).
+* :func:`simulate_many` / :class:`DeviceSweep` run thousands of configs in one
+  persistent launch and return fixed-size per-config records (steps, virtual span,
+  event digest, Timekeeper state, status) plus optional per-request FIRST_TOKEN /
+  FINISHED stamps and audited full event streams.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (
+    EVENT_DTYPE,
+    EVENT_KIND_NAMES,
+    SIM_CFG_DTYPE,
+    SIM_RESULT_DTYPE,
+    TW_SIM_BAD_CONFIG,
+    TW_SIM_CAPACITY,
+    TW_SIM_OK,
+    TW_SIM_OVERFLOW_BIT,
+    TW_SIM_PRED_ERROR,
+    TW_SIM_STALLED_ACTIVE,
+    TW_SIM_STALLED_KV,
+    TW_SIM_TIMEKEEPER,
+)
+from .predictor import (
+    ConstantPredictor,
+    LinearPredictor,
+    PredictorSet,
+    TablePredictor,
+    raise_for_code,
+)
+from .workload import PackedWorkloads, pack_arrivals
+
+DEFAULT_COOLDOWN_NS = 500_000  # timekeeper.py:36 (DEFAULT_COOLDOWN_US * NS_PER_US)
+
+
+class SchedulingPolicy(enum.Enum):
+    MIXED = "mixed"
+    PREFILL_PRIORITIZED = "prefill_prioritized"
+
+
+class EngineError(Exception):
+    pass
+
+
+class OracleStalled(Exception):
+    """The simulated engine can never make progress again (oracle.py:26-27)."""
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Same fields, defaults and validation as engine.py:98-133."""
+
+    chunk_size: int = 512
+    policy: SchedulingPolicy = SchedulingPolicy.MIXED
+    max_batch_tokens: int = 512
+    max_running: int = 256
+    kv_block_tokens: int = 16
+    kv_capacity_blocks: int = 4096
+    workers_per_replica: int = 1
+    pp_stages: int = 1
+
+    def __post_init__(self) -> None:
+        if self.chunk_size < 1:
+            raise ValueError(f"chunk_size must be >= 1, got {self.chunk_size}")
+        if self.max_batch_tokens < self.chunk_size:
+            raise ValueError(
+                f"max_batch_tokens ({self.max_batch_tokens}) must be >= chunk_size ({self.chunk_size})"
+            )
+        if self.kv_block_tokens < 1 or self.kv_capacity_blocks < 1:
+            raise ValueError("KV geometry must be positive")
+        if self.workers_per_replica < 1 or self.pp_stages < 1:
+            raise ValueError("worker grid dimensions must be >= 1")
+
+    @classmethod
+    def from_doc(cls, doc: dict) -> "EngineConfig":
+        return cls(
+            chunk_size=int(doc.get("chunk_size", 512)),
+            policy=SchedulingPolicy(doc.get("policy", "mixed")),
+            max_batch_tokens=int(doc.get("max_batch_tokens", 512)),
+            max_running=int(doc.get("max_running", 256)),
+            kv_block_tokens=int(doc.get("kv_block_tokens", 16)),
+            kv_capacity_blocks=int(doc.get("kv_capacity_blocks", 4096)),
+            workers_per_replica=int(doc.get("workers_per_replica", 1)),
+            pp_stages=int(doc.get("pp_stages", 1)),
+        )
+
+
+def _policy_code(policy) -> int:
+    value = getattr(policy, "value", policy)
+    if value == "mixed":
+        return _lib.TW_POLICY_MIXED
+    if value == "prefill_prioritized":
+        return _lib.TW_POLICY_PREFILL_PRIORITIZED
+    raise ValueError(f"unknown scheduling policy {policy!r}")
+
+
+@dataclass
+class SweepConfig:
+    """One emulated configuration: engine knobs + which predictor and workload it uses."""
+
+    engine: object  # EngineConfig (ours or the reference's: duck-typed)
+    pred_id: int = 0
+    workload_id: int = 0
+    epoch_ns: int = 0
+    timekeeper: bool = True
+    tk_cooldown_ns: int = DEFAULT_COOLDOWN_NS
+    label: dict = field(default_factory=dict)
+
+
+def config_array(configs: Sequence[SweepConfig]) -> np.ndarray:
+    a = np.zeros(len(configs), SIM_CFG_DTYPE)
+    for i, c in enumerate(configs):
+        e = c.engine
+        a[i]["chunk_size"] = e.chunk_size
+        a[i]["max_batch_tokens"] = e.max_batch_tokens
+        a[i]["max_running"] = e.max_running
+        a[i]["kv_block_tokens"] = e.kv_block_tokens
+        a[i]["kv_capacity_blocks"] = e.kv_capacity_blocks
+        a[i]["workers_per_replica"] = e.workers_per_replica
+        a[i]["pp_stages"] = e.pp_stages
+        a[i]["policy"] = _policy_code(e.policy)
+        a[i]["pred_id"] = c.pred_id
+        a[i]["workload_id"] = c.workload_id
+        a[i]["epoch_ns"] = c.epoch_ns
+        a[i]["tk_cooldown_ns"] = c.tk_cooldown_ns
+        a[i]["flags"] = TW_SIM_TIMEKEEPER if c.timekeeper else 0
+    return a
+
+
+def as_device_predictor(p):
+    """Accept our predictors or the reference's (duck-typed by their attributes)."""
+    if isinstance(p, (ConstantPredictor, LinearPredictor, TablePredictor)):
+        return p
+    if hasattr(p, "_rows") and hasattr(p, "allow_extrapolation"):
+        return TablePredictor(p._rows, allow_extrapolation=p.allow_extrapolation)
+    if hasattr(p, "per_prefill_token_us"):
+        return LinearPredictor(p.base_us, p.per_prefill_token_us, p.per_decode_us, p.per_context_token_us)
+    if hasattr(p, "duration_us"):
+        return ConstantPredictor(p.duration_us)
+    raise TypeError(f"cannot run predictor {type(p).__name__} on the B200 engine")
+
+
+def estimate_cost(pset: PredictorSet, cfgs: np.ndarray, wl: PackedWorkloads) -> np.ndarray:
+    """Rough relative cost (~ steps) per config, for largest-first scheduling."""
+    tokens = np.zeros(wl.n_workloads, np.float64)
+    for w in range(wl.n_workloads):
+        lo, hi = int(wl.wl_off[w]), int(wl.wl_off[w + 1])
+        tokens[w] = float(wl.output[lo:hi].sum()) + 1.0
+    step_us = np.ones(len(pset.predictors))
+    for i, p in enumerate(pset.predictors):
+        if isinstance(p, ConstantPredictor):
+            step_us[i] = max(p.duration_us, 1)
+        elif isinstance(p, LinearPredictor):
+            step_us[i] = max(abs(p.base_us) + abs(p.per_decode_us), 1.0)
+        else:
+            vals = list(p._rows.values())
+            step_us[i] = max(min(vals), 1)
+    pid = np.clip(cfgs["pred_id"], 0, len(step_us) - 1)
+    return tokens[cfgs["workload_id"]] / np.sqrt(step_us[pid])
+
+
+@dataclass
+class SweepResult:
+    results: np.ndarray  # SIM_RESULT_DTYPE per config
+    first_ns: np.ndarray | None = None  # int64 per (config, request) at req_base[c] + i
+    finish_ns: np.ndarray | None = None
+    req_base: np.ndarray | None = None
+    events: dict = field(default_factory=dict)  # config -> EVENT_DTYPE array (audited)
+    kernel_ms: float | None = None
+
+    @property
+    def predictions(self) -> int:
+        return int(self.results["steps"].sum())
+
+    def virtual_seconds(self, epochs: np.ndarray | None = None) -> float:
+        """Sum over configs of (last FINISHED ts - epoch) (metrics.py:245)."""
+        end = self.results["final_now_ns"].astype(np.float64)
+        if epochs is not None:
+            end = end - epochs.astype(np.float64)
+        return float(end.sum()) / 1e9
+
+    def ok(self) -> np.ndarray:
+        return self.results["status"] == TW_SIM_OK
+
+
+class DeviceSweep:
+    """All inputs and outputs of a sweep resident in HBM; ``run()`` is one launch."""
+
+    def __init__(
+        self,
+        pset: PredictorSet,
+        workloads: PackedWorkloads,
+        cfgs: np.ndarray,
+        device=None,
+        per_request: bool = True,
+        audit: Sequence[int] = (),
+        order: np.ndarray | None = None,
+    ) -> None:
+        import torch
+
+        from ._device import require_cuda, to_device
+
+        self.device = require_cuda(device)
+        self.pset = pset
+        self.workloads = workloads
+        self.cfgs = np.ascontiguousarray(cfgs)
+        self.n_cfg = len(cfgs)
+        if order is None:
+            order = np.argsort(-estimate_cost(pset, self.cfgs, workloads), kind="stable").astype(np.int32)
+        self.order = np.ascontiguousarray(order, np.int32)
+        sizes = workloads.sizes()[self.cfgs["workload_id"]] if self.n_cfg else np.zeros(0, np.int64)
+        self.req_base = np.zeros(self.n_cfg + 1, np.int64)
+        np.cumsum(sizes, out=self.req_base[1:])
+        self.slot_capacity = int(max(32, int(self.cfgs["max_running"].max()) if self.n_cfg else 32))
+        self.slot_capacity = min(self.slot_capacity, 4096)
+        dev = self.device
+        self.d_pset = pset.device_blob(dev)
+        self.d_cfgs = to_device(self.cfgs, dev)
+        self.d_order = to_device(self.order, dev)
+        self.d_wl_off = to_device(workloads.wl_off, dev)
+        self.d_ts = to_device(workloads.offset_ns, dev)
+        self.d_prompt = to_device(workloads.prompt, dev)
+        self.d_output = to_device(workloads.output, dev)
+        self.d_res = torch.zeros(self.n_cfg * SIM_RESULT_DTYPE.itemsize + 16, dtype=torch.uint8, device=dev)
+        self.d_scratch = torch.zeros(64, dtype=torch.uint8, device=dev)
+        total_req = int(self.req_base[-1])
+        self.per_request = per_request
+        if per_request:
+            self.d_req_base = to_device(self.req_base, dev)
+            self.d_first = torch.full((max(total_req, 1),), -1, dtype=torch.int64, device=dev)
+            self.d_finish = torch.full((max(total_req, 1),), -1, dtype=torch.int64, device=dev)
+        else:
+            self.d_req_base = self.d_first = self.d_finish = None
+        self.audit = [int(c) for c in audit]
+        if self.audit:
+            caps = np.zeros(self.n_cfg, np.int64)
+            for c in self.audit:
+                lo, hi = workloads.wl_off[self.cfgs[c]["workload_id"]], workloads.wl_off[self.cfgs[c]["workload_id"] + 1]
+                caps[c] = int(workloads.output[lo:hi].astype(np.int64).sum() + (hi - lo))  # output+1 per request
+            self.ev_off = np.zeros(self.n_cfg + 1, np.int64)
+            np.cumsum(caps, out=self.ev_off[1:])
+            self.d_ev_off = to_device(self.ev_off, dev)
+            self.d_ev = torch.zeros(max(int(self.ev_off[-1]), 1) * EVENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        else:
+            self.ev_off = None
+            self.d_ev_off = self.d_ev = None
+
+    @property
+    def h2d_bytes(self) -> int:
+        n = self.pset.nbytes + self.cfgs.nbytes + self.order.nbytes + self.workloads.nbytes
+        if self.per_request:
+            n += self.req_base.nbytes
+        return int(n)
+
+    def run(self, stream=None) -> None:
+        from ._device import ptr, stream_handle
+
+        rc = _lib.load().tw_sim_many(
+            self.d_pset.data_ptr(), self.pset.nbytes, self.d_cfgs.data_ptr(), self.n_cfg,
+            self.d_order.data_ptr(), self.d_wl_off.data_ptr(), self.d_ts.data_ptr(),
+            self.d_prompt.data_ptr(), self.d_output.data_ptr(), self.d_res.data_ptr(),
+            ptr(self.d_req_base), ptr(self.d_first), ptr(self.d_finish), ptr(self.d_ev_off),
+            ptr(self.d_ev), self.slot_capacity, self.d_scratch.data_ptr(), stream_handle(stream),
+        )
+        _lib.check(rc, "tw_sim_many")
+
+    def fetch(self) -> SweepResult:
+        from ._device import to_numpy_struct
+
+        res = to_numpy_struct(self.d_res, SIM_RESULT_DTYPE, self.n_cfg)
+        out = SweepResult(results=res, req_base=self.req_base)
+        if self.per_request:
+            n = int(self.req_base[-1])
+            out.first_ns = self.d_first[:n].cpu().numpy()
+            out.finish_ns = self.d_finish[:n].cpu().numpy()
+        if self.audit:
+            evs = to_numpy_struct(self.d_ev, EVENT_DTYPE, int(self.ev_off[-1]))
+            for c in self.audit:
+                k = min(int(res[c]["events"]), int(self.ev_off[c + 1] - self.ev_off[c]))
+                out.events[c] = evs[self.ev_off[c] : self.ev_off[c] + k]
+        return out
+
+
+def simulate_many(
+    workloads,
+    configs: Sequence[SweepConfig],
+    predictors,
+    audit: Sequence[int] = (),
+    per_request: bool = True,
+    device=None,
+) -> SweepResult:
+    """Run every config's event loop on the GPU (one persistent launch).
+
+    workloads: PackedWorkloads or a list of Arrival lists; predictors: a PredictorSet
+    or a list of predictor objects (indexed by SweepConfig.pred_id).
+    """
+    import torch
+
+    wl = workloads if isinstance(workloads, PackedWorkloads) else pack_arrivals(workloads)
+    pset = predictors if isinstance(predictors, PredictorSet) else PredictorSet(
+        [as_device_predictor(p) for p in predictors]
+    )
+    sweep = DeviceSweep(pset, wl, config_array(configs), device=device, per_request=per_request, audit=audit)
+    sweep.run()
+    torch.cuda.synchronize(sweep.device)
+    return sweep.fetch()
+
+
+def _raise_status(res, what: str = "") -> None:
+    st = int(res["status"]) & ~TW_SIM_OVERFLOW_BIT
+    if st == TW_SIM_OK:
+        return
+    if st == TW_SIM_STALLED_ACTIVE:
+        raise OracleStalled(f"{what}active requests with no schedulable work: KV pool cannot cover the in-flight set")
+    if st == TW_SIM_STALLED_KV:
+        raise OracleStalled(f"{what}queue head needs more KV blocks than the pool holds")
+    if st == TW_SIM_PRED_ERROR:
+        raise_for_code(int(res["pred_code"]))
+    if st == TW_SIM_BAD_CONFIG:
+        raise ValueError(f"{what}invalid engine config")
+    if st == TW_SIM_CAPACITY:
+        raise EngineError(f"{what}config exceeds the engine's slot or actor capacity")
+    raise EngineError(f"{what}simulation status {st}")
+
+
+def events_to_docs(ev: np.ndarray, request_ids: Sequence[str]) -> list[dict]:
+    rk = ev["req_kind"].astype(np.int64)
+    req = rk >> 2
+    kind = rk & 3
+    return [
+        {
+            "request_id": request_ids[int(r)],
+            "kind": EVENT_KIND_NAMES[int(k)],
+            "virtual_ts_ns": int(t),
+            "step": int(s),
+        }
+        for r, k, t, s in zip(req, kind, ev["ts_ns"], ev["step"])
+    ]
+
+
+def simulate(arrivals, cfg, predictor, epoch_ns: int = 0) -> list[dict]:
+    """Drop-in for ``timewarp.oracle.simulate`` (oracle.py:49-114), run on the GPU."""
+    wl = pack_arrivals([arrivals])
+    sc = SweepConfig(engine=cfg, pred_id=0, workload_id=0, epoch_ns=epoch_ns, timekeeper=False)
+    out = simulate_many(wl, [sc], [predictor], audit=[0], per_request=False)
+    _raise_status(out.results[0])
+    return events_to_docs(out.events[0], wl.request_ids[0])

@@ -1,0 +1,117 @@
+"""Loaders for the golden fixtures (tests/golden/*, produced by make_golden.py from
+the reference implementation) and builders of the matching engine inputs."""
+
+from __future__ import annotations
+
+import functools
+import json
+import os
+
+import numpy as np
+
+from paper_2601_00397_b200 import calibration
+from paper_2601_00397_b200._lib import SIM_CFG_DTYPE, TK_OP_DTYPE, TW_SIM_TIMEKEEPER
+from paper_2601_00397_b200.predictor import (
+    ConstantPredictor,
+    LinearPredictor,
+    PredictorSet,
+    TablePredictor,
+)
+from paper_2601_00397_b200.sweep import EngineConfig, SweepConfig, config_array
+from paper_2601_00397_b200.workload import Arrival, WorkloadSpec, generate_arrivals, pack_arrivals
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _npz(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+@functools.lru_cache(maxsize=None)
+def predictor_golden():
+    z = _npz("predictor.npz")
+    specs = json.loads(bytes(z["specs"]).decode())
+    preds = [predictor_from_spec(s) for s in specs]
+    return specs, preds, z["P"], z["D"], z["C"], z["desc"], z["expected"]
+
+
+def predictor_from_spec(s):
+    if s["kind"] == "constant":
+        return ConstantPredictor(s["us"])
+    if s["kind"] == "linear":
+        return LinearPredictor(*s["coef"])
+    if "rows" in s:
+        return TablePredictor({(p, d): v for p, d, v in s["rows"]}, allow_extrapolation=s["ext"])
+    return TablePredictor.from_csv(calibration.csv_path(*s["table"]), allow_extrapolation=s.get("ext", True))
+
+
+@functools.lru_cache(maxsize=None)
+def barrier_golden():
+    z = _npz("barrier.npz")
+    ops = z["ops"].view(TK_OP_DTYPE)
+    return {k: z[k] for k in z.files if k != "ops"} | {"ops": ops}
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_golden():
+    z = _npz("oracle.npz")
+    cases = json.loads(bytes(z["cases"]).decode())
+    return cases, z["events"], z["ev_off"]
+
+
+SWEEP_WORKLOAD = {
+    "source": "poisson", "qps": 8, "seed": 1, "num_requests": 1000,
+    "prompt_tokens": {"kind": "uniform", "low": 64, "high": 2048},
+    "output_tokens": {"kind": "uniform", "low": 16, "high": 256},
+}
+
+
+@functools.lru_cache(maxsize=None)
+def workload_for(n: int, first: tuple):
+    """Regenerate a full-size golden workload (pinned by arrivals.json)."""
+    cands = [dict(SWEEP_WORKLOAD), dict(SWEEP_WORKLOAD, qps=4, num_requests=10000)]
+    for doc in cands:
+        if doc["num_requests"] != n:
+            continue
+        arr = generate_arrivals(WorkloadSpec.from_doc(doc))
+        if (arr[0].offset_ns, arr[0].prompt_tokens, arr[0].output_tokens) == tuple(first):
+            return arr
+    raise KeyError((n, first))
+
+
+def case_inputs(case, timekeeper=False):
+    """(PredictorSet, PackedWorkloads, cfg array[1]) for one oracle.npz case."""
+    if case["arrivals"] is not None:
+        arr = [Arrival(r, o, p, q) for r, o, p, q in case["arrivals"]]
+    else:
+        arr = workload_for(case["workload"]["n"], tuple(case["workload"]["first"]))
+    eng = EngineConfig.from_doc(case["engine"])
+    pset = PredictorSet([predictor_from_spec(case["pred"])])
+    wl = pack_arrivals([arr])
+    cfgs = config_array([SweepConfig(engine=eng, epoch_ns=case["epoch"], timekeeper=timekeeper)])
+    return pset, wl, cfgs
+
+
+def case_events(case, events, ev_off):
+    i = case["ev_index"]
+    return events[ev_off[i] : ev_off[i + 1]]
+
+
+@functools.lru_cache(maxsize=None)
+def tkgrid_golden():
+    with open(os.path.join(GOLDEN, "tkgrid.json")) as fh:
+        return json.load(fh)
+
+
+def tk_case_inputs(case):
+    doc = {"source": "poisson", "qps": 20, "seed": 5, "num_requests": 120,
+           "prompt_tokens": {"kind": "uniform", "low": 16, "high": 900},
+           "output_tokens": {"kind": "uniform", "low": 1, "high": 60}} if case["seed"] == 5 else SWEEP_WORKLOAD
+    arr = generate_arrivals(WorkloadSpec.from_doc(doc))
+    eng = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
+                       kv_capacity_blocks=32768, workers_per_replica=case["tp"], pp_stages=case["pp"])
+    pset = PredictorSet([TablePredictor.from_csv(calibration.csv_path(case["model"], case["tp"], case["pp"]),
+                                                 allow_extrapolation=True)])
+    cfgs = config_array([SweepConfig(engine=eng, epoch_ns=case["epoch"], timekeeper=True,
+                                     tk_cooldown_ns=case["cooldown"])])
+    return pset, pack_arrivals([arr]), cfgs
