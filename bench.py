@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark: emulated virtual-seconds per wall-second over a config sweep on B200.
+
+Metric (BASELINE.json): "emulated virtual-sec/wall-sec over config sweep; batch
+predictions/sec @1/2/4/8 GPU". One step = one pass of the hot path over one batch
+of synthetic input = the full event loop (oracle.simulate semantics + Timekeeper
+actor grid) of every config in the sweep, in one persistent tw_sim_many launch.
+
+Workload per rank (weak scaling): BASELINE config 4 — the 1,024-config grid
+(max_batch_tokens x chunk x max_running x (TP,PP) x policy) on Llama-3-8B tables,
+1,000 Poisson requests (qps 8); rank r uses workload seed 1 + r. `--sweep 65536`
+runs config 5 instead (65,536 configs sharded over the ranks, strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+value  = sum over all ranks' configs of virtual span / max-over-ranks device time
+e2e    = the same through the public host API (pinned host inputs -> H2D -> kernel ->
+         D2H of result records and per-request stamps), timed with CUDA events
+roofline / predictor_roofline / cpu_baseline: see DESIGN.md §Measurement.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2, written between timed iterations
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--sweep", choices=("1024", "65536"), default="1024")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_workload(args, world, rank):
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.distributed import partition
+    from paper_2601_00397_b200.sweep import estimate_cost
+
+    if args.sweep == "1024":
+        sw = presets.sweep_1024(model="8b", seed=1 + rank)
+        config = {"workload": "BASELINE config 4: 1,024-config sweep per GPU (weak scaling)",
+                  "model": "Llama-3-8B calibration tables (synthetic)", "configs_per_gpu": len(sw),
+                  "requests_per_config": 1000, "qps": 8, "workload_seed": f"1 + rank",
+                  "grid": "mbt{1024..8192} x chunk{128..1024} x max_running{32..256} x (TP,PP) x 8 x policy x 2",
+                  "timekeeper": "dispatcher + TP*PP workers, cooldown 500us", "parallelism": f"configs sharded, dp{world}",
+                  "l2": "flushed (512 MiB write) between timed iterations"}
+        return sw, config, "weak"
+    full = presets.sweep_65536()
+    shards = partition(estimate_cost(full.pset, full.cfgs, full.workloads), world)
+    sw = full.subset(shards[rank])
+    config = {"workload": "BASELINE config 5: 65,536-config sweep sharded over GPUs (strong scaling)",
+              "model": "Llama-3-8B/70B calibration tables (synthetic)", "configs_total": len(full),
+              "configs_this_rank": len(sw), "parallelism": f"configs sharded, dp{world}",
+              "l2": "flushed (512 MiB write) between timed iterations"}
+    return sw, config, "strong"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def flush_l2(buf):
+    buf.fill_(1)  # a plain write larger than L2
+
+
+def time_kernel_steps(run, steps, warmup, flush_buf, stream):
+    """Per-step CUDA-event durations of `run()` on `stream`, L2 flushed before each."""
+    import torch
+
+    for _ in range(warmup):
+        flush_l2(flush_buf)
+        run()
+    torch.cuda.synchronize()
+    durs = []
+    for _ in range(steps):
+        flush_l2(flush_buf)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        b.synchronize()
+        durs.append(a.elapsed_time(b))
+    return durs
+
+
+def predictor_roofline(device, peak_gbs):
+    """Bulk predictor kernel (tw_predict_features) at 2^27 queries: achieved GB/s vs HBM peak."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib, presets
+    from paper_2601_00397_b200._device import stream_handle
+
+    pset = presets.calibration_set()
+    n = 1 << 27
+    g = torch.Generator(device=device).manual_seed(0)
+    P = torch.randint(0, 8192, (n,), dtype=torch.int32, device=device, generator=g)
+    D = torch.randint(0, 257, (n,), dtype=torch.int32, device=device, generator=g)
+    C = torch.randint(0, 600_000, (n,), dtype=torch.int64, device=device, generator=g)
+    I = torch.randint(0, 16, (n,), dtype=torch.int32, device=device, generator=g)
+    out = torch.empty(n, dtype=torch.int64, device=device)
+    blob = pset.device_blob(device)
+    lib = _lib.load()
+    s = torch.cuda.current_stream()
+
+    def run():
+        _lib.check(lib.tw_predict_features(blob.data_ptr(), pset.nbytes, P.data_ptr(), D.data_ptr(), C.data_ptr(),
+                                           I.data_ptr(), n, out.data_ptr(), stream_handle(s)), "predict")
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    durs = []
+    for _ in range(10):  # inputs (3.7 GB) far exceed L2: no flush needed
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        run()
+        b.record(s)
+        b.synchronize()
+        durs.append(a.elapsed_time(b))
+    ms = statistics.median(durs)
+    bytes_per = 4 + 4 + 8 + 4 + 8  # P, D, C, desc_id in; ns out
+    gbs = n * bytes_per / (ms / 1e3) / 1e9
+    del P, D, C, I, out
+    return {"kernel": "k_predict_features", "bound": "hbm", "achieved": round(gbs, 1), "peak": peak_gbs,
+            "unit": "GB/s", "frac": round(gbs / peak_gbs, 4), "bytes_per_prediction": bytes_per,
+            "predictions_per_launch": n, "ms_per_launch": round(ms, 4),
+            "predictions_per_s": round(n / (ms / 1e3), 1), "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+
+def cpu_baseline(sw, budget_s: float, n_threads: int):
+    """The C oracle port over a stratified sample of the same sweep, all host threads."""
+    from oracle import oracle as orc
+
+    n = len(sw)
+    take = max(1, min(n, 8 * n_threads))
+    t_est = None
+    while True:
+        ids = np.linspace(0, n - 1, take).astype(np.int64)
+        sub = sw.subset(ids)
+        t0 = time.perf_counter()
+        res, *_ = orc.sim_many(sub.pset.blob, sub.cfgs, sub.workloads.wl_off, sub.workloads.offset_ns,
+                               sub.workloads.prompt, sub.workloads.output, n_threads=n_threads)
+        dt = time.perf_counter() - t0
+        if dt >= 0.5 * budget_s / 4 or take >= n:
+            t_est = dt
+            break
+        take = min(n, int(take * max(2.0, (budget_s / 4) / max(dt, 1e-3))))
+    vsec = float(res["final_now_ns"].astype(np.float64).sum()) / 1e9
+    steps = int(res["steps"].sum())
+    return {
+        "value": round(vsec / t_est, 1), "unit": "virtual-s/wall-s", "cores": n_threads, "kind": "port",
+        "sample": f"{take} of {n} configs (evenly spaced), C oracle (oracle/twb_oracle.c) on {n_threads} host threads",
+        "predictions_per_s": round(steps / t_est, 1), "seconds": round(t_est, 3),
+    }
+
+
+def run_reference(args):
+    """--impl reference: the CPU implementation (C oracle port; the reference is pure Python
+    and has no compiled path) on this box's host cores, same metric/config."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sw, config, scaling = build_workload(args, 1, 0)
+    from oracle import oracle as orc
+
+    threads = os.cpu_count() or 1
+    n = len(sw)
+    # each step: an evenly spaced sample of the sweep sized to ~1/(K+W) of a ~3 min budget
+    ids_all = np.arange(n)
+    sample = max(threads, min(n, 4 * threads))
+    vals, preds = [], []
+    for i in range(args.warmup + args.steps):
+        ids = ids_all[(np.arange(sample) * (n // sample) + i) % n]
+        sub = sw.subset(ids)
+        t0 = time.perf_counter()
+        res, *_ = orc.sim_many(sub.pset.blob, sub.cfgs, sub.workloads.wl_off, sub.workloads.offset_ns,
+                               sub.workloads.prompt, sub.workloads.output, n_threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            vals.append(float(res["final_now_ns"].astype(np.float64).sum()) / 1e9 / dt)
+            preds.append(float(res["steps"].sum()) / dt)
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "emulated virtual-sec/wall-sec over config sweep", "value": round(v, 1),
+        "unit": "virtual-s/wall-s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic", "config": config, "predictions_per_s": round(statistics.median(preds), 1),
+        "cpu_baseline": {"value": round(v, 1), "unit": "virtual-s/wall-s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} configs per step of {n} (C oracle restating oracle.simulate)"},
+        "e2e": {"value": round(v, 1), "unit": "virtual-s/wall-s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.sweep import DeviceSweep, HostSweep
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(device)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "fallback": True}
+    peak_gbs = float(peaks["hbm_gbs"])
+
+    sw, config, scaling = build_workload(args, world, rank)
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+    stream = torch.cuda.current_stream(device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- device-resident timed region
+    barrier()
+    torch.cuda.synchronize(device)
+    launches0 = _lib.launch_count()
+    with ClockSampler(device.index or 0) as clk:
+        durs = time_kernel_steps(dev.run, args.steps, args.warmup, flush, stream)
+    torch.cuda.synchronize(device)
+    barrier()
+    launches = _lib.launch_count() - launches0 - args.warmup
+    ms = sum(durs) / len(durs)
+    out = dev.fetch()
+    if not (out.results["status"] == 0).all():
+        raise SystemExit(f"rank {rank}: {int((out.results['status'] != 0).sum())} configs did not finish OK")
+    vsec_local = out.virtual_seconds(sw.cfgs["epoch_ns"])
+    steps_local = out.predictions
+    ms_max = ms
+    vsec, steps_total = vsec_local, steps_local
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        s = torch.tensor([vsec_local, float(steps_local)], dtype=torch.float64, device=device)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        vsec, steps_total = float(s[0].item()), float(s[1].item())
+        # merge the per-config records on every rank (the sweep's only collective)
+        from paper_2601_00397_b200.distributed import gather_results
+
+        n_local = torch.tensor([len(sw)], device=device)
+        dist.all_reduce(n_local, op=dist.ReduceOp.MAX)
+        ids = np.arange(len(sw), dtype=np.int64) + rank * len(sw) if args.sweep == "1024" else None
+        if ids is not None:
+            gather_results(ids, out.results, len(sw) * world, int(n_local.item()), device)
+
+    value = vsec / (ms_max / 1e3)
+    preds_per_s = steps_total / (ms_max / 1e3)
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = HostSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+        e_durs = []
+        for i in range(args.warmup + args.steps):
+            flush_l2(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            host.run_from_host()
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                e_durs.append(a.elapsed_time(b))
+        e_ms = sum(e_durs) / len(e_durs)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
+               "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": host.d2h_bytes,
+               "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps_total / (e_ms / 1e3), 1)}
+
+    # ---- roofline of the dominant kernel (k_sim): algorithmic bytes / device time
+    n_req = int(dev.req_base[-1])
+    alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req  # configs in, records out, stamps out
+                 + 16 * n_req  # each config reads its workload (ts 8 + prompt 4 + output 4 B/request)
+                 + dev.pset.nbytes * _lib.last_sim_launch()["grid"])
+    achieved = alg_bytes / (ms / 1e3) / 1e9
+    launch = _lib.last_sim_launch()
+    roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(achieved / peak_gbs, 6), "traffic": None, "algorithmic_bytes_per_launch": int(alg_bytes),
+            "note": "serial per-config event loop: latency-bound (one warp per config), not HBM-bound; "
+                    "see ns_per_step_per_config", "launch": launch,
+            "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2)}
+
+    extra = {}
+    if rank == 0:
+        try:
+            extra["predictor_roofline"] = predictor_roofline(device, peak_gbs)
+        except Exception as exc:  # report, never hide
+            extra["predictor_roofline"] = {"error": repr(exc)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(sw, args.cpu_budget_s, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": "emulated virtual-sec/wall-sec over config sweep", "value": round(value, 1),
+            "unit": "virtual-s/wall-s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "int64+f64", "data": "synthetic", "config": config,
+            "predictions_per_s": round(preds_per_s, 1), "predictions_per_step": int(steps_total),
+            "virtual_s_per_step": round(vsec, 3), "gpu_launches": int(launches), "clocks": clk.summary(),
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, **extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,7 +190,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   int64_t* finish = p.finish ? p.finish + p.req_base[c] : nullptr;
   tw_event* evp = nullptr;
   int64_t ev_cap = 0;
-  if (p.ev) {
+  if (p.ev && p.ev_off[c + 1] > p.ev_off[c]) {  // audited config: full event dump
     evp = p.ev + p.ev_off[c];
     ev_cap = p.ev_off[c + 1] - p.ev_off[c];
   }

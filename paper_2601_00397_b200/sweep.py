@@ -360,3 +360,47 @@ def simulate(arrivals, cfg, predictor, epoch_ns: int = 0) -> list[dict]:
     out = simulate_many(wl, [sc], [predictor], audit=[0], per_request=False)
     _raise_status(out.results[0])
     return events_to_docs(out.events[0], wl.request_ids[0])
+
+
+class HostSweep(DeviceSweep):
+    """A sweep driven from HOST buffers: every ``run_from_host()`` copies the inputs
+    from pinned host memory to HBM, runs the event-loop kernel and copies the result
+    records (and per-request stamps) back to pinned host memory, all stream-ordered.
+    This is the end-to-end path a host caller pays for (bench.py ``e2e``)."""
+
+    def __init__(self, *args, **kwargs) -> None:
+        import torch
+
+        super().__init__(*args, **kwargs)
+        self._pairs_in = []
+        for d in (self.d_pset, self.d_cfgs, self.d_order, self.d_wl_off, self.d_ts, self.d_prompt, self.d_output):
+            h = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
+            h.copy_(d.cpu())
+            self._pairs_in.append((d, h))
+        if self.per_request:
+            h = torch.empty(self.d_req_base.shape, dtype=self.d_req_base.dtype, pin_memory=True)
+            h.copy_(self.d_req_base.cpu())
+            self._pairs_in.append((self.d_req_base, h))
+        self._pairs_out = [(self.d_res, torch.empty(self.d_res.shape, dtype=self.d_res.dtype, pin_memory=True))]
+        if self.per_request:
+            for d in (self.d_first, self.d_finish):
+                self._pairs_out.append((d, torch.empty(d.shape, dtype=d.dtype, pin_memory=True)))
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(sum(h.numel() * h.element_size() for _, h in self._pairs_in))
+
+    @property
+    def d2h_bytes(self) -> int:
+        return int(sum(h.numel() * h.element_size() for _, h in self._pairs_out))
+
+    def run_from_host(self, stream=None) -> None:
+        for d, h in self._pairs_in:
+            d.copy_(h, non_blocking=True)
+        self.run(stream)
+        for d, h in self._pairs_out:
+            h.copy_(d, non_blocking=True)
+
+    def host_results(self) -> np.ndarray:
+        raw = self._pairs_out[0][1].numpy().view(np.uint8)[: self.n_cfg * SIM_RESULT_DTYPE.itemsize]
+        return raw.view(SIM_RESULT_DTYPE).copy()

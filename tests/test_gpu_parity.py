@@ -1,0 +1,317 @@
+"""GPU parity: libtwb200 (sm_100a) vs the reference's golden outputs and the C oracle.
+
+Bar: bit-exact for every integer output (ns durations, event streams, digests,
+Timekeeper offsets/seq/wall). The predictor's fp64 pre-rounding value has no
+separate output: the int64 ns result must match exactly, which is stricter than
+the north star's 1e-6 relative fp32 tolerance.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from _fixtures import (
+    barrier_golden,
+    case_events,
+    case_inputs,
+    oracle_golden,
+    predictor_golden,
+    tk_case_inputs,
+    tkgrid_golden,
+)
+
+pytestmark = pytest.mark.gpu
+
+MS = 1_000_000
+
+
+# ---------------------------------------------------------------------------------
+# predictor
+# ---------------------------------------------------------------------------------
+
+
+def test_predict_features_matches_reference_vectors():
+    from paper_2601_00397_b200.predictor import PredictorSet
+
+    specs, preds, P, D, C, desc, expected = predictor_golden()
+    got = PredictorSet(preds).predict_features(P, D, C, desc)
+    bad = np.nonzero(got != expected)[0]
+    assert bad.size == 0, [(specs[desc[i]]["name"], P[i], D[i], C[i], got[i], expected[i]) for i in bad[:5]]
+
+
+def test_predict_features_equals_oracle_on_random_sweep():
+    """>= 10^6 random queries against the C oracle."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+
+    pset = presets.calibration_set()
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    P = rng.integers(0, 8300, n).astype(np.int32)
+    D = rng.integers(0, 540, n).astype(np.int32)
+    C = rng.integers(0, 700_000, n).astype(np.int64)
+    ids = rng.integers(0, len(pset.predictors), n).astype(np.int32)
+    P[::7] = 0
+    D[::11] = 0
+    C[::101] = -1  # some empty batches where P == D == 0
+    got = pset.predict_features(P, D, C, ids)
+    want = orc.predict_many(pset.blob, P, D, C, ids)
+    assert np.array_equal(got, want)
+
+
+def test_reference_known_answers_through_drop_in_predict():
+    """pkg/tests/test_predictor.py:18-144 worked examples, via predict(batch)."""
+    from paper_2601_00397_b200.predictor import (
+        BatchComposition,
+        ConstantPredictor,
+        DecodeSlot,
+        EmptyBatch,
+        LinearPredictor,
+        NegativeDuration,
+        PrefillChunk,
+        TableMiss,
+        TablePredictor,
+    )
+
+    chunky = BatchComposition(
+        prefill_chunks=(PrefillChunk("r1", 256, 0), PrefillChunk("r2", 128, 512)),
+        decodes=(DecodeSlot("r3", 512), DecodeSlot("r4", 700)),
+    )
+    assert ConstantPredictor(20000).predict(chunky) == 20_000_000
+    assert LinearPredictor(500.0, 10.0, 150.0, 0.5).predict(chunky) == 5_502_000
+    assert LinearPredictor(0.0, 0.3).predict(BatchComposition(prefill_chunks=(PrefillChunk("r", 1, 0),))) == 0
+    with pytest.raises(NegativeDuration):
+        LinearPredictor(-100.0).predict(chunky)
+    with pytest.raises(EmptyBatch):
+        ConstantPredictor(10).predict(BatchComposition())
+    table = {(0, 1): 100, (0, 8): 800, (512, 1): 2000, (512, 8): 3000, (1024, 1): 4000, (1024, 8): 5200}
+
+    def batch(p, d):
+        chunks = (PrefillChunk("p", p, 0),) if p else ()
+        return BatchComposition(chunks, tuple(DecodeSlot(f"d{i}", 128) for i in range(d)))
+
+    t = TablePredictor(table)
+    assert t.predict(batch(512, 8)) == 3_000_000
+    assert t.predict(batch(256, 1)) == 1_050_000
+    assert t.predict(batch(256, 4)) == 1_414_000
+    with pytest.raises(TableMiss):
+        t.predict(batch(2048, 4))
+    assert TablePredictor(table, allow_extrapolation=True).predict(batch(2048, 4)) == 4_000_000
+    with pytest.raises(TableMiss):
+        TablePredictor({(0, 1): 100, (512, 1): 2000, (512, 8): 3000}).predict(batch(256, 4))
+    # bulk path with features
+    out, feat = t.predictor_set.predict_batches([chunky, batch(256, 4)], [0, 0], return_features=True)
+    assert feat[0].tolist() == [384, 2, 1724]
+    assert out[1] == 1_414_000
+
+
+# ---------------------------------------------------------------------------------
+# Timekeeper
+# ---------------------------------------------------------------------------------
+
+
+def test_tk_replay_matches_reference_barriercore():
+    from paper_2601_00397_b200.timekeeper import replay_arrays
+
+    g = barrier_golden()
+    r = replay_arrays(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"])
+    assert np.array_equal(r.acks, g["acks"])
+    for s in range(len(g["op_off"]) - 1):
+        want = g["events"][g["ev_off"][s] : g["ev_off"][s + 1]]
+        e = r.events[s]
+        got = np.stack([e["kind"], e["offset_ns"], e["seq"], e["wall_ns"]], axis=1) if len(e) else np.zeros((0, 4))
+        assert np.array_equal(got, want), s
+    assert np.array_equal(np.stack([r.final["offset_ns"], r.final["seq"], r.final["wall_ns"]], axis=1), g["final"])
+
+
+def test_tk_opstream_api_reproduces_two_round_example():
+    """pkg/tests/test_barrier_core.py:51-72 through the OpStream builder."""
+    from paper_2601_00397_b200.timekeeper import OpStream, replay_many
+
+    WALL0 = 1_000_000_000
+    h = OpStream(cooldown_ns=500_000)
+    a, b = h.register_actor(), h.register_actor()
+    h.seal()
+    h.jump(a, WALL0 + 100 * MS)
+    h.advance(20 * MS)
+    h.jump(b, WALL0 + 50 * MS)
+    h.jump(a, WALL0 + 100 * MS)
+    h.jump(b, WALL0 + 200 * MS)
+    r = replay_many([h])
+    assert r.broadcast_sequence(0) == [(30 * MS, 1), (79_500_000, 2)]
+    assert int(r.final[0]["wall_ns"]) == WALL0 + 20 * MS + 500_000
+
+
+@pytest.mark.parametrize("A", [1, 2, 5, 9, 17, 32])
+def test_tk_resolve_matches_oracle(A):
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.timekeeper import resolve_round
+
+    rng = np.random.default_rng(A)
+    C = 20000
+    pending = rng.integers(1, 10**12, C * A).astype(np.int64)
+    pending[rng.random(C * A) < 0.1] = np.iinfo(np.int64).max
+    elig = rng.integers(0, 1 << A, C, dtype=np.int64).astype(np.uint32)
+    elig[::3] = (1 << A) - 1 if A < 32 else 0xFFFFFFFF
+    for c in range(0, C, 5):  # make every eligible slot pending in a fifth of the configs
+        for a in range(A):
+            if (int(elig[c]) >> a) & 1 and pending[c * A + a] == np.iinfo(np.int64).max:
+                pending[c * A + a] = 5
+    offset = rng.integers(0, 10**9, C).astype(np.int64)
+    seq = rng.integers(0, 100, C).astype(np.int64)
+    wall = rng.integers(0, 10**12, C).astype(np.int64)
+    last = np.where(rng.random(C) < 0.3, np.iinfo(np.int64).min, wall - rng.integers(0, 10**6, C)).astype(np.int64)
+    cool = 500_000
+    st = [x.copy() for x in (pending, offset, seq, wall, last)]
+    bc_cpu = orc.tk_resolve(st[0], elig, A, cool, st[1], st[2], st[3], st[4])
+    dv = [torch.from_numpy(x.copy()).cuda() for x in (pending, offset, seq, wall, last)]
+    bc = resolve_round(dv[0], torch.from_numpy(elig.view(np.int32)).cuda(), A, cool, dv[1], dv[2], dv[3], dv[4])
+    assert np.array_equal(bc.cpu().numpy(), bc_cpu)
+    for d, c in zip(dv, st):
+        assert np.array_equal(d.cpu().numpy(), c)
+
+
+# ---------------------------------------------------------------------------------
+# event loop
+# ---------------------------------------------------------------------------------
+
+
+def _multi_case_sweep(cases, timekeeper=False, audit=True):
+    from paper_2601_00397_b200._lib import SIM_CFG_DTYPE
+    from paper_2601_00397_b200.predictor import PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    preds, arrays, ids = [], [], []
+    cfgs = np.zeros(len(cases), SIM_CFG_DTYPE)
+    for i, case in enumerate(cases):
+        pset, wl, c = case_inputs(case, timekeeper=timekeeper)
+        preds.append(pset.predictors[0])
+        arrays.append(wl.workload(0))
+        cfgs[i] = c[0]
+        cfgs[i]["pred_id"] = i
+        cfgs[i]["workload_id"] = i
+    sw = DeviceSweep(PredictorSet(preds), pack_arrays(arrays), cfgs, per_request=True,
+                     audit=list(range(len(cases))) if audit else ())
+    sw.run()
+    return sw.fetch()
+
+
+def _check(case, res, first, finish, events, ev_all, ev_off):
+    st = int(res["status"]) & 0xFF
+    assert st == case["status"], (case["name"], st)
+    if case["status"] != 0:
+        return
+    assert int(res["events"]) == case["n_events"], case["name"]
+    assert int(np.uint64(res["digest"])) == int(case["digest"]), case["name"]
+    assert int(res["final_now_ns"]) == case["final_ts"], case["name"]
+    assert int(res["steps"]) == case["steps"], case["name"]
+    assert hashlib.sha256(first.tobytes()).hexdigest() == case["first_sha"], case["name"]
+    assert hashlib.sha256(finish.tobytes()).hexdigest() == case["finish_sha"], case["name"]
+    if events is not None and "ev_index" in case:
+        want = case_events(case, ev_all, ev_off)
+        rk = events["req_kind"].astype(np.int64)
+        got = np.stack([rk >> 2, rk & 3, events["ts_ns"], events["step"]], axis=1)
+        assert np.array_equal(got, want), case["name"]
+
+
+def test_sim_small_cases_event_for_event():
+    cases, ev_all, ev_off = oracle_golden()
+    small = [c for c in cases if c["arrivals"] is not None]
+    out = _multi_case_sweep(small)
+    for i, case in enumerate(small):
+        lo, hi = out.req_base[i], out.req_base[i + 1]
+        _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], out.events.get(i), ev_all, ev_off)
+
+
+def test_sim_small_cases_with_timekeeper_keep_the_timeline():
+    """Driving time through the actor grid must not change any event (live == oracle)."""
+    cases, ev_all, ev_off = oracle_golden()
+    small = [c for c in cases if c["arrivals"] is not None]
+    out = _multi_case_sweep(small, timekeeper=True, audit=False)
+    for i, case in enumerate(small):
+        lo, hi = out.req_base[i], out.req_base[i + 1]
+        _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], None, ev_all, ev_off)
+
+
+def test_sim_full_size_cases_match_reference_digests():
+    cases, ev_all, ev_off = oracle_golden()
+    big = [c for c in cases if c["arrivals"] is None]
+    out = _multi_case_sweep(big, audit=False)
+    for i, case in enumerate(big):
+        lo, hi = out.req_base[i], out.req_base[i + 1]
+        _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], None, ev_all, ev_off)
+
+
+@pytest.mark.parametrize("case", tkgrid_golden(), ids=lambda c: c["name"])
+def test_sim_timekeeper_grid_matches_reference_barriercore(case):
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    pset, wl, cfgs = tk_case_inputs(case)
+    sw = DeviceSweep(pset, wl, cfgs, per_request=False)
+    sw.run()
+    r = sw.fetch().results[0]
+    assert int(r["status"]) == 0
+    assert int(np.uint64(r["digest"])) == int(case["digest"])
+    assert (int(r["tk_seq"]), int(r["tk_offset_ns"]), int(r["tk_wall_ns"])) == (case["seq"], case["offset"], case["wall"])
+
+
+def test_sweep_1024_equals_oracle_on_every_config():
+    """BASELINE config 4 at full size: every record bit-identical to the C oracle."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    sw = presets.sweep_1024()
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+    dev.run()
+    out = dev.fetch()
+    res, req_base, first, finish = orc.sim_many(
+        sw.pset.blob, sw.cfgs, sw.workloads.wl_off, sw.workloads.offset_ns, sw.workloads.prompt,
+        sw.workloads.output, per_request=True,
+    )
+    assert (out.results["status"] == 0).all()
+    for f in ("final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns", "status"):
+        assert np.array_equal(out.results[f], res[f]), f
+    assert np.array_equal(out.first_ns, first[: len(out.first_ns)])
+    assert np.array_equal(out.finish_ns, finish[: len(out.finish_ns)])
+    # size-independent properties: every request finishes once, after its first token
+    assert (out.finish_ns >= out.first_ns).all() and (out.first_ns >= 0).all()
+    events_expected = int((sw.workloads.output.astype(np.int64) + 1).sum()) * len(sw)
+    assert int(out.results["events"].sum()) == events_expected
+
+
+def test_drop_in_simulate_matches_reference_timeline():
+    """pkg/tests/test_oracle.py:35-43 through sweep.simulate (full event dicts)."""
+    from paper_2601_00397_b200.predictor import ConstantPredictor
+    from paper_2601_00397_b200.sweep import EngineConfig, OracleStalled, simulate
+    from paper_2601_00397_b200.workload import Arrival
+
+    cfg = EngineConfig(chunk_size=512, max_batch_tokens=1024, max_running=8, kv_block_tokens=16, kv_capacity_blocks=4096)
+    ev = simulate([Arrival("r00000", 0, 512, 2)], cfg, ConstantPredictor(10_000))
+    assert ev == [
+        {"request_id": "r00000", "kind": "FIRST_TOKEN", "virtual_ts_ns": 10 * MS, "step": 1},
+        {"request_id": "r00000", "kind": "OUTPUT_TOKEN", "virtual_ts_ns": 20 * MS, "step": 2},
+        {"request_id": "r00000", "kind": "FINISHED", "virtual_ts_ns": 20 * MS, "step": 2},
+    ]
+    with pytest.raises(OracleStalled):
+        simulate([Arrival("r00000", 0, 256, 1)], EngineConfig(chunk_size=512, max_batch_tokens=1024, max_running=8,
+                                                              kv_block_tokens=16, kv_capacity_blocks=8),
+                 ConstantPredictor(10_000))
+
+
+def test_native_library_is_the_in_tree_build():
+    import os
+
+    from paper_2601_00397_b200 import _lib
+
+    lib = _lib.load()
+    assert os.path.abspath(lib._name).startswith(os.path.abspath(os.path.join(os.path.dirname(_lib.__file__), "lib")))
+    before = _lib.launch_count()
+    from paper_2601_00397_b200.predictor import ConstantPredictor, BatchComposition, DecodeSlot
+
+    ConstantPredictor(5).predict(BatchComposition(decodes=(DecodeSlot("x", 1),)))
+    assert _lib.launch_count() == before + 1

@@ -1,0 +1,226 @@
+"""CPU tests: the C-ABI library's exports, host-side packing, presets, sharding (gloo)."""
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2601_00397_b200 import _lib, calibration, presets
+from paper_2601_00397_b200._lib import PRED_DESC_DTYPE, PSET_HEADER_DTYPE
+from paper_2601_00397_b200.predictor import (
+    BatchComposition,
+    DecodeSlot,
+    NegativeDuration,
+    PredictorError,
+    PredictorSet,
+    PrefillChunk,
+    TableParseError,
+    TablePredictor,
+    build_predictor,
+    pack_batches,
+)
+from paper_2601_00397_b200.sweep import EngineConfig, SchedulingPolicy
+from paper_2601_00397_b200.timekeeper import OpStream, client_index, pack_streams
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "twb200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tw_[a-z_0-9]+)\(", text, re.M)))
+
+
+def test_header_declares_what_the_binding_binds():
+    assert declared_symbols() == sorted(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2601_00397_b200.build import build_native
+
+        build_native()
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.tw_abi_version() == _lib.ABI_VERSION
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_sass_is_sm100a_and_uses_the_bulk_copy_engine():
+    out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out or "SM100" in out.upper()
+    assert "UBLKCP" in out  # cp.async.bulk (TMA) staging of the predictor blob
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    import importlib
+
+    mod = importlib.reload(_lib)
+    try:
+        with pytest.raises(mod.NativeLibraryMissing):
+            mod.load(str(tmp_path / "nope.so"))
+    finally:
+        importlib.reload(_lib)
+
+
+def test_pset_blob_layout_round_trips():
+    t = TablePredictor({(0, 1): 100, (512, 1): 2000, (512, 8): 3000}, allow_extrapolation=True)
+    ps = PredictorSet([build_predictor({"kind": "constant", "duration_us": 7}), t,
+                       build_predictor({"kind": "linear", "base_us": 1.5, "per_decode_us": 2.0})])
+    blob = ps.blob
+    assert blob.size % 16 == 0
+    hdr = blob[:16].view(PSET_HEADER_DTYPE)[0]
+    assert hdr["magic"] == _lib.TW_PSET_MAGIC and hdr["n_desc"] == 3 and hdr["total_bytes"] == blob.size
+    descs = blob[16 : 16 + 3 * 64].view(PRED_DESC_DTYPE)
+    assert descs["kind"].tolist() == [0, 2, 1]
+    assert descs[0]["constant_us"] == 7 and descs[2]["per_decode_us"] == 2.0
+    off, np_, nd = int(descs[1]["table_off"]), int(descs[1]["np"]), int(descs[1]["nd"])
+    assert off % 16 == 0
+    pax = blob[off : off + 4 * np_].view(np.int32)
+    dax = blob[off + 4 * np_ : off + 4 * (np_ + nd)].view(np.int32)
+    g0 = off + ((4 * (np_ + nd) + 7) // 8) * 8
+    grid = blob[g0 : g0 + 8 * np_ * nd].view(np.int64).reshape(np_, nd)
+    assert pax.tolist() == [0, 512] and dax.tolist() == [1, 8]
+    assert grid.tolist() == [[100, -1], [2000, 3000]]
+
+
+def test_predictor_construction_errors_mirror_reference(tmp_path):
+    with pytest.raises(TableParseError):
+        TablePredictor({})
+    with pytest.raises(NegativeDuration):
+        build_predictor({"kind": "constant", "duration_us": -1})
+    with pytest.raises(PredictorError):
+        build_predictor({"kind": "quadratic"})
+    p = tmp_path / "c.csv"
+    p.write_text("total_prefill_tokens,num_decodes,duration_us\n0,1,100\n512,1,2000\n512,1,2100\n")
+    t = TablePredictor.from_csv(str(p))
+    assert t._rows[(512, 1)] == 2100
+    p.write_text("prefill,decodes,us\n1,2,3\n")
+    with pytest.raises(TableParseError):
+        TablePredictor.from_csv(str(p))
+    p.write_text("total_prefill_tokens,num_decodes,duration_us\n0,1,fast\n")
+    with pytest.raises(TableParseError):
+        TablePredictor.from_csv(str(p))
+    p.write_text("total_prefill_tokens,num_decodes,duration_us\n0,1,-5\n")
+    with pytest.raises(NegativeDuration):
+        TablePredictor.from_csv(str(p))
+
+
+def test_pack_batches_csr():
+    chunky = BatchComposition(
+        prefill_chunks=(PrefillChunk("r1", 256, 0), PrefillChunk("r2", 128, 512)),
+        decodes=(DecodeSlot("r3", 512), DecodeSlot("r4", 700)),
+    )
+    off, tok, ctx = pack_batches([chunky, BatchComposition()])
+    assert off.tolist() == [0, 4, 4]
+    assert tok.tolist() == [256, 128, -1, -1]
+    assert ctx.tolist() == [0, 512, 512, 700]
+
+
+def test_engine_config_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        EngineConfig(chunk_size=0)
+    with pytest.raises(ValueError):
+        EngineConfig(chunk_size=1024, max_batch_tokens=512)
+    with pytest.raises(ValueError):
+        EngineConfig(kv_block_tokens=0)
+    with pytest.raises(ValueError):
+        EngineConfig(pp_stages=0)
+    assert EngineConfig.from_doc({"policy": "prefill_prioritized"}).policy is SchedulingPolicy.PREFILL_PRIORITIZED
+
+
+def test_presets_shapes():
+    sw = presets.sweep_1024()
+    assert len(sw) == 1024
+    assert sw.workloads.n_workloads == 1 and sw.workloads.sizes().tolist() == [1000]
+    assert set(sw.cfgs["pred_id"].tolist()) == set(range(8))
+    assert (sw.cfgs["flags"] == 1).all() and (sw.cfgs["tk_cooldown_ns"] == 500_000).all()
+    big = presets.sweep_65536(seeds=(1, 2))
+    assert len(big) == 1024 * 2 * 2
+
+
+def test_calibration_csvs_are_frozen():
+    for m in calibration.MODELS:
+        for tp, pp in calibration.TP_PP_GRID:
+            t = TablePredictor.from_csv(calibration.csv_path(m, tp, pp), allow_extrapolation=True)
+            assert t._rows == calibration.table_rows(m, tp, pp)
+    assert calibration.table_rows("8b", 1, 1)[(0, 1)] == 835
+    assert round(calibration.scale("70b", 4, 2), 2) == 6.22
+
+
+def test_opstream_encoding():
+    h = OpStream()
+    a = h.register_actor()
+    o = h.register_observer()
+    h.seal()
+    h.jump(a, 5)
+    h.enter(a, "g", 2)
+    h.enter(a, "h", 1)
+    h.jump("actor99", 3)
+    h.jump("bogus", 3)
+    h.deregister(o)
+    ops, off, wall0, cool, sup = pack_streams([h])
+    assert ops["type"].tolist() == [0, 1, 2, 3, 4, 4, 3, 7, 5]
+    assert ops["group"].tolist()[4:6] == [0, 1]
+    assert ops["client"].tolist()[6] == 98
+    assert client_index("observer2") == 1 and client_index("nope") == -1
+    assert off.tolist() == [0, 9]
+
+
+def test_partition_balances_and_covers():
+    from paper_2601_00397_b200.distributed import partition
+
+    costs = np.random.default_rng(0).random(1000) * 10
+    shards = partition(costs, 8)
+    allids = np.sort(np.concatenate(shards))
+    assert allids.tolist() == list(range(1000))
+    loads = [costs[s].sum() for s in shards]
+    assert max(loads) - min(loads) <= costs.max()
+
+
+def _gather_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_00397_b200._lib import SIM_RESULT_DTYPE
+    from paper_2601_00397_b200.distributed import gather_results, partition
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    n = 37
+    shards = partition(np.arange(n, dtype=np.float64) + 1, world)
+    ids = shards[rank]
+    res = np.zeros(len(ids), SIM_RESULT_DTYPE)
+    res["steps"] = ids * 10
+    res["digest"] = ids.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    res["final_now_ns"] = ids + 1_790_000_000_000_000_000
+    merged = gather_results(ids, res, n, max(len(s) for s in shards), torch.device("cpu"))
+    q.put((rank, merged["steps"].tolist(), merged["final_now_ns"].tolist(), merged["digest"].tolist()))
+    dist.destroy_process_group()
+
+
+def test_sharded_gather_world2_gloo():
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, steps, final, dig in outs:
+        assert steps == [i * 10 for i in range(37)]
+        assert final == [i + 1_790_000_000_000_000_000 for i in range(37)]
+        assert dig == [(i * 0x9E3779B97F4A7C15) % (1 << 64) for i in range(37)]
