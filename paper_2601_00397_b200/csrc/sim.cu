@@ -4,7 +4,7 @@
 // CPU timeline the live stack must match event-for-event
 // (pkg/tests/test_harness_integration.py:77-83).
 //
-// Design (DESIGN.md §4):
+// Design (DESIGN.md §4.1):
 //  * persistent kernel; each warp pulls whole configs from a device work counter in
 //    host-sorted (largest-first) order and runs that config's loop to completion;
 //  * the config's active list lives in the warp's slice of shared memory as SoA
@@ -16,8 +16,13 @@
 //    (budget, KV, slot) constraints hold;
 //  * features P/D/C are REDUX sums, the prediction is the warp-uniform exact-fp64
 //    predictor over the TMA-staged calibration blob in shared memory;
-//  * virtual time advances through the Timekeeper min-advance: lane a holds actor a
-//    (dispatcher + TP x PP workers) and each round is one int64 REDUX min;
+//  * virtual time advances through the config's Timekeeper min-advance (dispatcher +
+//    TP x PP workers, BarrierCore rules on a FakeClock);
+//  * decode-only runs are macro-stepped: while no request finishes and no arrival
+//    can be admitted, every step decodes the same D requests with the same predicted
+//    duration, so the run length is closed-form (min remaining outputs, first
+//    arrival crossing) and the run's K*D token events are hashed in parallel across
+//    the lanes instead of K serial plan/apply passes ("macro steps");
 //  * every token event is hashed into a position-bound digest (tw_event_hash) and
 //    FIRST_TOKEN / FINISHED stamps are stored per request; full event dumps only
 //    for audited configs.
@@ -56,14 +61,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// int64 warp min with two REDUX ops (hi signed, then lo unsigned among hi-minimal lanes)
-__device__ __forceinline__ int64_t warp_min_i64_redux(int64_t v) {
-  const int hi = (int)(v >> 32);
-  const int mh = __reduce_min_sync(kFull, hi);
-  const unsigned lo = (hi == mh) ? (unsigned)(uint64_t)v : 0xffffffffu;
-  const unsigned ml = __reduce_min_sync(kFull, lo);
-  return (int64_t)(((uint64_t)(uint32_t)mh << 32) | ml);
-}
 // int64 warp sum of non-negative values < 2^50 per lane, with two REDUX ops
 __device__ __forceinline__ int64_t warp_sum_i64_redux(int64_t v) {
   const unsigned lo = (unsigned)(v & 0xffffff);
@@ -83,9 +80,23 @@ __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
   return v;
 }
 
-__device__ __forceinline__ int64_t blocks_of(int64_t tokens, int64_t bk) {
-  return tokens > 0 ? (tokens + bk - 1) / bk : 0;  // oracle.py:39-40
-}
+// ceil(t / bk) for 0 <= t < 2^31 with a per-config magic reciprocal (no IDIV chain):
+// q0 = umulhi(t, floor((2^32-1)/bk)) is at most 2 below floor(t/bk).
+struct Blocks {
+  uint32_t bk, magic;
+  __device__ __forceinline__ void init(uint32_t b) {
+    bk = b;
+    magic = 0xffffffffu / b;
+  }
+  __device__ __forceinline__ int32_t ceil_div(int32_t t) const {  // oracle.py:39-40
+    if (t <= 0) return 0;
+    uint32_t q = __umulhi((uint32_t)t, magic);
+    uint32_t r = (uint32_t)t - q * bk;
+    if (r >= bk) { q++; r -= bk; }
+    if (r >= bk) { q++; r -= bk; }
+    return (int32_t)(q + (r != 0u));
+  }
+};
 
 struct Slots {
   int32_t* req;
@@ -96,15 +107,37 @@ struct Slots {
   int32_t* plan;  // >= 0 chunk tokens, -1 decode, -2 idle (this step)
 };
 
-// Per-config Timekeeper actor grid: actor 0 is the
-// dispatcher, actors 1..TP*S the workers; BarrierCore semantics on a FakeClock.
+// Lane-distributed window over a workload's arrival offsets: lane l holds
+// epoch + ts[base + l] (INT64_MAX past the end); one coalesced load per 32 arrivals.
+struct ArrWindow {
+  int32_t base;
+  int64_t v;
+  __device__ __forceinline__ void load(const int64_t* __restrict__ ts, int32_t n, int64_t epoch, int32_t b) {
+    const int lane = threadIdx.x & 31;
+    base = b;
+    v = (b + lane < n) ? epoch + __ldg(ts + b + lane) : INT64_MAX;
+  }
+  // uniform idx < n
+  __device__ __forceinline__ int64_t get(const int64_t* __restrict__ ts, int32_t n, int64_t epoch, int32_t idx) {
+    if (idx - base >= 32) load(ts, n, epoch, idx);
+    return __shfl_sync(kFull, v, idx - base);
+  }
+};
+
+// Per-config Timekeeper actor grid: actor 0 is the dispatcher,
+// actors 1..TP*S the WorkerGrid cells; BarrierCore rules on a FakeClock. Each round's
+// t_min is the min over the eligible actors' pending targets, which reduces to
+// min(dispatcher's next arrival, current stage deadline) because the TP ranks of a
+// stage share its deadline and parked workers are exempt.
 struct TkGrid {
   int64_t wall, offset, seq, last_bcast, V, cooldown, conv_cooldown;
-  int64_t disp, disp_ts;
+  int64_t disp_ts;
+  int32_t disp;
+  ArrWindow win;
 };
 
 __device__ __forceinline__ void tk_resolve(TkGrid& g, int64_t t_min) {
-  // timekeeper.py:326-366 with FakeClock sleep
+  // timekeeper.py:326-366 with FakeClock sleep (pkg/tests/_support.py:33-34)
   if (g.wall < t_min && g.last_bcast != INT64_MIN && g.cooldown > 0) {
     const int64_t wait = g.last_bcast + g.cooldown - g.wall;
     if (wait > 0) g.wall += (wait == g.cooldown) ? g.conv_cooldown : fake_sleep_ns(wait);
@@ -118,35 +151,69 @@ __device__ __forceinline__ void tk_resolve(TkGrid& g, int64_t t_min) {
   g.V = g.wall + g.offset;
 }
 
-// Advance until V >= end. stages == 0: idle jump, only the dispatcher drives time.
-__device__ __forceinline__ void tk_advance(TkGrid& g, const int64_t* __restrict__ ts, int64_t n,
-                                           int64_t epoch, int S, int TP, int stages_on, int64_t base,
-                                           int64_t d, int64_t end) {
-  const int lane = threadIdx.x & 31;
-  const int64_t per = d / S;
-  for (;;) {
-    while (g.disp < n && g.disp_ts <= g.V) {  // dispatcher passes every arrival <= V
-      g.disp++;
-      g.disp_ts = g.disp < n ? epoch + __ldg(ts + g.disp) : INT64_MAX;
-    }
-    if (g.V >= end) return;
-    int cs = S;
-    if (stages_on) {
-      for (int s = 0; s < S; s++) {
-        const int64_t e = (s == S - 1) ? base + d : base + per * (s + 1);
-        if (e > g.V) { cs = s; break; }
-      }
-    }
-    int64_t tgt = INT64_MAX;
-    if (lane == 0) {
-      tgt = g.disp_ts;
-    } else if (stages_on && lane <= TP * S) {
-      const int s = (lane - 1) / TP;
-      if (s == cs) tgt = (s == S - 1) ? base + d : base + per * (s + 1);
-    }
-    tk_resolve(g, warp_min_i64_redux(tgt));
+__device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch) {
+  while (g.disp_ts <= g.V) {  // the dispatcher passes every arrival <= V (runner.py:94-124)
+    g.disp++;
+    g.disp_ts = g.disp < n ? g.win.get(ts, n, epoch, g.disp) : INT64_MAX;
   }
 }
+
+// Rounds until V >= base + d. S == 0: idle jump (only the dispatcher drives time).
+// Stage deadlines: WorkerGrid.execute (engine.py:434-442).
+__device__ __forceinline__ void tk_advance(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+                                           int S, int64_t base, int64_t d) {
+  const int64_t end = base + d;
+  int64_t per = 0;
+  if (S > 1) per = (d >= 0 && d < 0x7fffffffLL) ? (int64_t)((uint32_t)d / (uint32_t)S) : d / S;
+  for (;;) {
+    tk_dispatch(g, ts, n, epoch);
+    if (g.V >= end) return;
+    int64_t stage = end;  // S == 0 (idle) -> the dispatcher's target is <= end
+    if (S > 1) {
+      for (int s = 0; s < S - 1; s++) {
+        const int64_t e = base + per * (s + 1);
+        if (e > g.V) { stage = e; break; }
+      }
+    } else if (S == 0) {
+      stage = INT64_MAX;
+    }
+    tk_resolve(g, g.disp_ts < stage ? g.disp_ts : stage);
+  }
+}
+
+struct PredCache {
+  int64_t P, D, C, d;
+  bool uses_c;
+};
+
+__device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, int id, int64_t P, int64_t D,
+                                                  int64_t C) {
+  if (P == pc.P && D == pc.D && (!pc.uses_c || C == pc.C)) return pc.d;
+  const int64_t d = predict_warp(ps, id, P, D, C);
+  pc.P = P;
+  pc.D = D;
+  pc.C = C;
+  pc.d = d;
+  return d;
+}
+
+struct Emitter {
+  uint64_t dig;  // lane-partial digest
+  int64_t* first;
+  int64_t* finish;
+  tw_event* evp;
+  int64_t ev_cap;
+  __device__ __forceinline__ void event(int64_t pos, int32_t rq, int kind, int64_t ts, int64_t step) {
+    dig += tw_event_hash((uint64_t)pos, (uint64_t)rq, (uint64_t)kind, ts, step);
+    if (evp && pos < ev_cap) {
+      tw_event e;
+      e.ts_ns = ts;
+      e.step = (int32_t)step;
+      e.req_kind = (rq << 2) | kind;
+      evp[pos] = e;
+    }
+  }
+};
 
 __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
   const int lane = threadIdx.x & 31;
@@ -177,23 +244,37 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   }
 
   const int64_t wl0 = p.wl_off[cfg.workload_id];
-  const int64_t n = p.wl_off[cfg.workload_id + 1] - wl0;
+  const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - wl0);
   const int64_t* __restrict__ ts = p.ts + wl0;
   const int32_t* __restrict__ prm = p.prompt + wl0;
   const int32_t* __restrict__ outp = p.output + wl0;
   const int64_t epoch = cfg.epoch_ns;
-  const int64_t bk = cfg.kv_block_tokens;
-  const int64_t chunk = cfg.chunk_size;
-  const int64_t mbt = cfg.max_batch_tokens;
-  const int64_t max_running = cfg.max_running;
-  int64_t* first = p.first ? p.first + p.req_base[c] : nullptr;
-  int64_t* finish = p.finish ? p.finish + p.req_base[c] : nullptr;
-  tw_event* evp = nullptr;
-  int64_t ev_cap = 0;
+  const int32_t chunk = cfg.chunk_size;
+  const int32_t mbt = cfg.max_batch_tokens;
+  const int32_t max_running = cfg.max_running;
+  Blocks blk;
+  blk.init((uint32_t)cfg.kv_block_tokens);
+
+  Emitter em;
+  em.dig = 0;
+  em.first = p.first ? p.first + p.req_base[c] : nullptr;
+  em.finish = p.finish ? p.finish + p.req_base[c] : nullptr;
+  em.evp = nullptr;
+  em.ev_cap = 0;
   if (p.ev && p.ev_off[c + 1] > p.ev_off[c]) {  // audited config: full event dump
-    evp = p.ev + p.ev_off[c];
-    ev_cap = p.ev_off[c + 1] - p.ev_off[c];
+    em.evp = p.ev + p.ev_off[c];
+    em.ev_cap = p.ev_off[c + 1] - p.ev_off[c];
   }
+
+  // predictor: cache + whether a decode-only run has a constant duration
+  const tw_pred_desc* pd = pset_desc(ps, cfg.pred_id < pset_ndesc(ps) ? cfg.pred_id : 0);
+  PredCache pc;
+  pc.P = -1;
+  pc.D = -1;
+  pc.C = -1;
+  pc.d = 0;
+  pc.uses_c = pd->kind == TW_PRED_LINEAR && pd->per_context_token_us != 0.0;
+  const bool macro_ok = !pc.uses_c && cfg.pred_id >= 0 && cfg.pred_id < pset_ndesc(ps);
 
   TkGrid g;
   g.wall = epoch;
@@ -204,80 +285,95 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   g.cooldown = cfg.tk_cooldown_ns;
   g.conv_cooldown = g.cooldown > 0 ? fake_sleep_ns(g.cooldown) : 0;
   g.disp = 0;
-  g.disp_ts = n > 0 ? epoch + __ldg(ts) : INT64_MAX;
+  g.win.load(ts, n, epoch, 0);
+  g.disp_ts = n > 0 ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
 
-  int64_t now = epoch, step = 0, n_events = 0, held_sum = 0;
-  int64_t fut = 0, w_head = 0;  // waiting = [w_head, fut), future = [fut, n)
-  int n_act = 0;
-  uint64_t dig = 0;  // lane-partial digest
-  // arrival-offset cache: lane l holds ts[cbase + l]
-  int64_t cbase = 0;
-  int64_t cts = (lane < n) ? __ldg(ts + lane) : INT64_MAX;
+  ArrWindow arr;
+  arr.load(ts, n, epoch, 0);
+  int64_t now = epoch, n_events = 0;
+  int32_t step = 0, fut = 0, w_head = 0, n_act = 0;  // waiting = [w_head, fut), future = [fut, n)
+  int64_t next_arr = n > 0 ? __shfl_sync(kFull, arr.v, 0) : INT64_MAX;
   int overflow = 0;
 
   while (fut < n || w_head < fut || n_act > 0) {
     // ---- arrivals with epoch + offset <= now join the waiting queue (oracle.py:73-75)
-    for (;;) {
-      if (fut >= n) break;
-      if (fut - cbase >= 32) {
-        cbase = fut;
-        cts = (cbase + lane < n) ? __ldg(ts + cbase + lane) : INT64_MAX;
-      }
-      const int sh = (int)(fut - cbase);
-      const bool le = (lane >= sh) && (cbase + lane < n) && (epoch + cts <= now);
-      const unsigned m = __ballot_sync(kFull, le) >> sh;    // bit 0 = arrival `fut`
-      const int width = 32 - sh;
-      const int k = (~m == 0u) ? width : min(__ffs(~m) - 1, width);
-      fut += k;
-      if (k < width) break;
+    while (next_arr <= now) {
+      fut++;
+      next_arr = fut < n ? arr.get(ts, n, epoch, fut) : INT64_MAX;
     }
+    const bool waiting = w_head < fut;
 
-    // ---- _plan (oracle.py:117-180), pass 1a: counts
-    const int64_t free0 = (int64_t)cfg.kv_capacity_blocks - held_sum;
+    // ---- _plan (oracle.py:117-180), pass 1a (only needed with > 32 active)
     int total_dec = 0;
     bool any_mid = false;
-    for (int b = 0; b < n_act; b += 32) {
-      const int i = b + lane;
-      const bool v = i < n_act;
-      const int32_t pr = v ? sl.prompt[i] : 0, dn = v ? sl.done[i] : 0;
-      const int32_t em = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
-      const bool mid = v && dn < pr;
-      total_dec += __popc(__ballot_sync(kFull, v && !mid && em < op));
-      any_mid |= __any_sync(kFull, mid);
-    }
-    bool do_dec = true, do_chunks = true;
-    if (cfg.policy == TW_POLICY_PREFILL_PRIORITIZED) {
-      bool have_prefill = any_mid;
-      if (!have_prefill && w_head < fut) {
-        const int64_t hp = __ldg(prm + w_head);
-        have_prefill = (int64_t)n_act < max_running && blocks_of(hp, bk) <= free0;
+    if (n_act > 32) {
+      for (int b = 0; b < n_act; b += 32) {
+        const int i = b + lane;
+        const bool v = i < n_act;
+        const int32_t pr = v ? sl.prompt[i] : 0, dn = v ? sl.done[i] : 0;
+        const int32_t e = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
+        const bool mid = v && dn < pr;
+        total_dec += __popc(__ballot_sync(kFull, v && !mid && e < op));
+        any_mid |= __any_sync(kFull, mid);
       }
-      do_chunks = have_prefill;
-      do_dec = !have_prefill;
     }
-    const int64_t n_dec = do_dec ? min((int64_t)total_dec, mbt) : 0;
-    int64_t budget = mbt - n_dec;
+    // KV: free = cap - sum(_held) (oracle.py:122), only needed when a queue head is probed
+    int64_t free0 = 0;
+    const bool need_free = waiting;
+    if (need_free) {
+      int64_t held_l = 0;
+      for (int b = 0; b < n_act; b += 32) {
+        const int i = b + lane;
+        if (i < n_act) {
+          const int32_t h0 = blk.ceil_div(sl.prompt[i]), h1 = blk.ceil_div(sl.done[i] + sl.emit[i]);
+          held_l += h0 > h1 ? h0 : h1;  // _held (oracle.py:43-46)
+        }
+      }
+      free0 = (int64_t)cfg.kv_capacity_blocks - warp_sum_i64_redux(held_l);
+    }
 
     // ---- pass 1b: decode cutoff, chunk takes, features
+    bool do_dec = true, do_chunks = true;
     int64_t p_l = 0, c_l = 0;  // lane partial P and C
-    int n_chunk = 0, chunk_ev = 0;
+    int n_chunk = 0, chunk_ev = 0, n_dec = 0;
     int dec_before = 0;
-    int64_t want_before = 0;
-    for (int b = 0; b < n_act; b += 32) {
+    int64_t want_before = 0, budget = mbt;
+    int min_rem = 0x7fffffff;  // min (output - emitted) over decoders (macro-step horizon)
+    for (int b = 0; b < (n_act > 0 ? n_act : 1); b += 32) {
       const int i = b + lane;
       const bool v = i < n_act;
       const int32_t pr = v ? sl.prompt[i] : 0, dn = v ? sl.done[i] : 0;
-      const int32_t em = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
+      const int32_t e = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
       const bool mid = v && dn < pr;
-      const bool dcand = v && !mid && em < op;
+      const bool dcand = v && !mid && e < op;
       const unsigned dm = __ballot_sync(kFull, dcand);
+      if (b == 0) {
+        if (n_act <= 32) {
+          total_dec = __popc(dm);
+          any_mid = __any_sync(kFull, mid);
+        }
+        if (cfg.policy == TW_POLICY_PREFILL_PRIORITIZED) {  // oracle.py:168-178
+          bool have_prefill = any_mid;
+          if (!have_prefill && waiting) {
+            const int32_t hp = __ldg(prm + w_head);
+            have_prefill = n_act < max_running && blk.ceil_div(hp) <= free0;
+          }
+          do_chunks = have_prefill;
+          do_dec = !have_prefill;
+        }
+        n_dec = do_dec ? min(total_dec, mbt) : 0;
+        budget = (int64_t)mbt - n_dec;
+      }
       const int rank = dec_before + __popc(dm & lt);
       const bool is_dec = do_dec && dcand && rank < mbt;
       dec_before += __popc(dm);
       int32_t plan = is_dec ? -1 : -2;
-      if (is_dec) c_l += (int64_t)pr + em;  // DecodeSlot.context_len = prompt + emitted
+      if (is_dec) {
+        c_l += (int64_t)pr + e;  // DecodeSlot.context_len = prompt + emitted
+        min_rem = min(min_rem, op - e);
+      }
       if (do_chunks && __any_sync(kFull, mid)) {
-        const int64_t want = mid ? min(chunk, (int64_t)(pr - dn)) : 0;
+        const int64_t want = mid ? min((int64_t)chunk, (int64_t)(pr - dn)) : 0;
         const int64_t incl = warp_incl_scan_i64(want);
         const int64_t E = want_before + incl - want;  // tokens taken by earlier chunks
         const bool chosen = mid && budget - E > 0;
@@ -294,21 +390,18 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       if (v) sl.plan[i] = plan;
     }
     // tokens the chunks consumed: every chosen chunk took `want` except possibly the last
-    {
-      const int64_t took = min(want_before, budget > 0 ? budget : 0);
-      budget -= took;
-    }
+    budget -= min(want_before, budget > 0 ? budget : (int64_t)0);
 
     // ---- admission from the waiting head: strict FCFS, KV + slot + budget gates
     int n_adm = 0;
-    if (do_chunks && budget > 0 && w_head < fut) {
-      int64_t free_l = free0, slots = max_running - n_act;
+    if (do_chunks && budget > 0 && waiting) {
+      int64_t free_l = free0, slots = (int64_t)max_running - n_act;
       while (budget > 0 && slots > 0 && w_head + n_adm < fut) {
-        const int64_t idx = w_head + n_adm + lane;
+        const int32_t idx = w_head + n_adm + lane;
         const bool cand = idx < fut && lane < slots;
-        const int64_t pr = cand ? __ldg(prm + idx) : 0;
-        const int64_t need = blocks_of(pr, bk);
-        const int64_t want = min(chunk, pr);
+        const int32_t pr = cand ? __ldg(prm + idx) : 0;
+        const int64_t need = blk.ceil_div(pr);
+        const int64_t want = min((int64_t)chunk, (int64_t)pr);
         const int64_t NEi = warp_incl_scan_i64(cand ? need : 0);
         const int64_t WEi = warp_incl_scan_i64(cand ? want : 0);
         const int64_t NE = NEi - need, WE = WEi - want;
@@ -318,8 +411,8 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         if (lane < k) {
           const int slot = n_act + n_adm + lane;
           const int64_t take = min(want, budget - WE);
-          sl.req[slot] = (int32_t)idx;
-          sl.prompt[slot] = (int32_t)pr;
+          sl.req[slot] = idx;
+          sl.prompt[slot] = pr;
           const int32_t op = __ldg(outp + idx);
           sl.output[slot] = op;
           sl.done[slot] = 0;
@@ -345,93 +438,154 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     __syncwarp();
 
     if (n_dec == 0 && n_chunk == 0) {
-      if (n_act > 0 || w_head < fut) {  // oracle.py:78-80 -> _diagnose_stall
+      if (n_act > 0 || waiting) {  // oracle.py:78-80 -> _diagnose_stall
         r.status = n_act > 0 ? TW_SIM_STALLED_ACTIVE : TW_SIM_STALLED_KV;
         break;
       }
-      // idle until the next arrival (oracle.py:81-83)
-      const int sh = (int)(fut - cbase);
-      const int64_t t_next = (sh < 32) ? __shfl_sync(kFull, cts, sh) : __ldg(ts + fut);
-      now = epoch + t_next;
-      if (tk_on) tk_advance(g, ts, n, epoch, S, TP, 0, now, 0, now);
+      now = next_arr;  // idle until the next arrival (oracle.py:81-83)
+      if (tk_on) tk_advance(g, ts, n, epoch, 0, now, 0);
       continue;
     }
 
     // ---- predict (oracle.py:85-86)
     const int64_t P = (int64_t)__reduce_add_sync(kFull, (unsigned)p_l);  // P <= max_batch_tokens
-    const int64_t C = warp_sum_i64_redux(c_l);
-    const int64_t d = predict_warp(ps, cfg.pred_id, P, n_dec, C);
+    const int64_t C = pc.uses_c ? warp_sum_i64_redux(c_l) : 0;
+    const int64_t d = predict_cached(pc, ps, cfg.pred_id, P, n_dec, C);
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
       r.pred_code = (int32_t)d;
       break;
     }
+
+    // ---- macro step: a decode-only run of K identical steps
+    if (macro_ok && n_chunk == 0 && n_dec == n_act) {
+      const int K_f = __reduce_min_sync(kFull, min_rem);  // first finish (>= 1)
+      int64_t K = K_f;
+      if (!waiting && fut < n && d > 0) {
+        // the plan after step j sees arrivals <= now + j*d: stop at the first crossing
+        const int64_t ka = (next_arr - now + d - 1) / d;
+        if (ka < K) K = ka;
+      }
+      if (K >= 2) {
+        const int D = n_act;
+        const int64_t now0 = now;
+        const int32_t step0 = step;
+        if (tk_on) {
+          for (int64_t j = 0; j < K; j++) tk_advance(g, ts, n, epoch, S, now0 + j * d, d);
+        }
+        // events of steps 1..K-1: D OUTPUT_TOKENs each, flattened over the lanes
+        const int64_t body = (K - 1) * (int64_t)D;
+        if (body > 0) {
+          const int q32 = 32 / D, r32 = 32 % D;
+          int64_t j = lane / D;
+          int i = lane - (int)j * D;
+          for (int64_t e = lane; e < body; e += 32) {
+            em.event(n_events + e, sl.req[i], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
+            i += r32;
+            j += q32;
+            if (i >= D) { i -= D; j++; }
+          }
+        }
+        // step K: every slot decodes; those reaching their output finish; compact
+        const int64_t nowK = now0 + K * d;
+        const int32_t stepK = step0 + (int32_t)K;
+        int64_t pos = n_events + body;
+        int kept = 0;
+        for (int b = 0; b < D; b += 32) {
+          const int i = b + lane;
+          const bool v = i < D;
+          int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0;
+          if (v) {
+            rq = sl.req[i];
+            pr = sl.prompt[i];
+            op = sl.output[i];
+            dn = sl.done[i];
+            e = sl.emit[i] + (int32_t)K;
+          }
+          const bool fin = v && e >= op;
+          const unsigned fm = __ballot_sync(kFull, fin);
+          if (v) {
+            const int64_t my = pos + i - b + __popc(fm & lt);
+            em.event(my, rq, TW_EV_OUTPUT_TOKEN, nowK, stepK);
+            if (fin) {
+              em.event(my + 1, rq, TW_EV_FINISHED, nowK, stepK);
+              if (em.finish) em.finish[rq] = nowK;
+            }
+          }
+          pos += min(32, D - b) + __popc(fm);
+          const bool keep = v && !fin;
+          const unsigned km = __ballot_sync(kFull, keep);
+          __syncwarp();
+          if (keep) {
+            const int np = kept + __popc(km & lt);
+            sl.req[np] = rq;
+            sl.prompt[np] = pr;
+            sl.output[np] = op;
+            sl.done[np] = dn;
+            sl.emit[np] = e;
+          }
+          kept += __popc(km);
+          __syncwarp();
+        }
+        n_events = pos;
+        n_act = kept;
+        now = nowK;
+        step = stepK;
+        continue;
+      }
+    }
+
     step += 1;
     const int64_t base = now;
     now += d;
-    if (tk_on) tk_advance(g, ts, n, epoch, S, TP, 1, base, d, now);  // WorkerGrid stage deadlines
+    if (tk_on) tk_advance(g, ts, n, epoch, S, base, d);  // WorkerGrid stage deadlines
 
     // ---- apply (oracle.py:88-112): chunks' events first, then decodes', in slot order
     const int n_tot = n_act + n_adm;
     const int chunk_ev_total = __reduce_add_sync(kFull, (unsigned)chunk_ev);
     int64_t pos_c = n_events, pos_d = n_events + chunk_ev_total;
     int kept = 0;
-    int64_t held_l = 0;
     for (int b = 0; b < n_tot; b += 32) {
       const int i = b + lane;
       const bool v = i < n_tot;
-      int32_t rq = 0, pr = 0, op = 0, dn = 0, em = 0, plan = -2;
+      int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0, plan = -2;
       if (v) {
         rq = sl.req[i];
         pr = sl.prompt[i];
         op = sl.output[i];
         dn = sl.done[i];
-        em = sl.emit[i];
+        e = sl.emit[i];
         plan = sl.plan[i];
       }
-      int nev = 0, k0 = 0, k1 = 0;
+      int nev = 0, k0 = 0;
       bool fin = false;
       const bool is_chunk = plan >= 0, is_dec = plan == -1;
       if (is_chunk) {
         dn += plan;
         if (dn >= pr) {
-          em = 1;
+          e = 1;
           nev = 1;
           k0 = TW_EV_FIRST_TOKEN;
-          if (em >= op) { nev = 2; k1 = TW_EV_FINISHED; fin = true; }
+          if (e >= op) { nev = 2; fin = true; }
         }
       } else if (is_dec) {
-        em += 1;
+        e += 1;
         nev = 1;
         k0 = TW_EV_OUTPUT_TOKEN;
-        if (em >= op) { nev = 2; k1 = TW_EV_FINISHED; fin = true; }
+        if (e >= op) { nev = 2; fin = true; }
       }
       const unsigned c1 = __ballot_sync(kFull, is_chunk && nev >= 1);
       const unsigned c2 = __ballot_sync(kFull, is_chunk && nev == 2);
       const unsigned d1 = __ballot_sync(kFull, is_dec && nev >= 1);
       const unsigned d2 = __ballot_sync(kFull, is_dec && nev == 2);
       if (nev) {
-        const int64_t pos = is_chunk ? pos_c + __popc(c1 & lt) + __popc(c2 & lt)
+        const int64_t ps0 = is_chunk ? pos_c + __popc(c1 & lt) + __popc(c2 & lt)
                                      : pos_d + __popc(d1 & lt) + __popc(d2 & lt);
-        dig += tw_event_hash((uint64_t)pos, (uint64_t)rq, (uint64_t)k0, now, step);
-        if (k0 == TW_EV_FIRST_TOKEN && first) first[rq] = now;
-        if (evp && pos < ev_cap) {
-          tw_event e;
-          e.ts_ns = now;
-          e.step = (int32_t)step;
-          e.req_kind = (rq << 2) | k0;
-          evp[pos] = e;
-        }
+        em.event(ps0, rq, k0, now, step);
+        if (k0 == TW_EV_FIRST_TOKEN && em.first) em.first[rq] = now;
         if (nev == 2) {
-          dig += tw_event_hash((uint64_t)(pos + 1), (uint64_t)rq, (uint64_t)k1, now, step);
-          if (finish) finish[rq] = now;
-          if (evp && pos + 1 < ev_cap) {
-            tw_event e;
-            e.ts_ns = now;
-            e.step = (int32_t)step;
-            e.req_kind = (rq << 2) | k1;
-            evp[pos + 1] = e;
-          }
+          em.event(ps0 + 1, rq, TW_EV_FINISHED, now, step);
+          if (em.finish) em.finish[rq] = now;
         }
       }
       pos_c += __popc(c1) + __popc(c2);
@@ -446,21 +600,19 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         sl.prompt[np] = pr;
         sl.output[np] = op;
         sl.done[np] = dn;
-        sl.emit[np] = em;
-        const int64_t h0 = blocks_of(pr, bk), h1 = blocks_of((int64_t)dn + em, bk);
-        held_l += h0 > h1 ? h0 : h1;  // _held (oracle.py:43-46)
+        sl.emit[np] = e;
       }
       kept += __popc(km);
       __syncwarp();
     }
     n_events = pos_d;
-    if (evp && n_events > ev_cap) overflow = 1;
-    held_sum = warp_sum_i64_redux(held_l);
     w_head += n_adm;
     n_act = kept;
   }
 
+  if (em.evp && n_events > em.ev_cap) overflow = 1;
   // digest: sum of lane partials mod 2^64
+  uint64_t dig = em.dig;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dig += __shfl_xor_sync(kFull, dig, o);
   r.final_now_ns = now;
