@@ -256,6 +256,12 @@ int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
 int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
                        int32_t* slot_capacity);
 
+/* Opt-in instrumentation for the next tw_sim_many calls on this thread: when set
+ * (device pointer, 8 int64 per config; NULL disables), each config records
+ * {SM cycles, normal steps, macro-stepped runs, steps covered by runs, Timekeeper
+ * cycles, run-event cycles, Timekeeper broadcasts, 0}. */
+int tw_sim_set_profile(int64_t* per_config_8xi64);
+
 /* ---- misc ------------------------------------------------------------------ */
 int tw_abi_version(void);
 const char* tw_last_error(void);

@@ -134,6 +134,7 @@ EXPORTED_SYMBOLS = (
     "tw_tk_resolve",
     "tw_sim_many",
     "tw_sim_last_launch",
+    "tw_sim_set_profile",
     "tw_abi_version",
     "tw_last_error",
     "tw_launch_count",
@@ -162,6 +163,7 @@ _SIGNATURES = {
         [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P],
     ),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
+    "tw_sim_set_profile": (_I32, [_P]),
     "tw_abi_version": (_I32, []),
     "tw_last_error": (ctypes.c_char_p, []),
     "tw_launch_count": (_I64, []),

@@ -53,6 +53,7 @@ struct SimParams {
   tw_event* ev;
   int32_t* counter;
   int32_t cap;
+  int64_t* prof;  // optional: per config {cycles, normal steps, runs, run steps, tk cycles, run-event cycles, tk rounds, -}
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -104,7 +105,8 @@ struct Slots {
   int32_t* output;
   int32_t* done;
   int32_t* emit;
-  int32_t* plan;  // >= 0 chunk tokens, -1 decode, -2 idle (this step)
+  int32_t* plan;   // >= 0 chunk tokens, -1 decode, -2 idle (this step)
+  int32_t* dlist;  // this step's decode slots in order (rank -> slot)
 };
 
 // Lane-distributed window over a workload's arrival offsets: lane l holds
@@ -158,26 +160,97 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
   }
 }
 
-// Rounds until V >= base + d. S == 0: idle jump (only the dispatcher drives time).
-// Stage deadlines: WorkerGrid.execute (engine.py:434-442).
-__device__ __forceinline__ void tk_advance(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
-                                           int S, int64_t base, int64_t d) {
-  const int64_t end = base + d;
-  int64_t per = 0;
+// K consecutive steps of duration d from now0 through the Timekeeper (a macro run, or
+// K = 1 for a normal step). The deadlines form a fixed pattern per step (stage s ends
+// at base + per*(s+1), the last at base + d), so the walk keeps (step k, stage s) and
+// only resolves targets beyond V; a V that jumped several steps ahead (the FakeClock
+// wall outrunning short steps) is skipped in O(1). Each resolve is one BarrierCore
+// round with t_min = min(dispatcher's next arrival, the stage deadline).
+__device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+                                       int S, int64_t now0, int64_t d, int64_t K) {
+  int64_t per = d;
   if (S > 1) per = (d >= 0 && d < 0x7fffffffLL) ? (int64_t)((uint32_t)d / (uint32_t)S) : d / S;
+  const int64_t end_all = now0 + K * d;
+  const int64_t cj = g.cooldown > 0 ? g.conv_cooldown : 0;
+  const int64_t gap = (S > 1) ? min(per, d - per * (S - 1)) : d;
+  const int64_t maxgap = (S > 1) ? max(per, d - per * (S - 1)) : d;
+  const bool steady_ok = gap > cj && (S == 1 || per > 0);
+  const bool wallbound_ok = cj > 0 && d > 0 && maxgap <= cj;
+  int64_t k = 0;
+  int s = 0;
+  int64_t base = now0;
+  int64_t tgt = (S == 1) ? now0 + d : now0 + per;
+  for (;;) {
+    tk_dispatch(g, ts, n, epoch);
+    if (g.V >= end_all) return;
+    if (tgt <= g.V) {
+      // the deadline is already behind V: move to the first one beyond it
+      if (d > 0 && g.V - base >= 4 * d) {  // V far ahead: skip whole steps at once
+        const int64_t jump = (g.V - base) / d;
+        k += jump;
+        base += jump * d;
+        s = 0;
+      }
+      for (;;) {
+        tgt = (s == S - 1) ? base + d : base + per * (s + 1);
+        if (tgt > g.V) break;
+        if (++s == S) {
+          s = 0;
+          k++;
+          base += d;
+        }
+      }
+    }
+    const int64_t t_min = g.disp_ts < tgt ? g.disp_ts : tgt;
+    tk_resolve(g, t_min);
+    // Steady state: the round broadcast and landed V on its deadline. If the stage
+    // gaps exceed the cooldown step cJ, every later deadline below the dispatcher's
+    // target is resolved the same way (sleep cJ, broadcast, V := deadline), so R of
+    // them are closed-form: wall += R*cJ, seq += R, offset = t_R - wall, V = t_R.
+    // Wall-bound state: consecutive deadlines are at most cJ apart and the offset is at
+    // least cJ. Every round then sleeps cJ, broadcasts without growing the offset
+    // (its target lies within V + cJ) and moves V by exactly cJ, so the remaining
+    // rounds up to end_all are R = ceil((end_all - V) / cJ): wall += R*cJ, seq += R.
+    // Dispatcher targets inside that window change no clock value, only which
+    // arrivals have been passed (tk_dispatch above).
+    if (wallbound_ok && g.last_bcast == g.wall && g.offset >= cj && g.V < end_all) {
+      const int64_t R = (end_all - g.V + cj - 1) / cj;
+      g.wall += R * cj;
+      g.seq += R;
+      g.last_bcast = g.wall;
+      g.V += R * cj;
+      continue;
+    }
+    if (steady_ok && g.V == t_min && g.last_bcast == g.wall) {
+      int64_t X = end_all;  // last deadline we may cover (< dispatcher target)
+      if (g.disp_ts <= X) X = g.disp_ts - 1;
+      if (X > g.V) {
+        // deadlines <= Y: full steps f contribute S each, plus the stages of the partial step
+        const int64_t fx = (X - now0) / d, rx = X - now0 - fx * d;
+        const int64_t fv = (g.V - now0) / d, rv = g.V - now0 - fv * d;
+        const int64_t px = (S > 1) ? min((int64_t)(S - 1), rx / per) : 0;
+        const int64_t pv = (S > 1) ? min((int64_t)(S - 1), rv / per) : 0;
+        const int64_t R = (fx * S + px) - (fv * S + pv);
+        if (R > 0) {
+          const int64_t tR = now0 + fx * d + per * px;  // largest deadline <= X
+          g.wall += R * cj;
+          g.seq += R;
+          g.last_bcast = g.wall;
+          g.offset = tR - g.wall;
+          g.V = tR;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+                                        int64_t end) {
+  // idle jump: only the dispatcher drives time (its target is <= end while V < end)
   for (;;) {
     tk_dispatch(g, ts, n, epoch);
     if (g.V >= end) return;
-    int64_t stage = end;  // S == 0 (idle) -> the dispatcher's target is <= end
-    if (S > 1) {
-      for (int s = 0; s < S - 1; s++) {
-        const int64_t e = base + per * (s + 1);
-        if (e > g.V) { stage = e; break; }
-      }
-    } else if (S == 0) {
-      stage = INT64_MAX;
-    }
-    tk_resolve(g, g.disp_ts < stage ? g.disp_ts : stage);
+    tk_resolve(g, g.disp_ts);
   }
 }
 
@@ -218,6 +291,8 @@ struct Emitter {
 __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
+  const long long t_start = clock64();
+  int64_t n_normal = 0, n_runs = 0, n_run_steps = 0, tk_cyc = 0, ev_cyc = 0;
   const tw_sim_cfg cfg = p.cfgs[c];
   tw_sim_result r;
   r.final_now_ns = cfg.epoch_ns;
@@ -338,7 +413,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     int n_chunk = 0, chunk_ev = 0, n_dec = 0;
     int dec_before = 0;
     int64_t want_before = 0, budget = mbt;
-    int min_rem = 0x7fffffff;  // min (output - emitted) over decoders (macro-step horizon)
+    int min_rem = 0x7fffffff;  // macro-step horizon: decoders' remaining outputs, chunks' repeats
     for (int b = 0; b < (n_act > 0 ? n_act : 1); b += 32) {
       const int i = b + lane;
       const bool v = i < n_act;
@@ -371,6 +446,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       if (is_dec) {
         c_l += (int64_t)pr + e;  // DecodeSlot.context_len = prompt + emitted
         min_rem = min(min_rem, op - e);
+        sl.dlist[rank] = i;
       }
       if (do_chunks && __any_sync(kFull, mid)) {
         const int64_t want = mid ? min((int64_t)chunk, (int64_t)(pr - dn)) : 0;
@@ -383,6 +459,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           p_l += take;
           c_l += dn;  // PrefillChunk.context_len_before = done_prefill
           if (dn + take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
+          // steps this chunk repeats with the same take before the one that completes
+          // the prompt: ceil(rem / take) - 1
+          min_rem = min(min_rem, (int)((uint32_t)(pr - dn - 1) / (uint32_t)take));
         }
         n_chunk += __popc(__ballot_sync(kFull, chosen));
         want_before += __shfl_sync(kFull, incl, 31);
@@ -443,7 +522,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         break;
       }
       now = next_arr;  // idle until the next arrival (oracle.py:81-83)
-      if (tk_on) tk_advance(g, ts, n, epoch, 0, now, 0);
+      if (tk_on) tk_idle(g, ts, n, epoch, now);
       continue;
     }
 
@@ -457,62 +536,72 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       break;
     }
 
-    // ---- macro step: a decode-only run of K identical steps
-    if (macro_ok && n_chunk == 0 && n_dec == n_act) {
-      const int K_f = __reduce_min_sync(kFull, min_rem);  // first finish (>= 1)
-      int64_t K = K_f;
+    // ---- macro step: a run of K steps with an identical plan.
+    // With no admission this step, the same decoders decode and the same chunks take
+    // the same tokens until a decoder finishes (min remaining output, finishing step
+    // included), a chunk reaches its prompt's last chunk (excluded), or a new arrival
+    // becomes visible to an empty queue; a blocked queue head stays blocked (slots and
+    // budget constant, KV free non-increasing). P and D are constant, so is d.
+    if (macro_ok && n_adm == 0) {
+      int64_t K = __reduce_min_sync(kFull, min_rem);
       if (!waiting && fut < n && d > 0) {
         // the plan after step j sees arrivals <= now + j*d: stop at the first crossing
         const int64_t ka = (next_arr - now + d - 1) / d;
         if (ka < K) K = ka;
       }
       if (K >= 2) {
-        const int D = n_act;
+        const int D = n_dec;  // events per step: one OUTPUT_TOKEN per decode slot
         const int64_t now0 = now;
         const int32_t step0 = step;
-        if (tk_on) {
-          for (int64_t j = 0; j < K; j++) tk_advance(g, ts, n, epoch, S, now0 + j * d, d);
-        }
-        // events of steps 1..K-1: D OUTPUT_TOKENs each, flattened over the lanes
+        long long c0 = clock64();
+        if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);
+        long long c1 = clock64();
+        tk_cyc += c1 - c0;
+        // events of steps 1..K-1, flattened over the lanes: e -> (step j, decode rank i)
         const int64_t body = (K - 1) * (int64_t)D;
         if (body > 0) {
           const int q32 = 32 / D, r32 = 32 % D;
           int64_t j = lane / D;
           int i = lane - (int)j * D;
           for (int64_t e = lane; e < body; e += 32) {
-            em.event(n_events + e, sl.req[i], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
+            em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
             i += r32;
             j += q32;
             if (i >= D) { i -= D; j++; }
           }
         }
-        // step K: every slot decodes; those reaching their output finish; compact
+        // step K: decoders emit (and may finish), chunks advance K takes; compact
         const int64_t nowK = now0 + K * d;
         const int32_t stepK = step0 + (int32_t)K;
         int64_t pos = n_events + body;
         int kept = 0;
-        for (int b = 0; b < D; b += 32) {
+        for (int b = 0; b < n_act; b += 32) {
           const int i = b + lane;
-          const bool v = i < D;
-          int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0;
+          const bool v = i < n_act;
+          int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0, plan = -2;
           if (v) {
             rq = sl.req[i];
             pr = sl.prompt[i];
             op = sl.output[i];
             dn = sl.done[i];
-            e = sl.emit[i] + (int32_t)K;
+            e = sl.emit[i];
+            plan = sl.plan[i];
           }
-          const bool fin = v && e >= op;
+          const bool is_dec = plan == -1;
+          if (is_dec) e += (int32_t)K;
+          if (plan >= 0) dn += plan * (int32_t)K;
+          const bool fin = is_dec && e >= op;
+          const unsigned dm = __ballot_sync(kFull, is_dec);
           const unsigned fm = __ballot_sync(kFull, fin);
-          if (v) {
-            const int64_t my = pos + i - b + __popc(fm & lt);
+          if (is_dec) {
+            const int64_t my = pos + __popc(dm & lt) + __popc(fm & lt);
             em.event(my, rq, TW_EV_OUTPUT_TOKEN, nowK, stepK);
             if (fin) {
               em.event(my + 1, rq, TW_EV_FINISHED, nowK, stepK);
               if (em.finish) em.finish[rq] = nowK;
             }
           }
-          pos += min(32, D - b) + __popc(fm);
+          pos += __popc(dm) + __popc(fm);
           const bool keep = v && !fin;
           const unsigned km = __ballot_sync(kFull, keep);
           __syncwarp();
@@ -531,14 +620,22 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         n_act = kept;
         now = nowK;
         step = stepK;
+        ev_cyc += clock64() - c1;
+        n_runs++;
+        n_run_steps += K;
         continue;
       }
     }
 
     step += 1;
+    n_normal++;
     const int64_t base = now;
     now += d;
-    if (tk_on) tk_advance(g, ts, n, epoch, S, base, d);  // WorkerGrid stage deadlines
+    {
+      const long long c0 = clock64();
+      if (tk_on) tk_run(g, ts, n, epoch, S, base, d, 1);  // WorkerGrid stage deadlines
+      tk_cyc += clock64() - c0;
+    }
 
     // ---- apply (oracle.py:88-112): chunks' events first, then decodes', in slot order
     const int n_tot = n_act + n_adm;
@@ -625,7 +722,19 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     r.tk_wall_ns = g.wall;
   }
   if (overflow) r.status |= 1 << 8;
-  if (lane == 0) p.res[c] = r;
+  if (lane == 0) {
+    p.res[c] = r;
+    if (p.prof) {
+      p.prof[8 * c] = clock64() - t_start;
+      p.prof[8 * c + 1] = n_normal;
+      p.prof[8 * c + 2] = n_runs;
+      p.prof[8 * c + 3] = n_run_steps;
+      p.prof[8 * c + 4] = tk_cyc;
+      p.prof[8 * c + 5] = ev_cyc;
+      p.prof[8 * c + 6] = g.seq;
+      p.prof[8 * c + 7] = 0;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kSimThreads) k_sim(SimParams p) {
@@ -634,7 +743,7 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimParams p) {
   char* ps = smem + 128;
   tma_stage_to_smem(ps, p.pset, p.pset_bytes, bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 6 * p.cap;
+  int32_t* base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 7 * p.cap;
   Slots sl;
   sl.req = base;
   sl.prompt = base + p.cap;
@@ -642,6 +751,7 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimParams p) {
   sl.done = base + 3 * p.cap;
   sl.emit = base + 4 * p.cap;
   sl.plan = base + 5 * p.cap;
+  sl.dlist = base + 6 * p.cap;
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = atomicAdd(p.counter, 1);
@@ -654,6 +764,7 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimParams p) {
 }
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
+static thread_local int64_t* g_prof = nullptr;
 
 }  // namespace twb
 
@@ -685,7 +796,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
     return TW_ENOSMEM;
   }
   const uint32_t pset_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
-  const size_t smem = 128 + pset_smem + (size_t)kSimWarps * 6 * sizeof(int32_t) * cap;
+  const size_t smem = 128 + pset_smem + (size_t)kSimWarps * 7 * sizeof(int32_t) * cap;
   int dev = 0, sms = 148, per_sm = 0, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -721,6 +832,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   p.ev = ev;
   p.counter = reinterpret_cast<int32_t*>(scratch);
   p.cap = cap;
+  p.prof = g_prof;
   k_sim<<<(int)grid, kSimThreads, smem, s>>>(p);
   count_launch();
   g_last[0] = (int32_t)grid;
@@ -728,6 +840,11 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   g_last[2] = (int32_t)smem;
   g_last[3] = cap;
   return check_launch("tw_sim_many");
+}
+
+extern "C" int tw_sim_set_profile(int64_t* per_config_8xi64) {
+  g_prof = per_config_8xi64;
+  return TW_OK;
 }
 
 extern "C" int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes, int32_t* slot_capacity) {

@@ -1,0 +1,39 @@
+"""Per-config critical-path profile of k_sim (tw_sim_set_profile) on the 1,024 sweep."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2601_00397_b200 import _lib, presets  # noqa: E402
+from paper_2601_00397_b200.sweep import DeviceSweep  # noqa: E402
+
+sw = presets.sweep_1024()
+dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+prof = torch.zeros(8 * len(sw), dtype=torch.int64, device="cuda")
+_lib.load().tw_sim_set_profile(prof.data_ptr())
+for _ in range(3):
+    dev.run()
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record(); dev.run(); e.record(); e.synchronize()
+ms = s.elapsed_time(e)
+_lib.load().tw_sim_set_profile(None)
+pr = prof.view(-1, 8).cpu().numpy()
+res = dev.fetch().results
+cyc, normal, runs, run_steps, tkc, evc, rounds, _ = pr.T
+order = np.argsort(-cyc)
+print(f"kernel {ms:.2f} ms; max config {cyc.max()/1.965e6:.2f} ms @1.965GHz, median {np.median(cyc)/1.965e6:.2f} ms")
+print(f"steps total {res['steps'].sum()}, normal {normal.sum()}, runs {runs.sum()}, run steps {run_steps.sum()}")
+print(f"cycles per normal step (approx, all configs) {cyc.sum()/max(1,normal.sum()+runs.sum()):.0f} per normal-or-run")
+for c in order[:12]:
+    lab = sw.configs[c].label
+    print(c, f"{cyc[c]/1.965e6:.2f}ms", "steps", res['steps'][c], "normal", normal[c], "runs", runs[c], "runsteps", run_steps[c],
+          f"tk {100*tkc[c]/cyc[c]:.0f}% ev {100*evc[c]/cyc[c]:.0f}% bcasts {rounds[c]}", lab)
+# fit cycles ~ a*normal + b*runs + c*run_steps
+A = np.stack([normal, runs, run_steps], 1).astype(float)
+coef, *_ = np.linalg.lstsq(A, cyc.astype(float), rcond=None)
+print("fit cycles/normal step, /run, /run step:", coef.round(1))
+json.dump({"ms": ms, "cyc": cyc.tolist(), "normal": normal.tolist(), "runs": runs.tolist(), "run_steps": run_steps.tolist()},
+          open("gpurun_out/prof_sim.json", "w"))
