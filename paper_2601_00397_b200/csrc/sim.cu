@@ -81,6 +81,13 @@ __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
   return v;
 }
 
+// a / b for a >= 0, b > 0: one 32-bit divide when both fit (the common case for
+// nanosecond spans below 4.29 s), the 64-bit routine otherwise.
+__device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) {
+  if ((((uint64_t)a | (uint64_t)b) >> 32) == 0) return (int64_t)((uint32_t)a / (uint32_t)b);
+  return a / b;
+}
+
 // ceil(t / bk) for 0 <= t < 2^31 with a per-config magic reciprocal (no IDIV chain):
 // q0 = umulhi(t, floor((2^32-1)/bk)) is at most 2 below floor(t/bk).
 struct Blocks {
@@ -169,7 +176,7 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
   int64_t per = d;
-  if (S > 1) per = (d >= 0 && d < 0x7fffffffLL) ? (int64_t)((uint32_t)d / (uint32_t)S) : d / S;
+  if (S > 1) per = div_nn(d, S);
   const int64_t end_all = now0 + K * d;
   const int64_t cj = g.cooldown > 0 ? g.conv_cooldown : 0;
   const int64_t gap = (S > 1) ? min(per, d - per * (S - 1)) : d;
@@ -186,7 +193,7 @@ __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts
     if (tgt <= g.V) {
       // the deadline is already behind V: move to the first one beyond it
       if (d > 0 && g.V - base >= 4 * d) {  // V far ahead: skip whole steps at once
-        const int64_t jump = (g.V - base) / d;
+        const int64_t jump = div_nn(g.V - base, d);
         k += jump;
         base += jump * d;
         s = 0;
@@ -214,7 +221,7 @@ __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts
     // Dispatcher targets inside that window change no clock value, only which
     // arrivals have been passed (tk_dispatch above).
     if (wallbound_ok && g.last_bcast == g.wall && g.offset >= cj && g.V < end_all) {
-      const int64_t R = (end_all - g.V + cj - 1) / cj;
+      const int64_t R = div_nn(end_all - g.V + cj - 1, cj);
       g.wall += R * cj;
       g.seq += R;
       g.last_bcast = g.wall;
@@ -226,10 +233,10 @@ __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts
       if (g.disp_ts <= X) X = g.disp_ts - 1;
       if (X > g.V) {
         // deadlines <= Y: full steps f contribute S each, plus the stages of the partial step
-        const int64_t fx = (X - now0) / d, rx = X - now0 - fx * d;
-        const int64_t fv = (g.V - now0) / d, rv = g.V - now0 - fv * d;
-        const int64_t px = (S > 1) ? min((int64_t)(S - 1), rx / per) : 0;
-        const int64_t pv = (S > 1) ? min((int64_t)(S - 1), rv / per) : 0;
+        const int64_t fx = div_nn(X - now0, d), rx = X - now0 - fx * d;
+        const int64_t fv = div_nn(g.V - now0, d), rv = g.V - now0 - fv * d;
+        const int64_t px = (S > 1) ? min((int64_t)(S - 1), div_nn(rx, per)) : 0;
+        const int64_t pv = (S > 1) ? min((int64_t)(S - 1), div_nn(rv, per)) : 0;
         const int64_t R = (fx * S + px) - (fv * S + pv);
         if (R > 0) {
           const int64_t tR = now0 + fx * d + per * px;  // largest deadline <= X
@@ -499,6 +506,8 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           sl.plan[slot] = (int32_t)take;
           p_l += take;
           if (take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
+          // repeats of this first take before the completing chunk (macro horizon)
+          min_rem = min(min_rem, take > 0 ? (int)((uint32_t)(pr - 1) / (uint32_t)take) : 0);
         }
         if (k == 0) break;
         const int64_t tot_need = __shfl_sync(kFull, NEi, k - 1);
@@ -537,16 +546,18 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     }
 
     // ---- macro step: a run of K steps with an identical plan.
-    // With no admission this step, the same decoders decode and the same chunks take
+    // After this step's admissions (the admitted become mid-prefill chunk slots with the
+    // same take), the same decoders decode and the same chunks take
     // the same tokens until a decoder finishes (min remaining output, finishing step
     // included), a chunk reaches its prompt's last chunk (excluded), or a new arrival
     // becomes visible to an empty queue; a blocked queue head stays blocked (slots and
     // budget constant, KV free non-increasing). P and D are constant, so is d.
-    if (macro_ok && n_adm == 0) {
+    if (macro_ok) {
       int64_t K = __reduce_min_sync(kFull, min_rem);
-      if (!waiting && fut < n && d > 0) {
+      // an emptied queue can admit the next arrival; a non-empty one stays blocked
+      if (w_head + n_adm == fut && fut < n && d > 0) {
         // the plan after step j sees arrivals <= now + j*d: stop at the first crossing
-        const int64_t ka = (next_arr - now + d - 1) / d;
+        const int64_t ka = div_nn(next_arr - now + d - 1, d);
         if (ka < K) K = ka;
       }
       if (K >= 2) {
@@ -575,9 +586,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         const int32_t stepK = step0 + (int32_t)K;
         int64_t pos = n_events + body;
         int kept = 0;
-        for (int b = 0; b < n_act; b += 32) {
+        const int n_tot = n_act + n_adm;  // admitted this step: chunk slots at the end
+        for (int b = 0; b < n_tot; b += 32) {
           const int i = b + lane;
-          const bool v = i < n_act;
+          const bool v = i < n_tot;
           int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0, plan = -2;
           if (v) {
             rq = sl.req[i];
@@ -618,6 +630,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         }
         n_events = pos;
         n_act = kept;
+        w_head += n_adm;
         now = nowK;
         step = stepK;
         ev_cyc += clock64() - c1;
