@@ -179,7 +179,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("TWB200_LIB") or LIB_PATH  # override for A/B builds
         if not os.path.exists(p):
             raise NativeLibraryMissing(
                 f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

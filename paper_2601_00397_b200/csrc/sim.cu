@@ -81,12 +81,11 @@ __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
   return v;
 }
 
-// a / b for a >= 0, b > 0: one 32-bit divide when both fit (the common case for
-// nanosecond spans below 4.29 s), the 64-bit routine otherwise.
-__device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) {
-  if ((((uint64_t)a | (uint64_t)b) >> 32) == 0) return (int64_t)((uint32_t)a / (uint32_t)b);
-  return a / b;
-}
+// a / b for a >= 0, b > 0. (A hand-made 32-bit fast path measured 13% slower than
+// the compiler's 64-bit routine, which already short-cuts small operands; a variant
+// that moved the Timekeeper rounds to a partner warp behind a shared-memory ring
+// measured 10-18% slower than keeping them inline — see profiles/README.md.)
+__device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) { return a / b; }
 
 // ceil(t / bk) for 0 <= t < 2^31 with a per-config magic reciprocal (no IDIV chain):
 // q0 = umulhi(t, floor((2^32-1)/bk)) is at most 2 below floor(t/bk).
