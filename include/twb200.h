@@ -257,10 +257,11 @@ int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
                        int32_t* slot_capacity);
 
 /* Opt-in instrumentation for the next tw_sim_many calls on this thread: when set
- * (device pointer, 8 int64 per config; NULL disables), each config records
- * {SM cycles, normal steps, macro-stepped runs, steps covered by runs, Timekeeper
- * cycles, run-event cycles, Timekeeper broadcasts, 0}. */
-int tw_sim_set_profile(int64_t* per_config_8xi64);
+ * (device pointer, 16 int64 per config; NULL disables), each config records
+ * {SM cycles, normal steps, macro runs, steps covered by runs, Timekeeper cycles,
+ * run-event cycles, Timekeeper broadcasts, arrival cycles, plan cycles, admission
+ * cycles, predict cycles, apply cycles, 0, 0, 0, 0}. */
+int tw_sim_set_profile(int64_t* per_config_16xi64);
 
 /* ---- misc ------------------------------------------------------------------ */
 int tw_abi_version(void);

@@ -30,6 +30,20 @@
 
 namespace twb {
 
+// Phase boundaries of the event loop. With -DTWB_PROFILE_PHASES they read the SM clock
+// (scripts/prof_sim.py); otherwise they are compiler memory barriers: keeping ptxas from
+// moving shared/global accesses across phases measured 14% faster on the 1,024-config
+// sweep than letting it schedule freely (15.6 -> 13.4 ms; profiles/README.md).
+#if defined(TWB_PROFILE_PHASES)
+#define TWB_CLK() clock64()
+#else
+__device__ __forceinline__ long long twb_phase_barrier() {
+  asm volatile("" ::: "memory");
+  return 0LL;
+}
+#define TWB_CLK() twb_phase_barrier()
+#endif
+
 constexpr int kSimThreads = 128;  // 4 warps per CTA
 constexpr int kSimWarps = kSimThreads / 32;
 constexpr int kMaxSlotCap = 4096;
@@ -53,7 +67,7 @@ struct SimParams {
   tw_event* ev;
   int32_t* counter;
   int32_t cap;
-  int64_t* prof;  // optional: per config {cycles, normal steps, runs, run steps, tk cycles, run-event cycles, tk rounds, -}
+  int64_t* prof;  // optional: 16 int64 per config (tw_sim_set_profile)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -86,6 +100,17 @@ __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
 // that moved the Timekeeper rounds to a partner warp behind a shared-memory ring
 // measured 10-18% slower than keeping them inline — see profiles/README.md.)
 __device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) { return a / b; }
+
+// floor(a / b) for 0 <= a < 2^52 and b > 0 given rb ~= 1/b (any fp64 approximation):
+// the fp64 estimate is within 2 of the quotient, fixed up with exact int64 checks.
+__device__ __forceinline__ int64_t div_rcp(int64_t a, int64_t b, double rb) {
+  if (a >= (1LL << 52)) return a / b;
+  int64_t q = (int64_t)__dmul_rz(__ll2double_rn(a), rb);
+  int64_t r = a - q * b;
+  while (r < 0) { q--; r += b; }
+  while (r >= b) { q++; r -= b; }
+  return q;
+}
 
 // ceil(t / bk) for 0 <= t < 2^31 with a per-config magic reciprocal (no IDIV chain):
 // q0 = umulhi(t, floor((2^32-1)/bk)) is at most 2 below floor(t/bk).
@@ -139,6 +164,7 @@ struct ArrWindow {
 // stage share its deadline and parked workers are exempt.
 struct TkGrid {
   int64_t wall, offset, seq, last_bcast, V, cooldown, conv_cooldown;
+  double rcp_cooldown;
   int64_t disp_ts;
   int32_t disp;
   ArrWindow win;
@@ -174,79 +200,86 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 // round with t_min = min(dispatcher's next arrival, the stage deadline).
 __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
+  // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
   int64_t per = d;
-  if (S > 1) per = div_nn(d, S);
+  if (S == 2) per = d >> 1;
+  else if (S > 2) per = div_nn(d, S);
   const int64_t end_all = now0 + K * d;
-  const int64_t cj = g.cooldown > 0 ? g.conv_cooldown : 0;
+  const int64_t cj = g.conv_cooldown;  // 0 when the cooldown is 0
   const int64_t gap = (S > 1) ? min(per, d - per * (S - 1)) : d;
   const int64_t maxgap = (S > 1) ? max(per, d - per * (S - 1)) : d;
   const bool steady_ok = gap > cj && (S == 1 || per > 0);
   const bool wallbound_ok = cj > 0 && d > 0 && maxgap <= cj;
-  int64_t k = 0;
+  int64_t base = now0;  // walk position: deadline (base, s) is index m_walk
   int s = 0;
-  int64_t base = now0;
+  int64_t m_walk = 1;
   int64_t tgt = (S == 1) ? now0 + d : now0 + per;
+  int64_t m_on = g.V == now0 ? 0 : -1;  // index of the deadline V sits on, or -1
   for (;;) {
     tk_dispatch(g, ts, n, epoch);
     if (g.V >= end_all) return;
+    if (g.last_bcast == g.wall) {
+      // Wall-bound state: consecutive deadlines are at most cJ apart and the offset is
+      // at least cJ. Every round then sleeps cJ, broadcasts without growing the offset
+      // (the next deadline lies within V + cJ) and moves V by exactly cJ, so the rounds
+      // up to end_all are R = ceil((end_all - V) / cJ): wall += R*cJ, seq += R.
+      // Dispatcher targets inside that window change no clock value, only which
+      // arrivals have been passed (tk_dispatch).
+      if (wallbound_ok && g.offset >= cj) {
+        const int64_t R = div_rcp(end_all - g.V + cj - 1, cj, g.rcp_cooldown);
+        g.wall += R * cj;
+        g.seq += R;
+        g.last_bcast = g.wall;
+        g.V += R * cj;
+        continue;
+      }
+      // Steady state: V sits on deadline m_on and the stage gaps exceed cJ, so every
+      // later deadline below the dispatcher's target resolves the same way (sleep cJ,
+      // broadcast, V := deadline): R of them are closed-form: wall += R*cJ, seq += R,
+      // offset = t_R - wall, V = t_R.
+      if (steady_ok && m_on >= 0) {
+        int64_t m_x = K * S;  // last deadline we may cover: end_all, or below the target
+        if (g.disp_ts <= end_all) {
+          const int64_t x = g.disp_ts - 1 - now0;
+          const int64_t fx = div_nn(x, d);
+          const int64_t px = (S > 1) ? min((int64_t)(S - 1), div_nn(x - fx * d, per)) : 0;
+          m_x = fx * S + px;
+        }
+        const int64_t R = m_x - m_on;
+        if (R > 0) {
+          const int64_t fx = (S == 1) ? m_x : (S == 2 ? (m_x >> 1) : m_x / S);
+          const int64_t tR = now0 + fx * d + per * (m_x - fx * S);
+          g.wall += R * cj;
+          g.seq += R;
+          g.last_bcast = g.wall;
+          g.offset = tR - g.wall;
+          g.V = tR;
+          m_on = m_x;
+          continue;
+        }
+      }
+    }
+    // one round, resolved at min(dispatcher's next arrival, first deadline beyond V)
     if (tgt <= g.V) {
-      // the deadline is already behind V: move to the first one beyond it
       if (d > 0 && g.V - base >= 4 * d) {  // V far ahead: skip whole steps at once
         const int64_t jump = div_nn(g.V - base, d);
-        k += jump;
         base += jump * d;
+        m_walk += jump * S - s;
         s = 0;
       }
       for (;;) {
         tgt = (s == S - 1) ? base + d : base + per * (s + 1);
         if (tgt > g.V) break;
+        m_walk++;
         if (++s == S) {
           s = 0;
-          k++;
           base += d;
         }
       }
     }
     const int64_t t_min = g.disp_ts < tgt ? g.disp_ts : tgt;
     tk_resolve(g, t_min);
-    // Steady state: the round broadcast and landed V on its deadline. If the stage
-    // gaps exceed the cooldown step cJ, every later deadline below the dispatcher's
-    // target is resolved the same way (sleep cJ, broadcast, V := deadline), so R of
-    // them are closed-form: wall += R*cJ, seq += R, offset = t_R - wall, V = t_R.
-    // Wall-bound state: consecutive deadlines are at most cJ apart and the offset is at
-    // least cJ. Every round then sleeps cJ, broadcasts without growing the offset
-    // (its target lies within V + cJ) and moves V by exactly cJ, so the remaining
-    // rounds up to end_all are R = ceil((end_all - V) / cJ): wall += R*cJ, seq += R.
-    // Dispatcher targets inside that window change no clock value, only which
-    // arrivals have been passed (tk_dispatch above).
-    if (wallbound_ok && g.last_bcast == g.wall && g.offset >= cj && g.V < end_all) {
-      const int64_t R = div_nn(end_all - g.V + cj - 1, cj);
-      g.wall += R * cj;
-      g.seq += R;
-      g.last_bcast = g.wall;
-      g.V += R * cj;
-      continue;
-    }
-    if (steady_ok && g.V == t_min && g.last_bcast == g.wall) {
-      int64_t X = end_all;  // last deadline we may cover (< dispatcher target)
-      if (g.disp_ts <= X) X = g.disp_ts - 1;
-      if (X > g.V) {
-        // deadlines <= Y: full steps f contribute S each, plus the stages of the partial step
-        const int64_t fx = div_nn(X - now0, d), rx = X - now0 - fx * d;
-        const int64_t fv = div_nn(g.V - now0, d), rv = g.V - now0 - fv * d;
-        const int64_t px = (S > 1) ? min((int64_t)(S - 1), div_nn(rx, per)) : 0;
-        const int64_t pv = (S > 1) ? min((int64_t)(S - 1), div_nn(rv, per)) : 0;
-        const int64_t R = (fx * S + px) - (fv * S + pv);
-        if (R > 0) {
-          const int64_t tR = now0 + fx * d + per * px;  // largest deadline <= X
-          g.wall += R * cj;
-          g.seq += R;
-          g.last_bcast = g.wall;
-          g.offset = tR - g.wall;
-          g.V = tR;
-        }
-      }
-    }
+    m_on = g.V == tgt ? m_walk : -1;
   }
 }
 
@@ -260,19 +293,37 @@ __device__ __forceinline__ void tk_idle(TkGrid& g, const int64_t* __restrict__ t
   }
 }
 
+// Prediction cache: 32 entries held one per lane (key = P << 32 | D, for predictors
+// whose duration ignores C); a lookup is one compare + ballot + shuffle. Linear models
+// with a context term keep a single exact (P, D, C) entry.
 struct PredCache {
-  int64_t P, D, C, d;
+  int64_t key, val;    // this lane's entry
+  int64_t P, D, C, d;  // single entry (uses_c)
   bool uses_c;
+  int victim;
 };
 
 __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, int id, int64_t P, int64_t D,
                                                   int64_t C) {
-  if (P == pc.P && D == pc.D && (!pc.uses_c || C == pc.C)) return pc.d;
+  const int lane = threadIdx.x & 31;
+  if (pc.uses_c) {
+    if (P == pc.P && D == pc.D && C == pc.C) return pc.d;
+    const int64_t d = predict_warp(ps, id, P, D, C);
+    pc.P = P;
+    pc.D = D;
+    pc.C = C;
+    pc.d = d;
+    return d;
+  }
+  const int64_t key = (P << 32) | D;
+  const unsigned hit = __ballot_sync(kFull, pc.key == key);
+  if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
   const int64_t d = predict_warp(ps, id, P, D, C);
-  pc.P = P;
-  pc.D = D;
-  pc.C = C;
-  pc.d = d;
+  if (lane == pc.victim) {
+    pc.key = key;
+    pc.val = d;
+  }
+  pc.victim = (pc.victim + 1) & 31;
   return d;
 }
 
@@ -297,8 +348,9 @@ struct Emitter {
 __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
-  const long long t_start = clock64();
+  const long long t_start = clock64();  // per-config cycles (always on: 2 reads)
   int64_t n_normal = 0, n_runs = 0, n_run_steps = 0, tk_cyc = 0, ev_cyc = 0;
+  int64_t plan_cyc = 0, pred_cyc = 0, apply_cyc = 0, arr_cyc = 0, adm_cyc = 0;
   const tw_sim_cfg cfg = p.cfgs[c];
   tw_sim_result r;
   r.final_now_ns = cfg.epoch_ns;
@@ -350,6 +402,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   // predictor: cache + whether a decode-only run has a constant duration
   const tw_pred_desc* pd = pset_desc(ps, cfg.pred_id < pset_ndesc(ps) ? cfg.pred_id : 0);
   PredCache pc;
+  pc.key = -1;
+  pc.val = 0;
+  pc.victim = 0;
   pc.P = -1;
   pc.D = -1;
   pc.C = -1;
@@ -365,6 +420,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   g.V = epoch;
   g.cooldown = cfg.tk_cooldown_ns;
   g.conv_cooldown = g.cooldown > 0 ? fake_sleep_ns(g.cooldown) : 0;
+  g.rcp_cooldown = g.conv_cooldown > 0 ? __drcp_rn(__ll2double_rn(g.conv_cooldown)) : 0.0;
   g.disp = 0;
   g.win.load(ts, n, epoch, 0);
   g.disp_ts = n > 0 ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
@@ -374,15 +430,23 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   int64_t now = epoch, n_events = 0;
   int32_t step = 0, fut = 0, w_head = 0, n_act = 0;  // waiting = [w_head, fut), future = [fut, n)
   int64_t next_arr = n > 0 ? __shfl_sync(kFull, arr.v, 0) : INT64_MAX;
+  // waiting-queue window: lane l holds prompt/output of request w_head + l, reloaded
+  // (prefetched) right after every admission so the next admission finds it in registers
+  int32_t qbase = 0;
+  int32_t q_pr = (lane < n) ? __ldg(prm + lane) : 0;
+  int32_t q_op = (lane < n) ? __ldg(outp + lane) : 0;
   int overflow = 0;
 
   while (fut < n || w_head < fut || n_act > 0) {
     // ---- arrivals with epoch + offset <= now join the waiting queue (oracle.py:73-75)
+    const long long q0 = TWB_CLK();
     while (next_arr <= now) {
       fut++;
       next_arr = fut < n ? arr.get(ts, n, epoch, fut) : INT64_MAX;
     }
     const bool waiting = w_head < fut;
+    const long long q1 = TWB_CLK();
+    arr_cyc += q1 - q0;
 
     // ---- _plan (oracle.py:117-180), pass 1a (only needed with > 32 active)
     int total_dec = 0;
@@ -436,7 +500,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         if (cfg.policy == TW_POLICY_PREFILL_PRIORITIZED) {  // oracle.py:168-178
           bool have_prefill = any_mid;
           if (!have_prefill && waiting) {
-            const int32_t hp = __ldg(prm + w_head);
+            const int32_t hp = __shfl_sync(kFull, q_pr, 0);  // qbase == w_head
             have_prefill = n_act < max_running && blk.ceil_div(hp) <= free0;
           }
           do_chunks = have_prefill;
@@ -478,13 +542,16 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     budget -= min(want_before, budget > 0 ? budget : (int64_t)0);
 
     // ---- admission from the waiting head: strict FCFS, KV + slot + budget gates
+    const long long q2 = TWB_CLK();
+    plan_cyc += q2 - q1;
     int n_adm = 0;
     if (do_chunks && budget > 0 && waiting) {
       int64_t free_l = free0, slots = (int64_t)max_running - n_act;
       while (budget > 0 && slots > 0 && w_head + n_adm < fut) {
         const int32_t idx = w_head + n_adm + lane;
         const bool cand = idx < fut && lane < slots;
-        const int32_t pr = cand ? __ldg(prm + idx) : 0;
+        const bool inwin = n_adm == 0;  // qbase == w_head: the window is this round
+        const int32_t pr = cand ? (inwin ? q_pr : __ldg(prm + idx)) : 0;
         const int64_t need = blk.ceil_div(pr);
         const int64_t want = min((int64_t)chunk, (int64_t)pr);
         const int64_t NEi = warp_incl_scan_i64(cand ? need : 0);
@@ -498,7 +565,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           const int64_t take = min(want, budget - WE);
           sl.req[slot] = idx;
           sl.prompt[slot] = pr;
-          const int32_t op = __ldg(outp + idx);
+          const int32_t op = inwin ? q_op : __ldg(outp + idx);
           sl.output[slot] = op;
           sl.done[slot] = 0;
           sl.emit[slot] = 0;
@@ -535,9 +602,12 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     }
 
     // ---- predict (oracle.py:85-86)
+    const long long q3 = TWB_CLK();
+    adm_cyc += q3 - q2;
     const int64_t P = (int64_t)__reduce_add_sync(kFull, (unsigned)p_l);  // P <= max_batch_tokens
     const int64_t C = pc.uses_c ? warp_sum_i64_redux(c_l) : 0;
     const int64_t d = predict_cached(pc, ps, cfg.pred_id, P, n_dec, C);
+    pred_cyc += TWB_CLK() - q3;
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
       r.pred_code = (int32_t)d;
@@ -554,18 +624,18 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     if (macro_ok) {
       int64_t K = __reduce_min_sync(kFull, min_rem);
       // an emptied queue can admit the next arrival; a non-empty one stays blocked
-      if (w_head + n_adm == fut && fut < n && d > 0) {
+      if (w_head + n_adm == fut && fut < n && d > 0 && next_arr - now <= (K - 1) * d) {
         // the plan after step j sees arrivals <= now + j*d: stop at the first crossing
-        const int64_t ka = div_nn(next_arr - now + d - 1, d);
+        const int64_t ka = div_rcp(next_arr - now + d - 1, d, __drcp_rn(__ll2double_rn(d)));
         if (ka < K) K = ka;
       }
       if (K >= 2) {
         const int D = n_dec;  // events per step: one OUTPUT_TOKEN per decode slot
         const int64_t now0 = now;
         const int32_t step0 = step;
-        long long c0 = clock64();
+        long long c0 = TWB_CLK();
         if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);
-        long long c1 = clock64();
+        long long c1 = TWB_CLK();
         tk_cyc += c1 - c0;
         // events of steps 1..K-1, flattened over the lanes: e -> (step j, decode rank i)
         const int64_t body = (K - 1) * (int64_t)D;
@@ -629,10 +699,15 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         }
         n_events = pos;
         n_act = kept;
-        w_head += n_adm;
+        if (n_adm) {
+          w_head += n_adm;
+          qbase = w_head;
+          q_pr = (qbase + lane < n) ? __ldg(prm + qbase + lane) : 0;
+          q_op = (qbase + lane < n) ? __ldg(outp + qbase + lane) : 0;
+        }
         now = nowK;
         step = stepK;
-        ev_cyc += clock64() - c1;
+        ev_cyc += TWB_CLK() - c1;
         n_runs++;
         n_run_steps += K;
         continue;
@@ -644,12 +719,13 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int64_t base = now;
     now += d;
     {
-      const long long c0 = clock64();
+      const long long c0 = TWB_CLK();
       if (tk_on) tk_run(g, ts, n, epoch, S, base, d, 1);  // WorkerGrid stage deadlines
-      tk_cyc += clock64() - c0;
+      tk_cyc += TWB_CLK() - c0;
     }
 
     // ---- apply (oracle.py:88-112): chunks' events first, then decodes', in slot order
+    const long long q4 = TWB_CLK();
     const int n_tot = n_act + n_adm;
     const int chunk_ev_total = __reduce_add_sync(kFull, (unsigned)chunk_ev);
     int64_t pos_c = n_events, pos_d = n_events + chunk_ev_total;
@@ -715,8 +791,14 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       __syncwarp();
     }
     n_events = pos_d;
-    w_head += n_adm;
     n_act = kept;
+    if (n_adm) {
+      w_head += n_adm;
+      qbase = w_head;
+      q_pr = (qbase + lane < n) ? __ldg(prm + qbase + lane) : 0;
+      q_op = (qbase + lane < n) ? __ldg(outp + qbase + lane) : 0;
+    }
+    apply_cyc += TWB_CLK() - q4;
   }
 
   if (em.evp && n_events > em.ev_cap) overflow = 1;
@@ -737,19 +819,27 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   if (lane == 0) {
     p.res[c] = r;
     if (p.prof) {
-      p.prof[8 * c] = clock64() - t_start;
-      p.prof[8 * c + 1] = n_normal;
-      p.prof[8 * c + 2] = n_runs;
-      p.prof[8 * c + 3] = n_run_steps;
-      p.prof[8 * c + 4] = tk_cyc;
-      p.prof[8 * c + 5] = ev_cyc;
-      p.prof[8 * c + 6] = g.seq;
-      p.prof[8 * c + 7] = 0;
+      int64_t* q = p.prof + 16 * c;
+      q[0] = clock64() - t_start;
+      q[1] = n_normal;
+      q[2] = n_runs;
+      q[3] = n_run_steps;
+      q[4] = tk_cyc;
+      q[5] = ev_cyc;
+      q[6] = g.seq;
+      q[7] = arr_cyc;
+      q[8] = plan_cyc;
+      q[9] = adm_cyc;
+      q[10] = pred_cyc;
+      q[11] = apply_cyc;
     }
   }
 }
 
-__global__ void __launch_bounds__(kSimThreads) k_sim(SimParams p) {
+#ifndef TWB_SIM_MIN_BLOCKS
+#define TWB_SIM_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kSimThreads, TWB_SIM_MIN_BLOCKS) k_sim(SimParams p) {
   extern __shared__ __align__(128) char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   char* ps = smem + 128;
@@ -854,8 +944,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   return check_launch("tw_sim_many");
 }
 
-extern "C" int tw_sim_set_profile(int64_t* per_config_8xi64) {
-  g_prof = per_config_8xi64;
+extern "C" int tw_sim_set_profile(int64_t* per_config_16xi64) {
+  g_prof = per_config_16xi64;
   return TW_OK;
 }
 

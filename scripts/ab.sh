@@ -1,7 +1,7 @@
-# A/B the k_sim variants on the same box (3 alternating runs each)
+# A/B the k_sim variants on the same box (alternating runs)
 mkdir -p gpurun_out
-for i in 1 2 3; do
-  for v in plaindiv pairrel pairvol; do
+for i in 1 2; do
+  for v in $AB_VARIANTS; do
     TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_$v.so timeout 300 python scripts/prof_sim.py 2>/dev/null | head -1 | sed "s/^/$v: /" >> gpurun_out/ab.log
   done
 done
