@@ -49,7 +49,11 @@ extern "C" {
  *   tw_pset_header | tw_pred_desc[n_desc] | table pool
  * A table (kind TABLE) occupies, at byte offset `table_off` from the blob start:
  *   int32 paxis[np] (sorted, unique) | int32 daxis[nd] (sorted, unique) |
- *   (pad to 8) | int64 grid_us[np*nd] (row-major [p][d]; TW_TABLE_HOLE = no row)
+ *   (pad to 8) | int64 grid_us[np*nd] (row-major [p][d]; TW_TABLE_HOLE = no row) |
+ *   fp64 rp[np], rd[nd]: RN(1 / (axis[k+1] - axis[k])) per interval (last unused) |
+ *   int16 lutp[34][2], lutd[34][2]: for b = bitlen(v - axis[0]), the floor index of v
+ *   (largest i with axis[i] <= v) lies in [lut[b][0], lut[b][1]] |
+ *   int32 grid32[np*nd] (only when desc.pad == 1: every value < 2^31 us)
  * The blob is built on host (paper_2601_00397_b200/predictor.py::PredictorSet) and
  * staged whole into shared memory by each CTA with one cp.async.bulk (TMA). */
 #define TW_PSET_MAGIC 0x54534550u /* "PEST" little-endian */
@@ -76,7 +80,7 @@ typedef struct tw_pred_desc {
   int32_t table_off; /* TABLE: byte offset of paxis from blob start */
   int32_t np;        /* TABLE: prefill-axis length */
   int32_t nd;        /* TABLE: decode-axis length  */
-  int32_t pad;
+  int32_t pad;       /* TABLE: 1 = an int32 copy of the grid follows the LUTs */
 } tw_pred_desc; /* 64 B */
 
 /* ---- bulk predictor (kernel 2 of the north star) -------------------------- */
@@ -98,6 +102,11 @@ int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batc
                        const int32_t* slot_tok, const int32_t* slot_ctx,
                        const int32_t* desc_id, int64_t n_batches, int64_t* feat_out,
                        int64_t* out_ns, void* stream);
+
+/* Device self-test of the predictor's reciprocal-based exact division against the
+ * hardware's correctly rounded __ddiv_rn on n pseudo-random operand pairs; adds the
+ * number of differing quotients to *mismatches (device counter, caller-zeroed). */
+int tw_selftest_division(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream);
 
 /* ---- Timekeeper (kernel 3): BarrierCore op-stream replay ------------------ */
 /* One op stream per Timekeeper instance ("config"); every stream is replayed

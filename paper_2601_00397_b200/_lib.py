@@ -130,6 +130,7 @@ assert EVENT_DTYPE.itemsize == 16
 EXPORTED_SYMBOLS = (
     "tw_predict_features",
     "tw_predict_batches",
+    "tw_selftest_division",
     "tw_tk_replay",
     "tw_tk_resolve",
     "tw_sim_many",
@@ -156,6 +157,7 @@ _I64 = ctypes.c_int64
 _SIGNATURES = {
     "tw_predict_features": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P]),
     "tw_predict_batches": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
+    "tw_selftest_division": (_I32, [_I64, ctypes.c_uint64, _P, _P]),
     "tw_tk_replay": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tw_tk_resolve": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),
     "tw_sim_many": (

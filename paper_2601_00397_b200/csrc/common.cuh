@@ -79,6 +79,11 @@ struct TableView {
   const int32_t* pax;
   const int32_t* dax;
   const int64_t* grid;
+  const double* rp;  // RN(1 / (pax[k+1] - pax[k]))
+  const double* rd;  // RN(1 / (dax[k+1] - dax[k]))
+  const int16_t* lutp;  // bit-length LUTs (twb200.h table layout)
+  const int16_t* lutd;
+  const int32_t* grid32;  // int32 copy of the grid, or null
   int np, nd;
 };
 
@@ -96,6 +101,11 @@ __device__ __forceinline__ TableView table_view(const char* pset, const tw_pred_
   uint32_t goff = (uint32_t)(d->np + d->nd) * 4u;
   goff = (goff + 7u) & ~7u;
   t.grid = reinterpret_cast<const int64_t*>(base + goff);
+  t.rp = reinterpret_cast<const double*>(t.grid + d->np * d->nd);
+  t.rd = t.rp + d->np;
+  t.lutp = reinterpret_cast<const int16_t*>(t.rd + d->nd);
+  t.lutd = t.lutp + 68;
+  t.grid32 = d->pad ? reinterpret_cast<const int32_t*>(t.lutp + 136) : nullptr;
   t.np = d->np;
   t.nd = d->nd;
   return t;
@@ -104,18 +114,32 @@ __device__ __forceinline__ TableView table_view(const char* pset, const tw_pred_
 // Python round(float) -> int (half to even), then us -> ns.
 __device__ __forceinline__ int64_t us_to_ns_rn(double us) { return __double2ll_rn(us) * 1000; }
 
+// Correctly rounded a / b for an integer-valued b > 0 given rb = RN(1/b): a first
+// quotient RN(a*rb) within 2 ulps, then two FMA residual corrections (Markstein: with a
+// correctly rounded reciprocal, q + (a - b q) rb rounded once is RN(a/b) once q is
+// faithful). a / b is never a rounding midpoint here (a is a double, b an integer, so
+// the exact quotient is either representable or not dyadic), so the result equals
+// __ddiv_rn(a, b) bit for bit; tw_selftest_division checks it on device.
+__device__ __forceinline__ double div_rn_rcp(double a, double b, double rb) {
+  double q = __dmul_rn(a, rb);
+  double r = __fma_rn(-q, b, a);
+  q = __fma_rn(r, rb, q);
+  r = __fma_rn(-q, b, a);
+  return __fma_rn(r, rb, q);
+}
+
 // lerp with exact-int operands: Python evaluates (b-a)*(x-lo) exactly and the
-// int/int true division correctly rounded; equal to one __ddiv_rn while |num| < 2^53
-// (the host rejects tables that could exceed it).
-__device__ __forceinline__ double lerp_int(int64_t a, int64_t b, int64_t lo, int64_t hi, int64_t x) {
+// int/int true division correctly rounded; equal to one correctly rounded fp64
+// division while |num| < 2^53 (the host rejects tables that could exceed it).
+__device__ __forceinline__ double lerp_int(int64_t a, int64_t b, int64_t lo, int64_t hi, int64_t x, double rgap) {
   const int64_t num = (b - a) * (x - lo);
-  const double q = __ddiv_rn(__ll2double_rn(num), __ll2double_rn(hi - lo));
+  const double q = div_rn_rcp(__ll2double_rn(num), __ll2double_rn(hi - lo), rgap);
   return __dadd_rn(__ll2double_rn(a), q);
 }
-__device__ __forceinline__ double lerp_dbl(double a, double b, int64_t lo, int64_t hi, int64_t x) {
+__device__ __forceinline__ double lerp_dbl(double a, double b, int64_t lo, int64_t hi, int64_t x, double rgap) {
   const double diff = __dsub_rn(b, a);
   const double prod = __dmul_rn(diff, __ll2double_rn(x - lo));
-  return __dadd_rn(a, __ddiv_rn(prod, __ll2double_rn(hi - lo)));
+  return __dadd_rn(a, div_rn_rcp(prod, __ll2double_rn(hi - lo), rgap));
 }
 
 // Bilinear evaluation once both axes are bracketed (indices into the axes).
@@ -133,26 +157,139 @@ __device__ __forceinline__ int64_t table_corners(const TableView& t, int p0, int
   if (P1 == P0) {
     // level-1 lerps return the int corners (predictor.py:229-230); an exact hit
     // (predictor.py:213-215) is the P1==P0, D1==D0 case
-    us = (D1 == D0) ? __ll2double_rn(c00) : lerp_int(c00, c01, D0, D1, D);
+    us = (D1 == D0) ? __ll2double_rn(c00) : lerp_int(c00, c01, D0, D1, D, t.rd[d0]);
   } else {
-    const double at_d0 = lerp_int(c00, c10, P0, P1, P);
-    const double at_d1 = lerp_int(c01, c11, P0, P1, P);
-    us = (D1 == D0) ? at_d0 : lerp_dbl(at_d0, at_d1, D0, D1, D);
+    const double rp = t.rp[p0];
+    const double at_d0 = lerp_int(c00, c10, P0, P1, P, rp);
+    const double at_d1 = lerp_int(c01, c11, P0, P1, P, rp);
+    us = (D1 == D0) ? at_d0 : lerp_dbl(at_d0, at_d1, D0, D1, D, t.rd[d0]);
   }
   return us_to_ns_rn(us);
 }
 
-// scalar bracket: lo = index of max axis <= v, hi = index of min axis >= v
+// scalar bracket: lo = index of max axis <= v, hi = index of min axis >= v.
+// Branchless binary search: power-of-two steps from the largest below n.
 __device__ __forceinline__ bool bracket_scalar(const int32_t* axis, int n, int64_t v, int& lo, int& hi) {
   if (v < axis[0] || v > axis[n - 1]) return false;
-  int a = 0, b = n - 1;  // invariant: axis[a] <= v, answer in [a, b]
-  while (a < b) {
-    const int m = (a + b + 1) >> 1;
-    if (axis[m] <= v) a = m; else b = m - 1;
+  int pos = 0;
+  int32_t at = axis[0];
+  for (int step = (n > 1) ? (1 << (31 - __clz(n - 1))) : 0; step > 0; step >>= 1) {
+    const int cand = pos + step;
+    if (cand < n) {
+      const int32_t a = axis[cand];
+      if ((int64_t)a <= v) {
+        pos = cand;
+        at = a;
+      }
+    }
   }
-  lo = a;
-  hi = (axis[a] == v) ? a : a + 1;
+  lo = pos;
+  hi = ((int64_t)at == v) ? pos : pos + 1;
   return true;
+}
+
+// bracket through the bit-length LUT: the floor index lies in [lut[b][0], lut[b][1]]
+// with b = bitlen(v - axis[0]); power-of-two-like axes need no search step at all.
+__device__ __forceinline__ bool bracket_lut(const int32_t* axis, const int16_t* lut, int n, int64_t v, int& lo,
+                                            int& hi, int64_t& vlo, int64_t& vhi) {
+  const int64_t a0 = axis[0];
+  if (v < a0 || v > (int64_t)axis[n - 1]) return false;
+  const uint32_t x = (uint32_t)(v - a0);
+  const int b = 32 - __clz(x);
+  const uint32_t pr = *reinterpret_cast<const uint32_t*>(lut + 2 * b);  // (lo, hi) pair
+  int i = (int16_t)(pr & 0xffff), j = (int16_t)(pr >> 16);
+  while (i < j) {
+    const int m = (i + j + 1) >> 1;
+    if ((int64_t)axis[m] <= v) i = m; else j = m - 1;
+  }
+  lo = i;
+  vlo = axis[i];
+  if (vlo == v) {
+    hi = i;
+    vhi = vlo;
+  } else {
+    hi = i + 1;
+    vhi = axis[i + 1];
+  }
+  return true;
+}
+
+// 32-bit variant for the bulk path (features are int32 there)
+__device__ __forceinline__ bool bracket_lut32(const int32_t* axis, const int16_t* lut, int n, int32_t v, int& lo,
+                                              int& hi, int32_t& vlo, int32_t& vhi) {
+  const int32_t a0 = axis[0];
+  if (v < a0 || v > axis[n - 1]) return false;
+  const int b = 32 - __clz((uint32_t)(v - a0));
+  const uint32_t pr = *reinterpret_cast<const uint32_t*>(lut + 2 * b);
+  int i = (int16_t)(pr & 0xffff), j = (int16_t)(pr >> 16);
+  while (i < j) {
+    const int m = (i + j + 1) >> 1;
+    if (axis[m] <= v) i = m; else j = m - 1;
+  }
+  lo = i;
+  vlo = axis[i];
+  if (vlo == v) {
+    hi = i;
+    vhi = vlo;
+  } else {
+    hi = i + 1;
+    vhi = axis[i + 1];
+  }
+  return true;
+}
+
+// int32-grid bilinear evaluation for the bulk path: 4-byte corner gathers; the int
+// lerp numerators are one 32x32->64 multiply each (values and axes are int32)
+__device__ __forceinline__ int64_t table_corners32(const TableView& t, int p0, int p1, int d0, int d1, int32_t P0,
+                                                   int32_t P1, int32_t D0, int32_t D1, int32_t P, int32_t D) {
+  const int32_t c00 = t.grid32[p0 * t.nd + d0];
+  const int32_t c10 = t.grid32[p1 * t.nd + d0];
+  const int32_t c01 = t.grid32[p0 * t.nd + d1];
+  const int32_t c11 = t.grid32[p1 * t.nd + d1];
+  if ((c00 | c10 | c01 | c11) < 0) return TW_PRED_TABLE_MISS;  // holes are the only negatives
+  double us;
+  if (P1 == P0) {
+    if (D1 == D0) {
+      us = (double)c00;
+    } else {
+      const int64_t num = (int64_t)(c01 - c00) * (int64_t)(D - D0);
+      us = __dadd_rn((double)c00, div_rn_rcp(__ll2double_rn(num), (double)(D1 - D0), t.rd[d0]));
+    }
+  } else {
+    const double rp = t.rp[p0], gp = (double)(P1 - P0);
+    const int64_t n0 = (int64_t)(c10 - c00) * (int64_t)(P - P0);
+    const int64_t n1 = (int64_t)(c11 - c01) * (int64_t)(P - P0);
+    const double at_d0 = __dadd_rn((double)c00, div_rn_rcp(__ll2double_rn(n0), gp, rp));
+    const double at_d1 = __dadd_rn((double)c01, div_rn_rcp(__ll2double_rn(n1), gp, rp));
+    if (D1 == D0) {
+      us = at_d0;
+    } else {
+      const double prod = __dmul_rn(__dsub_rn(at_d1, at_d0), (double)(D - D0));
+      us = __dadd_rn(at_d0, div_rn_rcp(prod, (double)(D1 - D0), t.rd[d0]));
+    }
+  }
+  return us_to_ns_rn(us);
+}
+
+// bilinear evaluation from bracket indices and their axis values; holes (-1) are the
+// only negative grid entries, so one OR of the corners detects any of them
+__device__ __forceinline__ int64_t table_corners2(const TableView& t, int p0, int p1, int d0, int d1, int64_t P0,
+                                                  int64_t P1, int64_t D0, int64_t D1, int64_t P, int64_t D) {
+  const int64_t c00 = t.grid[p0 * t.nd + d0];
+  const int64_t c10 = t.grid[p1 * t.nd + d0];
+  const int64_t c01 = t.grid[p0 * t.nd + d1];
+  const int64_t c11 = t.grid[p1 * t.nd + d1];
+  if ((c00 | c10 | c01 | c11) < 0) return TW_PRED_TABLE_MISS;
+  double us;
+  if (P1 == P0) {
+    us = (D1 == D0) ? __ll2double_rn(c00) : lerp_int(c00, c01, D0, D1, D, t.rd[d0]);
+  } else {
+    const double rp = t.rp[p0];
+    const double at_d0 = lerp_int(c00, c10, P0, P1, P, rp);
+    const double at_d1 = lerp_int(c01, c11, P0, P1, P, rp);
+    us = (D1 == D0) ? at_d0 : lerp_dbl(at_d0, at_d1, D0, D1, D, t.rd[d0]);
+  }
+  return us_to_ns_rn(us);
 }
 
 // manhattan-nearest row, ties -> smallest (p, d) (predictor.py:205-207); scalar
@@ -190,12 +327,35 @@ __device__ __forceinline__ int64_t predict_scalar(const char* pset, int id, int6
   if (d->kind != TW_PRED_TABLE) return TW_PRED_BAD_DESC;
   const TableView t = table_view(pset, d);
   int p0, p1, d0, d1;
-  if (bracket_scalar(t.pax, t.np, P, p0, p1) && bracket_scalar(t.dax, t.nd, D, d0, d1)) {
-    const int64_t r = table_corners(t, p0, p1, d0, d1, P, D);
+  int64_t P0, P1, D0, D1;
+  if (bracket_lut(t.pax, t.lutp, t.np, P, p0, p1, P0, P1) && bracket_lut(t.dax, t.lutd, t.nd, D, d0, d1, D0, D1)) {
+    const int64_t r = table_corners2(t, p0, p1, d0, d1, P0, P1, D0, D1, P, D);
     if (r != TW_PRED_TABLE_MISS) return r;
   }
   if (d->allow_extrapolation) return table_nearest_scalar(t, P, D);
   return TW_PRED_TABLE_MISS;
+}
+
+// One prediction for the bulk kernel: int32 P and D (the features API), table path
+// first. Same results as predict_scalar.
+__device__ __forceinline__ int64_t predict_bulk(const char* pset, int id, int32_t P, int32_t D, int64_t C) {
+  if ((unsigned)id >= (unsigned)pset_ndesc(pset)) return TW_PRED_BAD_DESC;
+  const tw_pred_desc* d = pset_desc(pset, id);
+  const int kind = d->kind;
+  if (kind == TW_PRED_TABLE) {
+    const TableView t = table_view(pset, d);
+    int p0, p1, d0, d1;
+    int32_t P0, P1, D0, D1;
+    if (bracket_lut32(t.pax, t.lutp, t.np, P, p0, p1, P0, P1) &&
+        bracket_lut32(t.dax, t.lutd, t.nd, D, d0, d1, D0, D1)) {
+      const int64_t r = t.grid32 ? table_corners32(t, p0, p1, d0, d1, P0, P1, D0, D1, P, D)
+                                 : table_corners2(t, p0, p1, d0, d1, P0, P1, D0, D1, P, D);
+      if (r != TW_PRED_TABLE_MISS) return r;
+    }
+    if (d->allow_extrapolation) return table_nearest_scalar(t, P, D);
+    return TW_PRED_TABLE_MISS;
+  }
+  return predict_scalar(pset, id, P, D, C);
 }
 
 // ------------------------------------------------------------------------------

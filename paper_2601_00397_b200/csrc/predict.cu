@@ -27,10 +27,13 @@ struct PsetSmem {
 __device__ __forceinline__ int64_t predict_one(const char* ps, int32_t p, int32_t d, int64_t c,
                                                int32_t id) {
   if (p == 0 && d == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
-  return predict_scalar(ps, id, p, d, c);
+  return predict_bulk(ps, id, p, d, c);
 }
 
-__global__ void __launch_bounds__(kPredThreads) k_predict_features(
+#ifndef TWB_PRED_MIN_BLOCKS
+#define TWB_PRED_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_features(
     const void* __restrict__ pset, uint32_t pset_bytes, const int32_t* __restrict__ P,
     const int32_t* __restrict__ D, const int64_t* __restrict__ C, const int32_t* __restrict__ id,
     int64_t n, int64_t* __restrict__ out) {
@@ -80,6 +83,33 @@ __global__ void __launch_bounds__(kPredThreads) k_predict_batches(
     }
     out[b] = (s1 == s0) ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(ps, id[b], Pt, Dn, Ct);
   }
+}
+
+// Self-test of div_rn_rcp against the hardware-correct __ddiv_rn on pseudo-random
+// operands shaped like the lerps' (integer numerators up to 2^53, products of a double
+// difference and a small integer, integer gaps up to 2^24).
+__global__ void k_selftest_division(int64_t n, uint64_t seed, unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long local = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t h1 = tw_mix64(seed ^ (uint64_t)i * 0x9E3779B97F4A7C15ULL);
+    const uint64_t h2 = tw_mix64(h1 + 0x632BE59BD9B4E019ULL);
+    const uint64_t h3 = tw_mix64(h2 ^ 0x85EBCA77C2B2AE63ULL);
+    const int bits_b = 1 + (int)(h3 % 24);
+    const double b = (double)(int64_t)(1 + (h2 >> (64 - bits_b)));
+    double a;
+    if (h3 & 64) {
+      const int bits_a = 1 + (int)((h3 >> 8) % 53);
+      a = (double)(int64_t)(h1 >> (64 - bits_a));
+      if (h3 & 128) a = -a;
+    } else {  // (at_d1 - at_d0) * (x - lo): a double difference times a small integer
+      const double u = __ll2double_rn((int64_t)(h1 >> 12)) * 0x1p-30;
+      const double v = __ll2double_rn((int64_t)(h2 >> 20)) * 0x1p-25;
+      a = __dmul_rn(__dsub_rn(u, v), (double)(1 + (h3 >> 40) % 4096));
+    }
+    if (div_rn_rcp(a, b, __drcp_rn(b)) != __ddiv_rn(a, b)) local++;
+  }
+  if (local) atomicAdd(bad, local);
 }
 
 static int pred_grid(int64_t work, size_t smem, const void* fn) {
@@ -134,6 +164,16 @@ extern "C" int tw_predict_features(const void* pset, int64_t pset_bytes, const i
       pset, (uint32_t)pset_bytes, P, D, C, desc_id, n, out_ns);
   count_launch();
   return check_launch("tw_predict_features");
+}
+
+extern "C" int tw_selftest_division(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream) {
+  if (n < 0 || !mismatches) {
+    set_error("tw_selftest_division: bad arguments");
+    return TW_EINVAL;
+  }
+  k_selftest_division<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(n, seed, mismatches);
+  count_launch();
+  return check_launch("tw_selftest_division");
 }
 
 extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batch_off,

@@ -313,6 +313,22 @@ def build_predictor(config: dict):
 # ---------------------------------------------------------------------------------
 
 
+def _bitlen_lut(axis: np.ndarray) -> np.ndarray:
+    """Per bit length b = 0..32 of x = v - axis[0]: (lo[b], hi[b]) = the largest index i
+    with axis[i] - axis[0] <= the smallest / largest x of that bit length, so the floor
+    index of v lies in [lo[b], hi[b]] (equal for power-of-two-like axes: no search).
+    Stored as int16 pairs (twb200.h table layout)."""
+    a = np.asarray(axis, np.int64)
+    rel = a - a[0]
+    lut = np.zeros((34, 2), np.int16)
+    for b in range(34):
+        low = 0 if b == 0 else (1 << (b - 1))
+        high = 0 if b == 0 else (1 << b) - 1
+        lut[b, 0] = int(np.searchsorted(rel, low, side="right")) - 1
+        lut[b, 1] = int(np.searchsorted(rel, high, side="right")) - 1
+    return lut
+
+
 def _align(n: int, a: int) -> int:
     return (n + a - 1) // a * a
 
@@ -336,7 +352,20 @@ class PredictorSet:
                 pax, dax, grid = tab
                 axes = pax.tobytes() + dax.tobytes()
                 axes += b"\0" * (_align(len(axes), 8) - len(axes))
-                blob = axes + grid.tobytes()
+                # RN(1 / axis gap) per interval (Python float division is correctly
+                # rounded): the kernels divide by gaps with a multiply + FMA corrections
+                rp = np.array([1.0 / float(pax[k + 1] - pax[k]) if k + 1 < len(pax) else 0.0
+                               for k in range(len(pax))], np.float64)
+                rd = np.array([1.0 / float(dax[k + 1] - dax[k]) if k + 1 < len(dax) else 0.0
+                               for k in range(len(dax))], np.float64)
+                blob = axes + grid.tobytes() + rp.tobytes() + rd.tobytes()
+                blob += _bitlen_lut(pax).tobytes() + _bitlen_lut(dax).tobytes()
+                # int32 copy of the grid for the bulk kernel's gathers (half the bytes);
+                # tables with values >= 2^31 us carry none and use the int64 grid
+                small = bool(grid.max() < 2**31)
+                descs[i]["pad"] = 1 if small else 0
+                if small:
+                    blob += grid.astype(np.int32).tobytes()
                 blob += b"\0" * (_align(len(blob), 16) - len(blob))
                 descs[i]["table_off"] = cursor
                 pool.append(blob)

@@ -60,6 +60,19 @@ def test_predict_features_equals_oracle_on_random_sweep():
     assert np.array_equal(got, want)
 
 
+def test_reciprocal_division_equals_hardware_division():
+    """div_rn_rcp (multiply + 2 FMA corrections) == __ddiv_rn on 2^28 operand pairs."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for seed in (1, 2, 3, 4):
+        _lib.check(_lib.load().tw_selftest_division(1 << 26, seed, bad.data_ptr(), None), "selftest")
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+
+
 def test_reference_known_answers_through_drop_in_predict():
     """pkg/tests/test_predictor.py:18-144 worked examples, via predict(batch)."""
     from paper_2601_00397_b200.predictor import (
