@@ -253,10 +253,19 @@ __device__ __forceinline__ int64_t table_corners32(const TableView& t, int p0, i
       us = (double)c00;
     } else {
       const int64_t num = (int64_t)(c01 - c00) * (int64_t)(D - D0);
+#ifndef TWB_RCP_FROM_BLOB
+      const double gd = (double)(D1 - D0);
+      us = __dadd_rn((double)c00, div_rn_rcp(__ll2double_rn(num), gd, __drcp_rn(gd)));
+#else
       us = __dadd_rn((double)c00, div_rn_rcp(__ll2double_rn(num), (double)(D1 - D0), t.rd[d0]));
+#endif
     }
   } else {
+#ifndef TWB_RCP_FROM_BLOB
+    const double gp = (double)(P1 - P0), rp = __drcp_rn(gp);
+#else
     const double rp = t.rp[p0], gp = (double)(P1 - P0);
+#endif
     const int64_t n0 = (int64_t)(c10 - c00) * (int64_t)(P - P0);
     const int64_t n1 = (int64_t)(c11 - c01) * (int64_t)(P - P0);
     const double at_d0 = __dadd_rn((double)c00, div_rn_rcp(__ll2double_rn(n0), gp, rp));
@@ -265,7 +274,12 @@ __device__ __forceinline__ int64_t table_corners32(const TableView& t, int p0, i
       us = at_d0;
     } else {
       const double prod = __dmul_rn(__dsub_rn(at_d1, at_d0), (double)(D - D0));
+#ifndef TWB_RCP_FROM_BLOB
+      const double gd = (double)(D1 - D0);
+      us = __dadd_rn(at_d0, div_rn_rcp(prod, gd, __drcp_rn(gd)));
+#else
       us = __dadd_rn(at_d0, div_rn_rcp(prod, (double)(D1 - D0), t.rd[d0]));
+#endif
     }
   }
   return us_to_ns_rn(us);
@@ -338,8 +352,9 @@ __device__ __forceinline__ int64_t predict_scalar(const char* pset, int id, int6
 
 // One prediction for the bulk kernel: int32 P and D (the features API), table path
 // first. Same results as predict_scalar.
-__device__ __forceinline__ int64_t predict_bulk(const char* pset, int id, int32_t P, int32_t D, int64_t C) {
-  if ((unsigned)id >= (unsigned)pset_ndesc(pset)) return TW_PRED_BAD_DESC;
+__device__ __forceinline__ int64_t predict_bulk(const char* pset, int n_desc, int id, int32_t P, int32_t D,
+                                                int64_t C) {
+  if ((unsigned)id >= (unsigned)n_desc) return TW_PRED_BAD_DESC;
   const tw_pred_desc* d = pset_desc(pset, id);
   const int kind = d->kind;
   if (kind == TW_PRED_TABLE) {

@@ -24,20 +24,21 @@ struct PsetSmem {
   }
 };
 
-__device__ __forceinline__ int64_t predict_one(const char* ps, int32_t p, int32_t d, int64_t c,
+__device__ __forceinline__ int64_t predict_one(const char* ps, int n_desc, int32_t p, int32_t d, int64_t c,
                                                int32_t id) {
   if (p == 0 && d == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
-  return predict_bulk(ps, id, p, d, c);
+  return predict_bulk(ps, n_desc, id, p, d, c);
 }
 
 #ifndef TWB_PRED_MIN_BLOCKS
-#define TWB_PRED_MIN_BLOCKS 4
+#define TWB_PRED_MIN_BLOCKS 5
 #endif
 __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_features(
     const void* __restrict__ pset, uint32_t pset_bytes, const int32_t* __restrict__ P,
     const int32_t* __restrict__ D, const int64_t* __restrict__ C, const int32_t* __restrict__ id,
     int64_t n, int64_t* __restrict__ out) {
   const char* ps = PsetSmem::stage(pset, pset_bytes);
+  const int n_desc = pset_ndesc(ps);
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // vector body: groups of 4 consecutive queries (all arrays 16-B aligned by contract)
@@ -49,14 +50,14 @@ __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_f
     const longlong2 c01 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g);
     const longlong2 c23 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g + 1);
     longlong2 o01, o23;
-    o01.x = predict_one(ps, p4.x, d4.x, c01.x, i4.x);
-    o01.y = predict_one(ps, p4.y, d4.y, c01.y, i4.y);
-    o23.x = predict_one(ps, p4.z, d4.z, c23.x, i4.z);
-    o23.y = predict_one(ps, p4.w, d4.w, c23.y, i4.w);
+    o01.x = predict_one(ps, n_desc, p4.x, d4.x, c01.x, i4.x);
+    o01.y = predict_one(ps, n_desc, p4.y, d4.y, c01.y, i4.y);
+    o23.x = predict_one(ps, n_desc, p4.z, d4.z, c23.x, i4.z);
+    o23.y = predict_one(ps, n_desc, p4.w, d4.w, c23.y, i4.w);
     __stcs(reinterpret_cast<longlong2*>(out) + 2 * g, o01);
     __stcs(reinterpret_cast<longlong2*>(out) + 2 * g + 1, o23);
   }
-  for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, P[i], D[i], C[i], id[i]);
+  for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, n_desc, P[i], D[i], C[i], id[i]);
 }
 
 // Fused extraction + prediction. One thread per batch; its slots are a contiguous
