@@ -156,6 +156,15 @@ def time_kernel_steps(run, steps, warmup, flush_buf, stream):
     return durs
 
 
+def measured_traffic(kernel: str):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)[kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def predictor_roofline(device, peak_gbs):
     """Bulk predictor kernel (tw_predict_features) at 2^27 queries: achieved GB/s vs HBM peak."""
     import torch
@@ -197,7 +206,8 @@ def predictor_roofline(device, peak_gbs):
     return {"kernel": "k_predict_features", "bound": "hbm", "achieved": round(gbs, 1), "peak": peak_gbs,
             "unit": "GB/s", "frac": round(gbs / peak_gbs, 4), "bytes_per_prediction": bytes_per,
             "predictions_per_launch": n, "ms_per_launch": round(ms, 4),
-            "predictions_per_s": round(n / (ms / 1e3), 1), "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+            "predictions_per_s": round(n / (ms / 1e3), 1), "traffic": measured_traffic("k_predict_features"),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
 
 
 def cpu_baseline(sw, budget_s: float, n_threads: int):
@@ -365,7 +375,8 @@ def main():
     achieved = alg_bytes / (ms / 1e3) / 1e9
     launch = _lib.last_sim_launch()
     roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 6), "traffic": None, "algorithmic_bytes_per_launch": int(alg_bytes),
+            "frac": round(achieved / peak_gbs, 6), "traffic": measured_traffic("k_sim"),
+            "algorithmic_bytes_per_launch": int(alg_bytes),
             "note": "serial per-config event loop: latency-bound (one warp per config), not HBM-bound; "
                     "see ns_per_step_per_config", "launch": launch,
             "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2)}
