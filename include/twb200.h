@@ -46,7 +46,7 @@ extern "C" {
 
 /* ---- predictor set ("pset") blob ------------------------------------------ */
 /* One contiguous, 16-byte aligned byte blob holding every predictor a sweep uses:
- *   tw_pset_header | tw_pred_desc[n_desc] | table pool
+ *   tw_pset_header | tw_pred_desc[n_desc] | table pool | bulk-lookup section
  * A table (kind TABLE) occupies, at byte offset `table_off` from the blob start:
  *   int32 paxis[np] (sorted, unique) | int32 daxis[nd] (sorted, unique) |
  *   (pad to 8) | int64 grid_us[np*nd] (row-major [p][d]; TW_TABLE_HOLE = no row) |
@@ -54,8 +54,23 @@ extern "C" {
  *   int16 lutp[34][2], lutd[34][2]: for b = bitlen(v - axis[0]), the floor index of v
  *   (largest i with axis[i] <= v) lies in [lut[b][0], lut[b][1]] |
  *   int32 grid32[np*nd] (only when desc.pad == 1: every value < 2^31 us)
- * The blob is built on host (paper_2601_00397_b200/predictor.py::PredictorSet) and
- * staged whole into shared memory by each CTA with one cp.async.bulk (TMA). */
+ * Bulk-lookup section (derived data for the bulk predictor kernels; byte offsets
+ * below are from the blob start and stored in 16-byte units):
+ *   uint32 qhdr[n_desc][2] (padded to 16 B): w0 = quads16 | prec16 << 16,
+ *     w1 = drec16 | nd << 16 | TW_QHDR_FAST (bit 31: the table takes the fast path)
+ *   axis record sets, one per DISTINCT axis (tables on a common grid share them):
+ *     int32 rec[32][4] = {lo, hi, info, 0} for b = bitlen(v), v >= 0: every v of
+ *     that bit length inside [axis[0], axis[n-1]] has floor index i = info & 0xffff
+ *     (info < 0: the bucket straddles several intervals -> generic path);
+ *     lo = axis[i], hi = axis[i+1] (axis[i] at the last index); v outside [lo, hi]
+ *     is outside the axis
+ *   int32 quads[np][nd][4] per fast table = {c[i][j], c[i+1][j], c[i][j+1],
+ *     c[i+1][j+1]} (indices clamped at the last row/column; holes = -1)
+ * The event loop needs only the first core_bytes (pass that as pset_bytes to
+ * tw_sim_many); the bulk predictor kernels take the whole blob. The blob is built on
+ * host (paper_2601_00397_b200/predictor.py::PredictorSet) and staged into shared
+ * memory by each CTA with cp.async.bulk (TMA). */
+#define TW_QHDR_FAST 0x80000000u
 #define TW_PSET_MAGIC 0x54534550u /* "PEST" little-endian */
 #define TW_PRED_CONSTANT 0        /* predictor.py:100-111 */
 #define TW_PRED_LINEAR 1          /* predictor.py:114-146 */
@@ -64,10 +79,14 @@ extern "C" {
 
 typedef struct tw_pset_header {
   uint32_t magic;
-  uint32_t version;
+  uint32_t version;     /* 2 */
   int32_t n_desc;
-  int32_t total_bytes; /* whole blob, multiple of 16 */
-} tw_pset_header;      /* 16 B */
+  int32_t total_bytes;  /* whole blob, multiple of 16 */
+  int32_t core_bytes;   /* header | descs | table pool: all the event loop reads */
+  int32_t fast_off;     /* == core_bytes: start of the bulk-lookup section (below) */
+  int32_t n_axis_sets;  /* distinct table axes in the bulk-lookup section */
+  int32_t reserved;
+} tw_pset_header;       /* 32 B */
 
 typedef struct tw_pred_desc {
   int32_t kind;                /* TW_PRED_* */

@@ -24,6 +24,7 @@ TW_PRED_EMPTY_BATCH, TW_PRED_NEGATIVE, TW_PRED_TABLE_MISS, TW_PRED_BAD_DESC = -1
 TW_PSET_MAGIC = 0x54534550
 TW_PRED_CONSTANT, TW_PRED_LINEAR, TW_PRED_TABLE = 0, 1, 2
 TW_TABLE_HOLE = -1
+TW_QHDR_FAST = 0x80000000
 
 TW_OP_REGISTER_ACTOR, TW_OP_REGISTER_OBSERVER, TW_OP_SEAL, TW_OP_JUMP = 0, 1, 2, 3
 TW_OP_ENTER, TW_OP_DEREGISTER, TW_OP_ADVANCE_CLOCK, TW_OP_BAD_CLIENT = 4, 5, 6, 7
@@ -51,7 +52,8 @@ EVENT_KIND_NAMES = ("FIRST_TOKEN", "OUTPUT_TOKEN", "FINISHED")
 
 # ---- struct mirrors ----------------------------------------------------------------
 PSET_HEADER_DTYPE = np.dtype(
-    [("magic", "<u4"), ("version", "<u4"), ("n_desc", "<i4"), ("total_bytes", "<i4")]
+    [("magic", "<u4"), ("version", "<u4"), ("n_desc", "<i4"), ("total_bytes", "<i4"),
+     ("core_bytes", "<i4"), ("fast_off", "<i4"), ("n_axis_sets", "<i4"), ("reserved", "<i4")]
 )
 PRED_DESC_DTYPE = np.dtype(
     [

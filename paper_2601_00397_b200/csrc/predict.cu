@@ -7,12 +7,16 @@
 // work: the predictor blob (descriptors + calibration tables, a few KB) is staged
 // once per CTA into shared memory by one TMA bulk copy; the query streams are read
 // with 16-byte vector loads marked evict-first, each thread handling 4 queries per
-// iteration for memory-level parallelism; grid = a multiple of the 148 SMs.
+// iteration for memory-level parallelism; grid = one 1024-thread CTA per SM (A/B on
+// B200: 1024x1 > 640x2 > 512x2 > 256x3; profiles/README.md).
 #include "common.cuh"
 
 namespace twb {
 
-constexpr int kPredThreads = 256;
+#ifndef TWB_PRED_THREADS
+#define TWB_PRED_THREADS 1024
+#endif
+constexpr int kPredThreads = TWB_PRED_THREADS;
 
 struct PsetSmem {
   static __device__ __forceinline__ char* stage(const void* pset, uint32_t bytes) {
@@ -24,14 +28,76 @@ struct PsetSmem {
   }
 };
 
-__device__ __forceinline__ int64_t predict_one(const char* ps, int n_desc, int32_t p, int32_t d, int64_t c,
-                                               int32_t id) {
-  if (p == 0 && d == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
+// Exact RN(a / g) for an integer gap g > 0: a power-of-two gap scales exactly (a is an
+// integer or a product of magnitude >= 1, so no underflow); any other gap takes the
+// reciprocal division (div_rn_rcp, == __ddiv_rn).
+__device__ __forceinline__ double div_gap(double a, int32_t g) {
+  if ((g & (g - 1)) == 0) {
+    const int k = __ffs(g) - 1;
+    return __dmul_rn(a, __hiloint2double((1023 - k) << 20, 0));
+  }
+  const double gd = (double)g;
+  return div_rn_rcp(a, gd, __drcp_rn(gd));
+}
+
+// Everything the bulk-lookup section cannot answer (non-table kinds, int64 grids,
+// ambiguous axis buckets, out-of-range keys, holes): the generic predictor, kept out
+// of line so the common path stays short.
+__device__ __noinline__ int64_t predict_generic(const char* ps, int n_desc, int32_t id, int32_t p, int32_t d,
+                                                int64_t c) {
   return predict_bulk(ps, n_desc, id, p, d, c);
 }
 
+// One query through the bulk-lookup section (twb200.h): one 8-byte descriptor header,
+// one 16-byte axis record per axis (shared by every table on the same axis, so lanes
+// on different tables mostly hit the same records), one 16-byte corner quad; exact
+// fp64 lerps in the reference's order (predictor.py:209-236).
+__device__ __forceinline__ int64_t predict_one(const char* ps, const uint2* qh, int n_desc, int32_t p, int32_t d,
+                                               int64_t c, int32_t id) {
+  if ((p | d) == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
+  if ((unsigned)id < (unsigned)n_desc && (p | d) >= 0) {
+    const uint2 h = qh[id];
+    if (h.y & TW_QHDR_FAST) {
+      const int4* rec = reinterpret_cast<const int4*>(ps);
+      const int4 rp = rec[(h.x >> 16) + (32 - __clz(p))];
+      const int4 rd = rec[(h.y & 0xffffu) + (32 - __clz(d))];
+      if ((rp.z | rd.z) >= 0 && p >= rp.x && p <= rp.y && d >= rd.x && d <= rd.y) {
+        const int nd = (int)((h.y >> 16) & 0x7fffu);
+        const int4 q = rec[(h.x & 0xffffu) + rp.z * nd + rd.z];
+        const bool pex = p == rp.x, dex = d == rd.x;
+        const int32_t c00 = q.x;
+        const int32_t c10 = pex ? c00 : q.y;
+        const int32_t c01 = dex ? c00 : q.z;
+        const int32_t c11 = pex ? c01 : (dex ? c10 : q.w);
+        if ((c00 | c10 | c01 | c11) >= 0) {  // holes are the only negative entries
+          double us;
+          if (pex) {
+            us = dex ? (double)c00
+                     : __dadd_rn((double)c00, div_gap(__ll2double_rn((int64_t)(c01 - c00) * (d - rd.x)), rd.y - rd.x));
+          } else {
+            const int32_t gp = rp.y - rp.x, xp = p - rp.x;
+            const double a0 = __dadd_rn((double)c00, div_gap(__ll2double_rn((int64_t)(c10 - c00) * xp), gp));
+            if (dex) {
+              us = a0;
+            } else {
+              const double a1 = __dadd_rn((double)c01, div_gap(__ll2double_rn((int64_t)(c11 - c01) * xp), gp));
+              us = __dadd_rn(a0, div_gap(__dmul_rn(__dsub_rn(a1, a0), (double)(d - rd.x)), rd.y - rd.x));
+            }
+          }
+          return __double2ll_rn(us) * 1000;
+        }
+      }
+    }
+  }
+  return predict_generic(ps, n_desc, id, p, d, c);
+}
+
+__device__ __forceinline__ const uint2* pset_qhdr(const char* ps) {
+  return reinterpret_cast<const uint2*>(ps + reinterpret_cast<const tw_pset_header*>(ps)->fast_off);
+}
+
 #ifndef TWB_PRED_MIN_BLOCKS
-#define TWB_PRED_MIN_BLOCKS 5
+#define TWB_PRED_MIN_BLOCKS 1
 #endif
 __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_features(
     const void* __restrict__ pset, uint32_t pset_bytes, const int32_t* __restrict__ P,
@@ -39,6 +105,7 @@ __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_f
     int64_t n, int64_t* __restrict__ out) {
   const char* ps = PsetSmem::stage(pset, pset_bytes);
   const int n_desc = pset_ndesc(ps);
+  const uint2* qh = pset_qhdr(ps);
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // vector body: groups of 4 consecutive queries (all arrays 16-B aligned by contract)
@@ -50,14 +117,14 @@ __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_f
     const longlong2 c01 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g);
     const longlong2 c23 = __ldcs(reinterpret_cast<const longlong2*>(C) + 2 * g + 1);
     longlong2 o01, o23;
-    o01.x = predict_one(ps, n_desc, p4.x, d4.x, c01.x, i4.x);
-    o01.y = predict_one(ps, n_desc, p4.y, d4.y, c01.y, i4.y);
-    o23.x = predict_one(ps, n_desc, p4.z, d4.z, c23.x, i4.z);
-    o23.y = predict_one(ps, n_desc, p4.w, d4.w, c23.y, i4.w);
+    o01.x = predict_one(ps, qh, n_desc, p4.x, d4.x, c01.x, i4.x);
+    o01.y = predict_one(ps, qh, n_desc, p4.y, d4.y, c01.y, i4.y);
+    o23.x = predict_one(ps, qh, n_desc, p4.z, d4.z, c23.x, i4.z);
+    o23.y = predict_one(ps, qh, n_desc, p4.w, d4.w, c23.y, i4.w);
     __stcs(reinterpret_cast<longlong2*>(out) + 2 * g, o01);
     __stcs(reinterpret_cast<longlong2*>(out) + 2 * g + 1, o23);
   }
-  for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, n_desc, P[i], D[i], C[i], id[i]);
+  for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, qh, n_desc, P[i], D[i], C[i], id[i]);
 }
 
 // Fused extraction + prediction. One thread per batch; its slots are a contiguous
@@ -67,6 +134,8 @@ __global__ void __launch_bounds__(kPredThreads) k_predict_batches(
     const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx, const int32_t* __restrict__ id,
     int64_t nb, int64_t* __restrict__ feat, int64_t* __restrict__ out) {
   const char* ps = PsetSmem::stage(pset, pset_bytes);
+  const int n_desc = pset_ndesc(ps);
+  const uint2* qh = pset_qhdr(ps);
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += nthreads) {
     const int64_t s0 = off[b], s1 = off[b + 1];
@@ -82,7 +151,10 @@ __global__ void __launch_bounds__(kPredThreads) k_predict_batches(
       feat[3 * b + 1] = Dn;
       feat[3 * b + 2] = Ct;
     }
-    out[b] = (s1 == s0) ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(ps, id[b], Pt, Dn, Ct);
+    const int32_t ib = id[b];
+    if (s1 == s0) out[b] = TW_PRED_EMPTY_BATCH;
+    else if (((Pt | Dn) >> 31) == 0 && Ct >= 0) out[b] = predict_one(ps, qh, n_desc, (int32_t)Pt, (int32_t)Dn, Ct, ib);
+    else out[b] = predict_scalar(ps, ib, Pt, Dn, Ct);
   }
 }
 

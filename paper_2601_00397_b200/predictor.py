@@ -38,6 +38,7 @@ from ._lib import (
     TW_PRED_TABLE,
     TW_PRED_TABLE_MISS,
     TW_PSET_MAGIC,
+    TW_QHDR_FAST,
     TW_TABLE_HOLE,
 )
 
@@ -329,8 +330,51 @@ def _bitlen_lut(axis: np.ndarray) -> np.ndarray:
     return lut
 
 
+# shared-memory staging budget of the predictor kernels (predict.cu check_pset); the
+# bulk-lookup section only covers the tables that fit beside the core blob
+PSET_SMEM_BUDGET = 200 * 1024 - 128
+
+
 def _align(n: int, a: int) -> int:
     return (n + a - 1) // a * a
+
+
+def _axis_records(axis: np.ndarray) -> np.ndarray:
+    """Bulk-lookup records of one axis (twb200.h): for b = bitlen(v) of v >= 0, the
+    floor interval shared by every in-range v of that bit length, as {lo, hi, info, 0};
+    info = interval index, or -1 when the bucket straddles several intervals."""
+    a = np.asarray(axis, np.int64)
+    n = len(a)
+    rec = np.zeros((32, 4), np.int32)
+    for b in range(32):
+        low = 0 if b == 0 else (1 << (b - 1))
+        high = 0 if b == 0 else (1 << b) - 1
+        lo_v, hi_v = max(low, int(a[0])), min(high, int(a[-1]))
+        if lo_v > hi_v:  # bucket entirely outside the axis: any v fails lo <= v <= hi
+            edge = int(a[0]) if high < a[0] else int(a[-1])
+            rec[b] = (edge, edge, 0, 0)
+            continue
+        i_lo = int(np.searchsorted(a, lo_v, side="right")) - 1
+        i_hi = int(np.searchsorted(a, hi_v, side="right")) - 1
+        if i_lo != i_hi:
+            rec[b] = (0, 0, -1, 0)
+            continue
+        nxt = int(a[i_lo + 1]) if i_lo + 1 < n else int(a[i_lo])
+        rec[b] = (int(a[i_lo]), nxt, i_lo, 0)
+    return rec
+
+
+def _quads(grid32: np.ndarray) -> np.ndarray:
+    """{c[i][j], c[i+1][j], c[i][j+1], c[i+1][j+1]} per cell, indices clamped."""
+    np_, nd = grid32.shape
+    i1 = np.minimum(np.arange(np_) + 1, np_ - 1)
+    j1 = np.minimum(np.arange(nd) + 1, nd - 1)
+    q = np.empty((np_, nd, 4), np.int32)
+    q[:, :, 0] = grid32
+    q[:, :, 1] = grid32[i1, :]
+    q[:, :, 2] = grid32[:, j1]
+    q[:, :, 3] = grid32[i1][:, j1]
+    return q
 
 
 class PredictorSet:
@@ -370,20 +414,57 @@ class PredictorSet:
                 descs[i]["table_off"] = cursor
                 pool.append(blob)
                 cursor += len(blob)
-        total = _align(cursor, 16)
+        core = _align(cursor, 16)
+        # bulk-lookup section: per-descriptor headers, deduplicated axis records, quads
+        qhdr = np.zeros((n, 2), np.uint32)
+        fast = bytearray(b"\0" * _align(qhdr.nbytes, 16))
+        sets: dict[bytes, int] = {}
+
+        def axis_set(axis) -> int:
+            key = np.asarray(axis, np.int32).tobytes()
+            if key not in sets:
+                sets[key] = core + len(fast)
+                fast.extend(_axis_records(axis).tobytes())
+            return sets[key]
+
+        for i, p in enumerate(self.predictors):
+            tab = p._table()
+            if tab is None:
+                continue
+            pax, dax, grid = tab
+            if not (descs[i]["pad"] == 1 and pax[0] >= 0 and dax[0] >= 0
+                    and len(pax) < 2**15 and len(dax) < 2**15):
+                continue  # generic path only (int64-grid or negative-axis tables)
+            need = 16 * len(pax) * len(dax) + sum(
+                32 * 16 for a in (pax, dax) if np.asarray(a, np.int32).tobytes() not in sets)
+            if core + len(fast) + need > PSET_SMEM_BUDGET:
+                continue  # the whole blob must fit the kernels' shared-memory staging budget
+            prec, drec = axis_set(pax), axis_set(dax)
+            quads = core + len(fast)
+            fast.extend(_quads(grid.astype(np.int32)).tobytes())
+            qhdr[i, 0] = (quads // 16) | ((prec // 16) << 16)
+            qhdr[i, 1] = (drec // 16) | (len(dax) << 16) | TW_QHDR_FAST
+        fast[: qhdr.nbytes] = qhdr.tobytes()
+        total = core + _align(len(fast), 16)
         hdr = np.zeros((), PSET_HEADER_DTYPE)
         hdr["magic"] = TW_PSET_MAGIC
-        hdr["version"] = 1
+        hdr["version"] = 2
         hdr["n_desc"] = n
         hdr["total_bytes"] = total
+        hdr["core_bytes"] = core
+        hdr["fast_off"] = core
+        hdr["n_axis_sets"] = len(sets)
         buf = bytearray(total)
-        buf[0:16] = hdr.tobytes()
-        buf[16 : 16 + descs.nbytes] = descs.tobytes()
+        hs = PSET_HEADER_DTYPE.itemsize
+        buf[0:hs] = hdr.tobytes()
+        buf[hs : hs + descs.nbytes] = descs.tobytes()
         pos = off
         for blob in pool:
             buf[pos : pos + len(blob)] = blob
             pos += len(blob)
+        buf[core : core + len(fast)] = fast
         self.blob = np.frombuffer(bytes(buf), np.uint8)
+        self.core_nbytes = core
         self._dev: dict = {}
 
     @property

@@ -262,7 +262,7 @@ class DeviceSweep:
 
     @property
     def h2d_bytes(self) -> int:
-        n = self.pset.nbytes + self.cfgs.nbytes + self.order.nbytes + self.workloads.nbytes
+        n = self.pset.core_nbytes + self.cfgs.nbytes + self.order.nbytes + self.workloads.nbytes
         if self.per_request:
             n += self.req_base.nbytes
         return int(n)
@@ -271,7 +271,7 @@ class DeviceSweep:
         from ._device import ptr, stream_handle
 
         rc = _lib.load().tw_sim_many(
-            self.d_pset.data_ptr(), self.pset.nbytes, self.d_cfgs.data_ptr(), self.n_cfg,
+            self.d_pset.data_ptr(), self.pset.core_nbytes, self.d_cfgs.data_ptr(), self.n_cfg,
             self.d_order.data_ptr(), self.d_wl_off.data_ptr(), self.d_ts.data_ptr(),
             self.d_prompt.data_ptr(), self.d_output.data_ptr(), self.d_res.data_ptr(),
             ptr(self.d_req_base), ptr(self.d_first), ptr(self.d_finish), ptr(self.d_ev_off),
@@ -373,7 +373,8 @@ class HostSweep(DeviceSweep):
 
         super().__init__(*args, **kwargs)
         self._pairs_in = []
-        for d in (self.d_pset, self.d_cfgs, self.d_order, self.d_wl_off, self.d_ts, self.d_prompt, self.d_output):
+        core = self.d_pset[: self.pset.core_nbytes]  # the event loop reads only the core blob
+        for d in (core, self.d_cfgs, self.d_order, self.d_wl_off, self.d_ts, self.d_prompt, self.d_output):
             h = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
             h.copy_(d.cpu())
             self._pairs_in.append((d, h))

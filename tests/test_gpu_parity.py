@@ -60,6 +60,45 @@ def test_predict_features_equals_oracle_on_random_sweep():
     assert np.array_equal(got, want)
 
 
+def test_predict_features_random_tables_equals_oracle():
+    """Bulk-lookup section vs the C oracle on irregular tables: random (non-power-of-two)
+    axes, so buckets straddle intervals and gaps take the reciprocal division; holes;
+    keys on, beside and outside the axes; int64-valued and Linear/Constant neighbours."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import ConstantPredictor, LinearPredictor, PredictorSet, TablePredictor
+
+    rng = np.random.default_rng(11)
+    preds = []
+    for k in range(24):
+        pax = np.unique(rng.integers(0 if k % 3 else 5, 9000, rng.integers(2, 40)))
+        dax = np.unique(rng.integers(0, 600, rng.integers(1, 30)))
+        hole = rng.random() * 0.3
+        lo, hi = (2**31, 2**32) if k == 5 else (0, 2_000_000)  # k == 5: int64 grid, generic path
+        rows = {(int(p), int(d)): int(rng.integers(lo, hi)) for p in pax for d in dax if rng.random() >= hole}
+        rows.setdefault((int(pax[0]), int(dax[0])), 1)
+        preds.append(TablePredictor(rows, allow_extrapolation=bool(k % 2)))
+    preds += [ConstantPredictor(123), LinearPredictor(10.5, 0.25, 3.0, 0.001)]
+    pset = PredictorSet(preds)
+    n = 1 << 20
+    ids = rng.integers(0, len(preds), n).astype(np.int32)
+    P = rng.integers(-3, 9100, n).astype(np.int32)
+    D = rng.integers(-2, 620, n).astype(np.int32)
+    on = rng.random(n) < 0.3  # keys exactly on an axis value of their own table
+    for i in np.nonzero(on)[0][:50_000]:
+        t = preds[ids[i]]
+        if isinstance(t, TablePredictor):
+            P[i] = rng.choice(t._prefill_axis)
+            D[i] = rng.choice(t._decode_axis) if rng.random() < 0.5 else D[i]
+    C = rng.integers(0, 700_000, n).astype(np.int64)
+    C[::97] = -1
+    P[::97] = 0
+    D[::97] = 0
+    got = pset.predict_features(P, D, C, ids)
+    want = orc.predict_many(pset.blob, P, D, C, ids)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, [(int(ids[i]), int(P[i]), int(D[i]), int(got[i]), int(want[i])) for i in bad[:5]]
+
+
 def test_reciprocal_division_equals_hardware_division():
     """div_rn_rcp (multiply + 2 FMA corrections) == __ddiv_rn on 2^28 operand pairs."""
     import torch

@@ -74,9 +74,10 @@ def test_pset_blob_layout_round_trips():
                        build_predictor({"kind": "linear", "base_us": 1.5, "per_decode_us": 2.0})])
     blob = ps.blob
     assert blob.size % 16 == 0
-    hdr = blob[:16].view(PSET_HEADER_DTYPE)[0]
+    hdr = blob[:32].view(PSET_HEADER_DTYPE)[0]
     assert hdr["magic"] == _lib.TW_PSET_MAGIC and hdr["n_desc"] == 3 and hdr["total_bytes"] == blob.size
-    descs = blob[16 : 16 + 3 * 64].view(PRED_DESC_DTYPE)
+    assert hdr["version"] == 2 and hdr["core_bytes"] == hdr["fast_off"] == ps.core_nbytes
+    descs = blob[32 : 32 + 3 * 64].view(PRED_DESC_DTYPE)
     assert descs["kind"].tolist() == [0, 2, 1]
     assert descs[0]["constant_us"] == 7 and descs[2]["per_decode_us"] == 2.0
     off, np_, nd = int(descs[1]["table_off"]), int(descs[1]["np"]), int(descs[1]["nd"])
@@ -224,3 +225,58 @@ def test_sharded_gather_world2_gloo():
         assert steps == [i * 10 for i in range(37)]
         assert final == [i + 1_790_000_000_000_000_000 for i in range(37)]
         assert dig == [(i * 0x9E3779B97F4A7C15) % (1 << 64) for i in range(37)]
+
+
+def test_bulk_lookup_section_decodes_to_the_tables():
+    """The derived bulk-lookup section (twb200.h) answers every in-range key with the
+    same bracket and corners as the table itself: records by bit length give the floor
+    interval, quads give the four grid corners (CPU decode of the blob the GPU reads)."""
+    from _fixtures import predictor_golden
+
+    _, preds, *_ = predictor_golden()
+    ps = PredictorSet(list(preds) + list(presets.calibration_set().predictors))
+    blob = ps.blob
+    hdr = blob[:32].view(PSET_HEADER_DTYPE)[0]
+    n = int(hdr["n_desc"])
+    qh = blob[int(hdr["fast_off"]) : int(hdr["fast_off"]) + 8 * n].view(np.uint32).reshape(n, 2)
+    words = blob.view(np.int32)
+    rng = np.random.default_rng(3)
+    n_fast = 0
+    for k, p in enumerate(ps.predictors):
+        tab = p._table()
+        if not (int(qh[k, 1]) & _lib.TW_QHDR_FAST):
+            assert tab is None or tab[2].max() >= 2**31 or tab[0][0] < 0 or tab[1][0] < 0
+            continue
+        n_fast += 1
+        pax, dax, grid = tab
+        nd = (int(qh[k, 1]) >> 16) & 0x7FFF
+        assert nd == len(dax)
+        quads = int(qh[k, 0]) & 0xFFFF
+        recs = {"p": int(qh[k, 0]) >> 16, "d": int(qh[k, 1]) & 0xFFFF}
+
+        def look(which, v):
+            r = words[(recs[which] + int(v).bit_length()) * 4 :][:3]
+            return int(r[0]), int(r[1]), int(r[2])
+
+        qp = np.concatenate([pax, pax + 1, pax - 1, rng.integers(0, int(pax[-1]) + 2, 200)])
+        qd = np.concatenate([dax, dax + 1, dax - 1, rng.integers(0, int(dax[-1]) + 2, 200)])
+        for which, axis, qs in (("p", pax, qp), ("d", dax, qd)):
+            for v in qs[qs >= 0]:
+                lo, hi, info = look(which, v)
+                inside = axis[0] <= v <= axis[-1]
+                if info < 0:
+                    continue  # the bucket straddles several intervals: generic path
+                if not (lo <= v <= hi):
+                    assert not inside
+                    continue
+                assert inside
+                i = int(np.searchsorted(axis, v, side="right")) - 1
+                assert (info, lo) == (i, int(axis[i]))
+                assert hi == (int(axis[i + 1]) if i + 1 < len(axis) else int(axis[i]))
+        for i in range(len(pax)):
+            for j in range(len(dax)):
+                q = words[(quads * 16) // 4 + 4 * (i * nd + j) :][:4]
+                i1, j1 = min(i + 1, len(pax) - 1), min(j + 1, len(dax) - 1)
+                assert q.tolist() == [grid[i, j], grid[i1, j], grid[i, j1], grid[i1, j1]]
+    assert n_fast >= 16
+    assert int(hdr["n_axis_sets"]) < 2 * n_fast  # calibration tables share their axes
