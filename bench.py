@@ -210,6 +210,22 @@ def predictor_roofline(device, peak_gbs):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
 
 
+def metrics_roofline(dev, args, flush, stream, peak_gbs):
+    """tw_metrics_many over the sweep's stamps: every config's
+    RunReport.summary() numbers. Algorithmic bytes: first + finish stamps (16 B),
+    arrival offset (8 B) and output count (4 B) per request, 160 B out per config."""
+    durs = time_kernel_steps(dev.run_metrics, args.steps, args.warmup, flush, stream)
+    ms = sum(durs) / len(durs)
+    m = dev.fetch_metrics()
+    n_req = int(dev.req_base[-1])
+    alg = 28 * n_req + 160 * dev.n_cfg
+    gbs = alg / (ms / 1e3) / 1e9
+    return {"kernel": "k_metrics", "bound": "hbm", "achieved": round(gbs, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(gbs / peak_gbs, 4), "traffic": measured_traffic("k_metrics"), "ms_per_launch": round(ms, 4),
+            "configs_per_s": round(dev.n_cfg / (ms / 1e3), 1), "requests_per_s": round(n_req / (ms / 1e3), 1),
+            "all_ok": bool((m["status"] == 0).all()), "algorithmic_bytes_per_launch": int(alg)}
+
+
 def cpu_baseline(sw, budget_s: float, n_threads: int):
     """The C oracle port over a stratified sample of the same sweep, all host threads."""
     from oracle import oracle as orc
@@ -371,7 +387,7 @@ def main():
     n_req = int(dev.req_base[-1])
     alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req  # configs in, records out, stamps out
                  + 16 * n_req  # each config reads its workload (ts 8 + prompt 4 + output 4 B/request)
-                 + dev.pset.nbytes * _lib.last_sim_launch()["grid"])
+                 + dev.pset.core_nbytes * _lib.last_sim_launch()["grid"])
     achieved = alg_bytes / (ms / 1e3) / 1e9
     launch = _lib.last_sim_launch()
     roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
@@ -387,6 +403,10 @@ def main():
             extra["predictor_roofline"] = predictor_roofline(device, peak_gbs)
         except Exception as exc:  # report, never hide
             extra["predictor_roofline"] = {"error": repr(exc)}
+        try:
+            extra["metrics_reduction"] = metrics_roofline(dev, args, flush, stream, peak_gbs)
+        except Exception as exc:
+            extra["metrics_reduction"] = {"error": repr(exc)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(sw, args.cpu_budget_s, os.cpu_count() or 1)

@@ -291,6 +291,49 @@ int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
  * cycles, predict cycles, apply cycles, 0, 0, 0, 0}. */
 int tw_sim_set_profile(int64_t* per_config_16xi64);
 
+/* ---- per-config latency metrics: metrics.py:62-253 ------ */
+/* RunReport.summary() of an oracle-mode run (runner.py:339-365), reduced on device
+ * from the per-request stamps tw_sim_many wrote: TTFT = first - epoch - offset,
+ * e2e = finish - epoch - offset, TPOT = (finish - first) / (output - 1) for outputs
+ * > 1 (metrics.py:49-62); nearest-rank p50/p90/p99 with rank = ceil(p/100.0 * n)
+ * (metrics.py:65-71) and mean = Python sum()/len, i.e. Neumaier-compensated
+ * summation in request order (CPython >= 3.12 sum of floats) then one division. */
+#define TW_METRICS_OK 0
+#define TW_METRICS_INCOMPLETE 1  /* some request has no FINISHED stamp (IncompleteLog) */
+#define TW_METRICS_SIM_FAILED 2  /* the config's tw_sim_result status is not OK      */
+#define TW_METRICS_TOO_LARGE 3   /* more requests than max_requests                   */
+
+typedef struct tw_latency_stats {
+  double p50, p90, p99, mean;
+  int64_t count; /* 0: no values (the summary omits the entry) */
+} tw_latency_stats; /* 40 B */
+
+typedef struct tw_run_metrics {
+  int64_t num_requests;
+  int64_t output_tokens;
+  int64_t virtual_elapsed_ns; /* max FINISHED - epoch (metrics.py:245) */
+  double tokens_per_virtual_s;
+  tw_latency_stats ttft, e2e, tpot;
+  int32_t status; /* TW_METRICS_* */
+  int32_t n_missing;
+} tw_run_metrics; /* 160 B */
+
+/* One CTA per config. Requests of config c are workload cfgs[c].workload_id's
+ * (CSR as in tw_sim_many) with stamps at req_base[c] + i (-1 = never stamped).
+ * sim (optional): tw_sim_many's records; a non-OK status gives TW_METRICS_SIM_FAILED.
+ * sum_order (optional, per workload request, CSR like the workload): the position
+ * of each request in the caller's arrival list, which sets the order of the
+ * compensated TPOT sum; NULL = the engine's (stable-sorted) order, which is the
+ * caller's order for sorted arrival lists such as generate_arrivals produces.
+ * max_requests: an upper bound on any workload's size (sizes shared memory; at most
+ * 16384). */
+int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off,
+                    const int64_t* req_offset_ns, const int32_t* req_output,
+                    const int64_t* req_base, const int64_t* req_first_ns,
+                    const int64_t* req_finish_ns, const tw_sim_result* sim,
+                    const int32_t* sum_order, int32_t max_requests, tw_run_metrics* out,
+                    void* stream);
+
 /* ---- misc ------------------------------------------------------------------ */
 int tw_abi_version(void);
 const char* tw_last_error(void);

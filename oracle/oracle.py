@@ -25,6 +25,7 @@ if ROOT not in sys.path:
 
 from paper_2601_00397_b200._lib import (  # noqa: E402  (struct layouts only)
     EVENT_DTYPE,
+    RUN_METRICS_DTYPE,
     SIM_RESULT_DTYPE,
     TK_EVENT_DTYPE,
     TK_FINAL_DTYPE,
@@ -63,6 +64,8 @@ def load():
         lib.orc_simulate.restype = None
         lib.orc_sim_many.argtypes = [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32]
         lib.orc_sim_many.restype = None
+        lib.orc_metrics.argtypes = [_I64, _P, _P, _P, _P, _I64, _P]
+        lib.orc_metrics.restype = None
         _lib = lib
     return _lib
 
@@ -144,6 +147,17 @@ def sim_many(blob, cfgs, wl_off, ts, prompt, output, n_threads=None, per_request
         _p(np.ascontiguousarray(output, np.int32)), _p(res), _p(req_base), _p(first), _p(finish), nt,
     )
     return res, req_base, first, finish
+
+
+def metrics(offset_ns, output, first, finish, epoch_ns: int) -> np.ndarray:
+    """RunReport.summary() numbers of one oracle-mode run (one RUN_METRICS_DTYPE record)."""
+    ts = np.ascontiguousarray(offset_ns, np.int64)
+    op = np.ascontiguousarray(output, np.int32)
+    f = np.ascontiguousarray(first, np.int64)
+    g = np.ascontiguousarray(finish, np.int64)
+    out = np.zeros(1, RUN_METRICS_DTYPE)
+    load().orc_metrics(len(ts), _p(ts), _p(op), _p(f), _p(g), int(epoch_ns), _p(out))
+    return out[0]
 
 
 # ---- the event digest, restated in Python (twb200.h: tw_event_hash) ------------------

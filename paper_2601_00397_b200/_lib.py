@@ -119,6 +119,23 @@ SIM_RESULT_DTYPE = np.dtype(
     ]
 )
 EVENT_DTYPE = np.dtype([("ts_ns", "<i8"), ("step", "<i4"), ("req_kind", "<i4")])
+LATENCY_STATS_DTYPE = np.dtype(
+    [("p50", "<f8"), ("p90", "<f8"), ("p99", "<f8"), ("mean", "<f8"), ("count", "<i8")]
+)
+RUN_METRICS_DTYPE = np.dtype(
+    [
+        ("num_requests", "<i8"),
+        ("output_tokens", "<i8"),
+        ("virtual_elapsed_ns", "<i8"),
+        ("tokens_per_virtual_s", "<f8"),
+        ("ttft", LATENCY_STATS_DTYPE),
+        ("e2e", LATENCY_STATS_DTYPE),
+        ("tpot", LATENCY_STATS_DTYPE),
+        ("status", "<i4"),
+        ("n_missing", "<i4"),
+    ]
+)
+TW_METRICS_OK, TW_METRICS_INCOMPLETE, TW_METRICS_SIM_FAILED, TW_METRICS_TOO_LARGE = 0, 1, 2, 3
 
 assert PRED_DESC_DTYPE.itemsize == 64
 assert TK_OP_DTYPE.itemsize == 16
@@ -127,6 +144,7 @@ assert TK_FINAL_DTYPE.itemsize == 64
 assert SIM_CFG_DTYPE.itemsize == 64
 assert SIM_RESULT_DTYPE.itemsize == 64
 assert EVENT_DTYPE.itemsize == 16
+assert RUN_METRICS_DTYPE.itemsize == 160
 
 # every symbol include/twb200.h declares (tests check the .so exports all of them)
 EXPORTED_SYMBOLS = (
@@ -138,6 +156,7 @@ EXPORTED_SYMBOLS = (
     "tw_sim_many",
     "tw_sim_last_launch",
     "tw_sim_set_profile",
+    "tw_metrics_many",
     "tw_abi_version",
     "tw_last_error",
     "tw_launch_count",
@@ -168,6 +187,7 @@ _SIGNATURES = {
     ),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
     "tw_sim_set_profile": (_I32, [_P]),
+    "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "tw_abi_version": (_I32, []),
     "tw_last_error": (ctypes.c_char_p, []),
     "tw_launch_count": (_I64, []),

@@ -1,0 +1,306 @@
+// metrics.cu — per-config latency summary on device.
+//
+// Reference: metrics.py:38-124 (RequestOutcome, percentile, _stats, RunReport.summary)
+// and collect_metrics (metrics.py:173-253) over an oracle-mode event log
+// (runner.py:339-365). The event log itself never exists here: tw_sim_many already
+// wrote each request's FIRST_TOKEN and FINISHED stamps, which is all the summary
+// needs. One CTA per config:
+//   * one pass over the requests: missing stamps, output tokens, max FINISHED, exact
+//     int64 sums of TTFT and e2e (all partial sums of non-negative integers below
+//     2^53 are exact in fp64, so Python's compensated float sum equals them);
+//   * TPOT values (correctly rounded int/int divisions) are scattered into shared
+//     memory in the caller's arrival order and summed by one thread with CPython's
+//     Neumaier recurrence (bltinmodule.c builtin_sum, CPython >= 3.12);
+//   * each metric is sorted in shared memory (bitonic, order-preserving uint64 keys of
+//     the fp64 values) and the nearest ranks ceil(p/100.0*n) are read out.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace twb {
+
+#ifndef TWB_MET_THREADS
+#define TWB_MET_THREADS 128
+#endif
+constexpr int kMetThreads = TWB_MET_THREADS;
+constexpr int kMetWarps = kMetThreads / 32;
+constexpr int kMetMaxRequests = 16384;
+
+// total-order key of a non-NaN double (negatives flipped, positives offset)
+__device__ __forceinline__ uint64_t dkey(double v) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double dval(uint64_t k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// ascending bitonic sort of keys[0, m), m a power of two, whole CTA. Pair i is always
+// handled by warp (i / 32) % warps, and for strides j <= 32 both elements of every
+// pair of that warp lie in its own 64-element chunk, so those substeps only need
+// __syncwarp; CTA barriers surround the wider strides.
+__device__ void block_bitonic_sort(uint64_t* keys, int m) {
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 64) __syncthreads();
+      for (int i = threadIdx.x; i < (m >> 1); i += blockDim.x) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int hi = lo + j;
+        const uint64_t a = keys[lo], b = keys[hi];
+        if ((a > b) == ((lo & k) == 0)) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      if (j >= 64) __syncthreads();
+      else __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// 0-based index of the nearest-rank percentile p of n sorted values (metrics.py:65-71)
+__device__ __forceinline__ int nearest_rank_index(int p, int n) {
+  const double q = __dmul_rn(__ddiv_rn((double)p, 100.0), (double)n);
+  const int r = (int)ceil(q);
+  return (r < 1 ? 1 : r) - 1;
+}
+
+// CPython sum() of floats: Neumaier's compensated recurrence, then f += c when c is a
+// non-zero finite number. NaN entries (no value) are skipped.
+__device__ double neumaier_sum(const double* v, int n) {
+  double f = 0.0, c = 0.0;
+  for (int i = 0; i < n; i++) {
+    const double x = v[i];
+    if (isnan(x)) continue;
+    const double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+    f = t;
+  }
+  if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
+  return f;
+}
+
+struct MetParams {
+  const tw_sim_cfg* cfgs;
+  int32_t n_cfg;
+  const int64_t* wl_off;
+  const int64_t* ts;
+  const int32_t* output;
+  const int64_t* req_base;
+  const int64_t* first;
+  const int64_t* finish;
+  const tw_sim_result* sim;
+  const int32_t* sum_order;
+  int32_t cap;  // keys capacity (power of two)
+  tw_run_metrics* out;
+};
+
+struct BlockRed {
+  int64_t miss, tokens, maxfin, s_ttft, s_e2e, n_tpot;
+};
+
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t w = __shfl_xor_sync(kFull, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// sorts keys[0, n) (padded with UINT64_MAX to the next power of two) and fills st
+__device__ void stats_from_keys(uint64_t* keys, int n, int count, double mean, tw_latency_stats& st) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + threadIdx.x; i < m; i += blockDim.x) keys[i] = ~0ULL;
+  __syncthreads();
+  if (m > 1) block_bitonic_sort(keys, m);
+  if (threadIdx.x == 0) {
+    st.count = count;
+    if (count > 0) {
+      st.p50 = dval(keys[nearest_rank_index(50, count)]);
+      st.p90 = dval(keys[nearest_rank_index(90, count)]);
+      st.p99 = dval(keys[nearest_rank_index(99, count)]);
+      st.mean = mean;
+    } else {
+      st.p50 = st.p90 = st.p99 = st.mean = __longlong_as_double(0x7ff8000000000000LL);  // NaN: absent
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
+  extern __shared__ __align__(16) uint64_t keys[];
+  __shared__ int64_t red[6][kMetWarps];
+  __shared__ tw_run_metrics res;
+  __shared__ double sh_mean;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = blockIdx.x; c < p.n_cfg; c += gridDim.x) {
+    const tw_sim_cfg cfg = p.cfgs[c];
+    const int64_t wl0 = p.wl_off[cfg.workload_id];
+    const int n = (int)(p.wl_off[cfg.workload_id + 1] - wl0);
+    const int64_t rb = p.req_base[c];
+    const int64_t epoch = cfg.epoch_ns;
+    if (tid == 0) {
+      memset(&res, 0, sizeof(res));
+      res.num_requests = n;
+    }
+    int status = TW_METRICS_OK;
+    if (p.sim && (p.sim[c].status & 0xff) != TW_SIM_OK) status = TW_METRICS_SIM_FAILED;
+    else if (n > p.cap) status = TW_METRICS_TOO_LARGE;
+    __syncthreads();
+    if (status != TW_METRICS_OK) {
+      if (tid == 0) {
+        res.status = status;
+        p.out[c] = res;
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- pass 1: per-request reductions (collect_metrics, metrics.py:213-247)
+    BlockRed r = {0, 0, INT64_MIN, 0, 0, 0};
+    for (int i = tid; i < n; i += kMetThreads) {
+      const int64_t fin = p.finish[rb + i], fst = p.first[rb + i];
+      const int64_t off = p.ts[wl0 + i];
+      const int32_t op = p.output[wl0 + i];
+      if (fin < 0 || fst < 0) {
+        r.miss++;
+        continue;
+      }
+      r.tokens += op;
+      const int64_t fr = fin - epoch;
+      r.maxfin = fr > r.maxfin ? fr : r.maxfin;
+      r.s_ttft += fst - epoch - off;
+      r.s_e2e += fin - epoch - off;
+      r.n_tpot += op > 1;
+    }
+    int64_t v[6] = {r.miss, r.tokens, r.maxfin, r.s_ttft, r.s_e2e, r.n_tpot};
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      const int64_t w = (k == 2) ? warp_max_i64(v[k]) : warp_sum_i64(v[k]);
+      if (lane == 0) red[k][warp] = w;
+    }
+    __syncthreads();
+    if (tid < 32) {
+#pragma unroll
+      for (int k = 0; k < 6; k++) {
+        int64_t w = lane < kMetWarps ? red[k][lane] : (k == 2 ? INT64_MIN : 0);
+        w = (k == 2) ? warp_max_i64(w) : warp_sum_i64(w);
+        if (lane == 0) red[k][0] = w;
+      }
+    }
+    __syncthreads();
+    const int64_t miss = red[0][0], tokens = red[1][0], maxfin = red[2][0];
+    const int64_t s_ttft = red[3][0], s_e2e = red[4][0];
+    const int n_tpot = (int)red[5][0];
+    if (miss > 0) {  // IncompleteLog (metrics.py:236-240)
+      if (tid == 0) {
+        res.status = TW_METRICS_INCOMPLETE;
+        res.n_missing = (int32_t)miss;
+        p.out[c] = res;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) {
+      res.output_tokens = tokens;
+      res.virtual_elapsed_ns = n > 0 ? maxfin : 0;
+      // tokens_per_virtual_s = total / (virtual_elapsed_ns / NS_PER_S) (metrics.py:113-115)
+      const double vs = __ddiv_rn((double)res.virtual_elapsed_ns, 1e9);
+      res.tokens_per_virtual_s = vs > 0.0 ? __ddiv_rn((double)tokens, vs) : 0.0;
+    }
+    double* vals = reinterpret_cast<double*>(keys);
+    const int32_t* pos = p.sum_order ? p.sum_order + wl0 : nullptr;
+    // ---- TTFT, e2e: exact integer sums unless they could round, then the CPython sum
+    for (int m = 0; m < 2; m++) {
+      const int64_t s = m == 0 ? s_ttft : s_e2e;
+      const bool exact = s >= 0 && s < (1LL << 53);
+      if (!exact) {
+        for (int i = tid; i < n; i += kMetThreads) {
+          const int64_t t = (m == 0 ? p.first[rb + i] : p.finish[rb + i]) - epoch - p.ts[wl0 + i];
+          vals[pos ? pos[i] : i] = (double)t;
+        }
+        __syncthreads();
+        if (tid == 0) sh_mean = neumaier_sum(vals, n);
+        __syncthreads();
+      }
+      for (int i = tid; i < n; i += kMetThreads) {
+        const int64_t t = (m == 0 ? p.first[rb + i] : p.finish[rb + i]) - epoch - p.ts[wl0 + i];
+        keys[i] = dkey((double)t);
+      }
+      const double sum = exact ? (double)s : sh_mean;
+      stats_from_keys(keys, n, n, n > 0 ? __ddiv_rn(sum, (double)n) : 0.0, m == 0 ? res.ttft : res.e2e);
+    }
+    // ---- TPOT over requests with more than one output token (metrics.py:54-60, 100-101)
+    for (int i = tid; i < n; i += kMetThreads) {
+      const int32_t op = p.output[wl0 + i];
+      double t = __longlong_as_double(0x7ff8000000000000LL);
+      if (op > 1) t = __ddiv_rn((double)(p.finish[rb + i] - p.first[rb + i]), (double)(op - 1));
+      vals[pos ? pos[i] : i] = t;
+    }
+    __syncthreads();
+    if (tid == 0) sh_mean = n_tpot > 0 ? __ddiv_rn(neumaier_sum(vals, n), (double)n_tpot) : 0.0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kMetThreads) {
+      const double t = vals[i];
+      keys[i] = isnan(t) ? ~0ULL : dkey(t);
+    }
+    stats_from_keys(keys, n, n_tpot, sh_mean, res.tpot);
+    if (tid == 0) {
+      res.status = TW_METRICS_OK;
+      p.out[c] = res;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace twb
+
+using namespace twb;
+
+extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off,
+                               const int64_t* req_offset_ns, const int32_t* req_output,
+                               const int64_t* req_base, const int64_t* req_first_ns,
+                               const int64_t* req_finish_ns, const tw_sim_result* sim,
+                               const int32_t* sum_order, int32_t max_requests, tw_run_metrics* out,
+                               void* stream) {
+  if (n_cfg < 0 || (n_cfg > 0 && (!cfgs || !wl_off || !req_offset_ns || !req_output || !req_base ||
+                                  !req_first_ns || !req_finish_ns || !out))) {
+    set_error("tw_metrics_many: bad arguments");
+    return TW_EINVAL;
+  }
+  if (max_requests < 0 || max_requests > kMetMaxRequests) {
+    set_error("tw_metrics_many: max_requests %d outside [0, %d]", max_requests, kMetMaxRequests);
+    return TW_ENOSMEM;
+  }
+  if (n_cfg == 0) return TW_OK;
+  int cap = 1;
+  while (cap < max_requests) cap <<= 1;
+  const size_t smem = (size_t)cap * sizeof(uint64_t);
+  cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_metrics, kMetThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > n_cfg) grid = n_cfg;
+  MetParams p;
+  p.cfgs = cfgs;
+  p.n_cfg = n_cfg;
+  p.wl_off = wl_off;
+  p.ts = req_offset_ns;
+  p.output = req_output;
+  p.req_base = req_base;
+  p.first = req_first_ns;
+  p.finish = req_finish_ns;
+  p.sim = sim;
+  p.sum_order = sum_order;
+  p.cap = cap;
+  p.out = out;
+  k_metrics<<<(int)grid, kMetThreads, smem, (cudaStream_t)stream>>>(p);
+  count_launch();
+  return check_launch("tw_metrics_many");
+}

@@ -44,7 +44,25 @@ __device__ __forceinline__ long long twb_phase_barrier() {
 #define TWB_CLK() twb_phase_barrier()
 #endif
 
-constexpr int kSimThreads = 128;  // 4 warps per CTA
+// Code placement: the event loop's SASS (~4.5 k instructions) exceeds the instruction
+// caches, but moving the rare or duplicated paths (prediction-cache misses, the
+// Timekeeper walk) out of line measured slower (A/B 13.4 ms inline vs 14.2 / 15.5 ms;
+// profiles/README.md), so they stay inlined unless these switches are set.
+#ifdef TWB_SIM_OUTLINE_PRED
+#define TWB_PRED_FN __device__ __noinline__
+#else
+#define TWB_PRED_FN __device__ __forceinline__
+#endif
+#ifdef TWB_SIM_OUTLINE_TK
+#define TWB_TK_FN __device__ __noinline__
+#else
+#define TWB_TK_FN __device__ __forceinline__
+#endif
+
+#ifndef TWB_SIM_WARPS
+#define TWB_SIM_WARPS 4
+#endif
+constexpr int kSimThreads = 32 * TWB_SIM_WARPS;  // warps per CTA (one config per warp at a time)
 constexpr int kSimWarps = kSimThreads / 32;
 constexpr int kMaxSlotCap = 4096;
 
@@ -198,7 +216,7 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 // only resolves targets beyond V; a V that jumped several steps ahead (the FakeClock
 // wall outrunning short steps) is skipped in O(1). Each resolve is one BarrierCore
 // round with t_min = min(dispatcher's next arrival, the stage deadline).
-__device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
   int64_t per = d;
@@ -283,7 +301,7 @@ __device__ __forceinline__ void tk_run(TkGrid& g, const int64_t* __restrict__ ts
   }
 }
 
-__device__ __forceinline__ void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+TWB_TK_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                         int64_t end) {
   // idle jump: only the dispatcher drives time (its target is <= end while V < end)
   for (;;) {
@@ -296,6 +314,10 @@ __device__ __forceinline__ void tk_idle(TkGrid& g, const int64_t* __restrict__ t
 // Prediction cache: 32 entries held one per lane (key = P << 32 | D, for predictors
 // whose duration ignores C); a lookup is one compare + ballot + shuffle. Linear models
 // with a context term keep a single exact (P, D, C) entry.
+TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
+  return predict_warp(ps, id, P, D, C);
+}
+
 struct PredCache {
   int64_t key, val;    // this lane's entry
   int64_t P, D, C, d;  // single entry (uses_c)
@@ -308,7 +330,7 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const int lane = threadIdx.x & 31;
   if (pc.uses_c) {
     if (P == pc.P && D == pc.D && C == pc.C) return pc.d;
-    const int64_t d = predict_warp(ps, id, P, D, C);
+    const int64_t d = predict_miss(ps, id, P, D, C);
     pc.P = P;
     pc.D = D;
     pc.C = C;
@@ -318,7 +340,7 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const int64_t key = (P << 32) | D;
   const unsigned hit = __ballot_sync(kFull, pc.key == key);
   if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
-  const int64_t d = predict_warp(ps, id, P, D, C);
+  const int64_t d = predict_miss(ps, id, P, D, C);
   if (lane == pc.victim) {
     pc.key = key;
     pc.val = d;

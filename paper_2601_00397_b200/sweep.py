@@ -11,6 +11,10 @@ pkg/src/timewarp/engine.py:46-133):
   persistent launch and return fixed-size per-config records (steps, virtual span,
   event digest, Timekeeper state, status) plus optional per-request FIRST_TOKEN /
   FINISHED stamps and audited full event streams.
+* :meth:`DeviceSweep.run_metrics` reduces those stamps on device to each config's
+  ``RunReport.summary()`` numbers (metrics.py:38-253): TTFT / e2e / TPOT nearest-rank
+  p50/p90/p99 and means, output tokens, virtual span, tokens per virtual second;
+  :func:`summary_doc` renders one record in the reference's summary layout.
 """
 
 from __future__ import annotations
@@ -24,6 +28,9 @@ import numpy as np
 from . import _lib
 from ._lib import (
     EVENT_DTYPE,
+    RUN_METRICS_DTYPE,
+    TW_METRICS_INCOMPLETE,
+    TW_METRICS_OK,
     EVENT_KIND_NAMES,
     SIM_CFG_DTYPE,
     SIM_RESULT_DTYPE,
@@ -279,6 +286,35 @@ class DeviceSweep:
         )
         _lib.check(rc, "tw_sim_many")
 
+    # -- per-config latency summary (metrics.py:173-253) ---------------------------
+    def run_metrics(self, stream=None) -> None:
+        """Launch the on-device reduction of this sweep's stamps (needs per_request)."""
+        import torch
+
+        from ._device import stream_handle, to_device
+
+        if not self.per_request:
+            raise EngineError("run_metrics needs per-request stamps (DeviceSweep(per_request=True))")
+        if getattr(self, "d_metrics", None) is None:
+            self.d_metrics = torch.zeros(max(self.n_cfg, 1) * RUN_METRICS_DTYPE.itemsize, dtype=torch.uint8,
+                                         device=self.device)
+            ci = self.workloads.caller_index
+            self.d_sum_order = to_device(ci, self.device) if ci is not None and len(ci) else None
+            self.max_requests = int(self.workloads.sizes().max()) if self.workloads.n_workloads else 0
+        rc = _lib.load().tw_metrics_many(
+            self.d_cfgs.data_ptr(), self.n_cfg, self.d_wl_off.data_ptr(), self.d_ts.data_ptr(),
+            self.d_output.data_ptr(), self.d_req_base.data_ptr(), self.d_first.data_ptr(),
+            self.d_finish.data_ptr(), self.d_res.data_ptr(),
+            self.d_sum_order.data_ptr() if self.d_sum_order is not None else None, self.max_requests,
+            self.d_metrics.data_ptr(), stream_handle(stream),
+        )
+        _lib.check(rc, "tw_metrics_many")
+
+    def fetch_metrics(self) -> np.ndarray:
+        from ._device import to_numpy_struct
+
+        return to_numpy_struct(self.d_metrics, RUN_METRICS_DTYPE, self.n_cfg)
+
     def fetch(self) -> SweepResult:
         from ._device import to_numpy_struct
 
@@ -319,6 +355,39 @@ def simulate_many(
     sweep.run()
     torch.cuda.synchronize(sweep.device)
     return sweep.fetch()
+
+
+def summary_doc(rec, mode: str = "oracle", workload_fingerprint: str = "", wall_elapsed_ns: int = 0) -> dict:
+    """One RUN_METRICS_DTYPE record in RunReport.summary()'s layout (metrics.py:97-124)."""
+    from .workload import NS_PER_S
+
+    st = int(rec["status"])
+    if st == TW_METRICS_INCOMPLETE:
+        raise EngineError(f"IncompleteLog: {int(rec['n_missing'])} requests never finished")
+    if st != TW_METRICS_OK:
+        raise EngineError(f"metrics status {st}")
+    ve = int(rec["virtual_elapsed_ns"])
+    doc = {
+        "mode": mode,
+        "workload_fingerprint": workload_fingerprint,
+        "num_requests": int(rec["num_requests"]),
+        "virtual_elapsed_ns": ve,
+        "wall_elapsed_ns": wall_elapsed_ns,
+        "speedup": ve / wall_elapsed_ns if wall_elapsed_ns > 0 else float("inf"),
+        "output_tokens": int(rec["output_tokens"]),
+    }
+
+    def stats(s):
+        return {"p50": float(s["p50"]), "p90": float(s["p90"]), "p99": float(s["p99"]),
+                "mean": float(s["mean"]), "count": int(s["count"])}
+
+    if int(rec["num_requests"]) > 0:
+        doc["ttft_ns"] = stats(rec["ttft"])
+        doc["e2e_ns"] = stats(rec["e2e"])
+        doc["tokens_per_virtual_s"] = float(rec["tokens_per_virtual_s"]) if ve / NS_PER_S > 0 else 0.0
+    if int(rec["tpot"]["count"]) > 0:
+        doc["tpot_ns"] = stats(rec["tpot"])
+    return doc
 
 
 def _raise_status(res, what: str = "") -> None:

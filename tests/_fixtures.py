@@ -115,3 +115,40 @@ def tk_case_inputs(case):
     cfgs = config_array([SweepConfig(engine=eng, epoch_ns=case["epoch"], timekeeper=True,
                                      tk_cooldown_ns=case["cooldown"])])
     return pset, pack_arrivals([arr]), cfgs
+
+
+@functools.lru_cache(maxsize=None)
+def metrics_golden():
+    """[(record, oracle case)]: the reference's RunReport.summary() per oracle case."""
+    with open(os.path.join(GOLDEN, "metrics.json")) as fh:
+        recs = json.load(fh)
+    cases = {c["name"]: c for c in oracle_golden()[0]}
+    return [(r, cases[r["name"]]) for r in recs]
+
+
+def caller_order(case, perm):
+    """Workloads packed with the golden record's arrival-list order (perm: position ->
+    original index, None = the original list), so caller_index orders the TPOT sum."""
+    if case["arrivals"] is not None:
+        arr = [Arrival(r, o, p, q) for r, o, p, q in case["arrivals"]]
+    else:
+        arr = workload_for(case["workload"]["n"], tuple(case["workload"]["first"]))
+    if perm is not None:
+        arr = [arr[i] for i in perm]
+    return arr
+
+
+def assert_summary_equal(rec, golden, what=""):
+    """Bit-exact comparison of one RUN_METRICS_DTYPE record with a golden summary."""
+    assert int(rec["status"]) == 0, (what, int(rec["status"]))
+    for k in ("num_requests", "virtual_elapsed_ns", "output_tokens"):
+        assert int(rec[k]) == golden[k], (what, k, int(rec[k]), golden[k])
+    assert float(rec["tokens_per_virtual_s"]).hex() == golden["tokens_per_virtual_s"], what
+    for m, key in (("ttft", "ttft_ns"), ("e2e", "e2e_ns"), ("tpot", "tpot_ns")):
+        if key not in golden:
+            assert int(rec[m]["count"]) == 0, (what, m)
+            continue
+        g = golden[key]
+        assert int(rec[m]["count"]) == g["count"], (what, m)
+        for f in ("p50", "p90", "p99", "mean"):
+            assert float(rec[m][f]).hex() == g[f], (what, m, f, float(rec[m][f]).hex(), g[f])

@@ -19,6 +19,8 @@ Fixtures:
   tkgrid.npz     the event loop's Timekeeper actor grid driven through the real
                  BarrierCore on a FakeClock -> (seq, offset, wall) + broadcast digest
   arrivals.npz   generate_arrivals outputs for the sweep workloads
+  metrics.json   collect_metrics(...).summary() of the oracle cases (floats as hex),
+                 including arrival lists in shuffled order (the TPOT sum is ordered)
 """
 
 from __future__ import annotations
@@ -677,8 +679,47 @@ def make_arrivals_golden():
     print("arrivals:", len(specs), "workloads")
 
 
+# ------------------------------------------------------------------------------
+# metrics (collect_metrics + RunReport.summary over oracle-mode event logs)
+# ------------------------------------------------------------------------------
+
+
+def summary_doc(s: dict) -> dict:
+    """The summary's numbers, floats as exact hex strings."""
+    out = {k: s[k] for k in ("num_requests", "virtual_elapsed_ns", "output_tokens")}
+    out["tokens_per_virtual_s"] = float(s.get("tokens_per_virtual_s", 0.0)).hex()
+    for m in ("ttft_ns", "e2e_ns", "tpot_ns"):
+        if m in s:
+            out[m] = {k: (float(v).hex() if k != "count" else v) for k, v in s[m].items()}
+    return out
+
+
+def make_metrics_golden():
+    from timewarp.metrics import collect_metrics
+
+    recs = []
+    rng = random.Random(397)
+    for name, arr, cfg, ps, epoch in oracle_case_list() + full_size_cases():
+        events, status, idx = run_ref_case(arr, cfg, ps, epoch)
+        if events is None:
+            continue
+        rep = collect_metrics(arr, events, epoch_ns=epoch, mode="oracle", workload_fingerprint="golden",
+                              wall_elapsed_ns=0)
+        recs.append({"name": name, "perm": None, "summary": summary_doc(rep.summary())})
+        if len(arr) > 1 and (name.startswith("random_") or name in ("config1_8b_tp1", "deterministic40")):
+            perm = list(range(len(arr)))
+            rng.shuffle(perm)
+            shuffled = [arr[i] for i in perm]
+            rep = collect_metrics(shuffled, events, epoch_ns=epoch, mode="oracle", workload_fingerprint="golden",
+                                  wall_elapsed_ns=0)
+            recs.append({"name": name, "perm": perm, "summary": summary_doc(rep.summary())})
+    with open(os.path.join(HERE, "metrics.json"), "w") as fh:
+        json.dump(recs, fh)
+    print("metrics:", len(recs), "summaries")
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals"}
+    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics"}
     rng = np.random.default_rng(20260100397)
     if "predictor" in which:
         make_predictor_golden(rng)
@@ -690,3 +731,5 @@ if __name__ == "__main__":
         make_oracle_golden()
     if "tkgrid" in which:
         make_tkgrid_golden()
+    if "metrics" in which:
+        make_metrics_golden()

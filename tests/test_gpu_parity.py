@@ -336,6 +336,62 @@ def test_sweep_1024_equals_oracle_on_every_config():
     assert int(out.results["events"].sum()) == events_expected
 
 
+# ---------------------------------------------------------------------------------
+# metrics: on-device RunReport.summary()
+# ---------------------------------------------------------------------------------
+
+
+def test_device_metrics_match_reference_summaries():
+    """tw_metrics_many == collect_metrics(...).summary() bit for bit on every golden
+    case (small, full size incl. the 10k-request config 3, shuffled arrival lists)."""
+    from _fixtures import assert_summary_equal, caller_order, metrics_golden
+    from paper_2601_00397_b200._lib import SIM_CFG_DTYPE, TW_METRICS_SIM_FAILED
+    from paper_2601_00397_b200.predictor import PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep, summary_doc
+    from paper_2601_00397_b200.workload import pack_arrivals
+
+    recs = metrics_golden()
+    stall = [c for c in oracle_golden()[0] if c["name"] == "stall"]
+    preds, lists = [], []
+    cfgs = np.zeros(len(recs) + len(stall), SIM_CFG_DTYPE)
+    for i, (rec, case) in enumerate([(r, c) for r, c in recs] + [(None, c) for c in stall]):
+        pset, _, c = case_inputs(case)
+        preds.append(pset.predictors[0])
+        lists.append(caller_order(case, rec["perm"] if rec else None))
+        cfgs[i] = c[0]
+        cfgs[i]["pred_id"] = i
+        cfgs[i]["workload_id"] = i
+    sw = DeviceSweep(PredictorSet(preds), pack_arrivals(lists), cfgs, per_request=True)
+    sw.run()
+    sw.run_metrics()
+    got = sw.fetch_metrics()
+    for i, (rec, case) in enumerate(recs):
+        assert_summary_equal(got[i], rec["summary"], (rec["name"], rec["perm"] is not None))
+        doc = summary_doc(got[i])
+        assert doc["num_requests"] == rec["summary"]["num_requests"]
+    assert int(got[len(recs)]["status"]) == TW_METRICS_SIM_FAILED  # stalled config: no summary
+
+
+def test_device_metrics_equal_oracle_on_sweep_1024():
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    sw = presets.sweep_1024()
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+    dev.run()
+    dev.run_metrics()
+    got = dev.fetch_metrics()
+    out = dev.fetch()
+    for c in range(0, len(sw), 1):
+        w = int(sw.cfgs[c]["workload_id"])
+        lo, hi = int(sw.workloads.wl_off[w]), int(sw.workloads.wl_off[w + 1])
+        rb = int(out.req_base[c])
+        want = orc.metrics(sw.workloads.offset_ns[lo:hi], sw.workloads.output[lo:hi],
+                           out.first_ns[rb : rb + hi - lo], out.finish_ns[rb : rb + hi - lo], int(sw.cfgs[c]["epoch_ns"]))
+        assert got[c].tobytes() == want.tobytes(), c
+
+
 def test_drop_in_simulate_matches_reference_timeline():
     """pkg/tests/test_oracle.py:35-43 through sweep.simulate (full event dicts)."""
     from paper_2601_00397_b200.predictor import ConstantPredictor

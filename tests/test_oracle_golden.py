@@ -27,7 +27,7 @@ from _fixtures import (
 )
 from oracle import oracle as orc
 from paper_2601_00397_b200.predictor import PredictorSet
-from paper_2601_00397_b200.workload import WorkloadSpec, poisson_arrays
+from paper_2601_00397_b200.workload import WorkloadSpec, pack_arrivals, poisson_arrays
 
 STATUS_OF = {0: 0, 1: 1, 2: 2, 3: 3}
 
@@ -150,3 +150,43 @@ def test_sim_many_threads_equal_single():
     res, *_ = orc.sim_many(blob, cfgs, wl.wl_off, wl.offset_ns, wl.prompt, wl.output, n_threads=4)
     for i, s in enumerate(singles):
         assert res[i].tobytes() == s.tobytes()
+
+
+def _oracle_metrics_case(rec, case):
+    from _fixtures import caller_order
+
+    pset, wl, cfgs = case_inputs(case)
+    ts, pr, out = wl.workload(0)
+    res, first, finish, _ = orc.simulate_one(pset.blob, cfgs[0], ts, pr, out, want_events=False)
+    arr = caller_order(case, rec["perm"])
+    cw = pack_arrivals([arr])  # the engine's sorted order + each request's caller position
+    pos = cw.caller_index
+    n = len(arr)
+    # arrays in the caller's order: engine request e sits at caller position pos[e]
+    c_ts, c_out, c_first, c_fin = (np.empty(n, np.int64), np.empty(n, np.int32), np.empty(n, np.int64),
+                                   np.empty(n, np.int64))
+    c_ts[pos], c_out[pos], c_first[pos], c_fin[pos] = cw.offset_ns, cw.output, first, finish
+    return orc.metrics(c_ts, c_out, c_first, c_fin, case["epoch"])
+
+
+def test_oracle_metrics_match_reference_summaries():
+    """orc_metrics == collect_metrics(...).summary() bit for bit (metrics.py:38-253),
+    including shuffled arrival lists (ordered TPOT sum); full-size cases: config 1 only."""
+    from _fixtures import assert_summary_equal, metrics_golden
+
+    done = 0
+    for rec, case in metrics_golden():
+        if case["arrivals"] is None and case["name"] != "config1_8b_tp1":
+            continue
+        assert_summary_equal(_oracle_metrics_case(rec, case), rec["summary"], rec["name"])
+        done += 1
+    assert done >= 100
+
+
+@pytest.mark.slow
+def test_oracle_metrics_full_size_cases():
+    from _fixtures import assert_summary_equal, metrics_golden
+
+    for rec, case in metrics_golden():
+        if case["arrivals"] is None:
+            assert_summary_equal(_oracle_metrics_case(rec, case), rec["summary"], rec["name"])
