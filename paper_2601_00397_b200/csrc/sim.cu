@@ -315,7 +315,24 @@ TWB_TK_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int
 // whose duration ignores C); a lookup is one compare + ballot + shuffle. Linear models
 // with a context term keep a single exact (P, D, C) entry.
 TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
+#ifdef TWB_SIM_WARP_PRED
   return predict_warp(ps, id, P, D, C);
+#else
+  // every lane runs the same scalar lookup (bit-length LUT bracketing, exact int
+  // lerps with blob reciprocals); only the rare nearest-row fallback uses the lanes
+  if (id < 0 || id >= pset_ndesc(ps)) return TW_PRED_BAD_DESC;
+  const tw_pred_desc* d = pset_desc(ps, id);
+  if (d->kind != TW_PRED_TABLE) return predict_scalar(ps, id, P, D, C);
+  const TableView t = table_view(ps, d);
+  int p0, p1, d0, d1;
+  int64_t P0, P1, D0, D1;
+  if (bracket_lut(t.pax, t.lutp, t.np, P, p0, p1, P0, P1) && bracket_lut(t.dax, t.lutd, t.nd, D, d0, d1, D0, D1)) {
+    const int64_t r = table_corners2(t, p0, p1, d0, d1, P0, P1, D0, D1, P, D);
+    if (r != TW_PRED_TABLE_MISS) return r;
+  }
+  if (d->allow_extrapolation) return table_nearest_warp(t, P, D);
+  return TW_PRED_TABLE_MISS;
+#endif
 }
 
 struct PredCache {
