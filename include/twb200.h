@@ -334,6 +334,102 @@ int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off
                     const int32_t* sum_order, int32_t max_requests, tw_run_metrics* out,
                     void* stream);
 
+/* ---- native BarrierCore for the live Timekeeper --------- */
+/* Host C++ (no GPU): the reference's single-threaded protocol state machine
+ * (timekeeper.py:68-398) behind an opaque handle. Replaces `BarrierCore(...)` in
+ * TimekeeperServer (timekeeper.py:435-440) through the Python shim
+ * NativeBarrierCore (paper_2601_00397_b200/barrier_core.py). Clients are
+ * registration indices (ids "actor<n>"/"observer<n>" in registration order); group
+ * ids are caller-assigned small integers. Not thread-safe: one state thread owns a
+ * core, as in the reference. */
+typedef struct tw_core tw_core;
+
+#define TW_MSG_REGISTER 0 /* wire.MessageType */
+#define TW_MSG_SEAL 1
+#define TW_MSG_JUMP_REQUEST 2
+#define TW_MSG_COLLECTIVE_ENTER 3
+#define TW_MSG_DEREGISTER 4
+#define TW_MSG_OTHER 5 /* any type clients may not send -> TW_EINVAL (MalformedBody) */
+#define TW_ROLE_ACTOR 0
+#define TW_ROLE_OBSERVER 1
+
+typedef struct tw_core_msg {
+  int32_t type;   /* TW_MSG_* */
+  int32_t client; /* registration index; -1 = absent or never issued */
+  int32_t role;   /* REGISTER: TW_ROLE_*, -1 = unknown role (MalformedBody) */
+  int32_t group;  /* COLLECTIVE_ENTER: group handle, -1 = missing group_id */
+  int64_t target; /* JUMP_REQUEST target ns (valid iff has_target) */
+  int64_t expected;
+  int32_t has_target, has_expected;
+} tw_core_msg; /* 40 B */
+
+typedef struct tw_core_ack {
+  int32_t error;      /* TW_ACK_* (0 = no error) */
+  int32_t client;     /* REGISTER: the new client's index; else the request's */
+  int32_t group;      /* COLLECTIVE_ENTER: the request's group */
+  int32_t resolve;    /* 1: deliver the ack, then call tw_core_try_resolve */
+  int64_t offset_ns;  /* REGISTER_ACK offset */
+  int64_t seq;        /* REGISTER_ACK seq */
+  int64_t generation; /* COLLECTIVE_ENTER generation (ExpectedMismatch: the open size) */
+} tw_core_ack;        /* 40 B */
+
+#define TW_REC_REGISTER 0 /* structured log records (timekeeper.py log_record) */
+#define TW_REC_SEAL 1
+#define TW_REC_REQUEST 2
+#define TW_REC_COLLECTIVE_ENTER 3
+#define TW_REC_COLLECTIVE_RELEASE 4
+#define TW_REC_DEREGISTER 5
+#define TW_REC_RESOLVE 6
+#define TW_REC_BROADCAST 7
+
+typedef struct tw_core_record {
+  int32_t kind; /* TW_REC_* */
+  int32_t client, role, group;
+  int64_t wall_ns, offset_ns, seq, target_ns, expected, generation, t_min_ns;
+  int32_t num_actors, eligible, broadcast, suppressed;
+  int32_t n_items, pad;
+  const int32_t* items;        /* release: members; resolve: pending clients (id order) */
+  const int64_t* item_targets; /* resolve: their targets */
+} tw_core_record;
+
+#define TW_EMIT_CLOCK_UPDATE 0
+#define TW_EMIT_COLLECTIVE_RELEASE 1
+typedef struct tw_core_emit {
+  int32_t kind, group;
+  int64_t offset_ns, seq, generation;
+} tw_core_emit;
+
+typedef struct tw_core_state_t {
+  int64_t offset_ns, seq, last_broadcast_wall_ns, barrier_open_since_ns;
+  int32_t sealed, has_last_broadcast, has_barrier_open, n_clients;
+  int32_t n_groups, eligible, n_pending, n_active_actors;
+} tw_core_state_t;
+
+typedef int64_t (*tw_core_clock_fn)(void* user);             /* wall ns */
+typedef void (*tw_core_sleep_fn)(void* user, double seconds); /* sleep(wait_ns / 1e9) */
+typedef void (*tw_core_emit_fn)(void* user, const tw_core_emit* ev);
+typedef void (*tw_core_log_fn)(void* user, const tw_core_record* rec);
+
+/* emit / log_record may be NULL; clock / sleep may be NULL for the host realtime clock
+ * (CLOCK_REALTIME ns, the reference's wall_now) and nanosleep. Returns TW_EINVAL for a
+ * negative cooldown. */
+int tw_core_new(int64_t cooldown_ns, int32_t suppress_broadcasts, tw_core_clock_fn clock,
+                tw_core_sleep_fn sleep, tw_core_emit_fn emit, tw_core_log_fn log_record,
+                void* user, tw_core** out);
+int tw_core_free(tw_core* core);
+/* One inbound message: validates and mutates state, fills the ack (protocol errors
+ * are ack.error, not call failures); TW_EINVAL = MalformedBody. */
+int tw_core_handle(tw_core* core, const tw_core_msg* msg, tw_core_ack* ack);
+int tw_core_try_resolve(tw_core* core);
+int tw_core_state(const tw_core* core, tw_core_state_t* st);
+/* flags: 1 active, 2 exempt, 4 has a pending target (pending_target) */
+int tw_core_client(const tw_core* core, int32_t idx, int32_t* role, int32_t* flags,
+                   int64_t* pending_target);
+/* flags: 1 exists, 2 expected set, 4 open; members sorted by client id (<= cap). */
+int tw_core_group(const tw_core* core, int32_t group, int64_t* generation, int64_t* expected,
+                  int64_t* open_since_ns, int32_t* flags, int32_t* members, int32_t cap,
+                  int32_t* n_members);
+
 /* ---- misc ------------------------------------------------------------------ */
 int tw_abi_version(void);
 const char* tw_last_error(void);

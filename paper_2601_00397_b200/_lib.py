@@ -157,6 +157,13 @@ EXPORTED_SYMBOLS = (
     "tw_sim_last_launch",
     "tw_sim_set_profile",
     "tw_metrics_many",
+    "tw_core_new",
+    "tw_core_free",
+    "tw_core_handle",
+    "tw_core_try_resolve",
+    "tw_core_state",
+    "tw_core_client",
+    "tw_core_group",
     "tw_abi_version",
     "tw_last_error",
     "tw_launch_count",

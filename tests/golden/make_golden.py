@@ -21,6 +21,9 @@ Fixtures:
   arrivals.npz   generate_arrivals outputs for the sweep workloads
   metrics.json   collect_metrics(...).summary() of the oracle cases (floats as hex),
                  including arrival lists in shuffled order (the TPOT sum is ordered)
+  core_log.json.gz full BarrierCore transcripts (every message and ack with all fields,
+                 every structured log record, every emitted broadcast/release) of the
+                 scripted scenarios and 190 random schedules: pins NativeBarrierCore
 """
 
 from __future__ import annotations
@@ -680,6 +683,115 @@ def make_arrivals_golden():
 
 
 # ------------------------------------------------------------------------------
+# full BarrierCore transcripts (native core pin)
+# ------------------------------------------------------------------------------
+
+_MSG_FIELDS = ("client_id", "role", "offset", "target", "seq", "group_id", "expected", "generation", "error")
+
+
+def msg_doc(m) -> dict:
+    d = {"type": m.type.value}
+    for f in _MSG_FIELDS:
+        v = getattr(m, f)
+        if v is not None:
+            d[f] = v
+    return d
+
+
+def make_core_golden():
+    transcripts = []
+
+    def wrap(h, cooldown, suppress):
+        tr = {"cooldown": cooldown, "suppress": suppress, "steps": []}
+        orig = h.core.handle
+
+        def handle(msg, reply=None):
+            ack = orig(msg, reply)
+            tr["steps"].append({"msg": msg_doc(msg), "ack": msg_doc(ack)})
+            return ack
+
+        h.core.handle = handle
+        orig_adv = h.clock.advance
+
+        def advance(ns):
+            orig_adv(ns)
+            tr["steps"].append({"advance": int(ns)})
+
+        h.clock.advance = advance
+        transcripts.append((h, tr))
+
+    orig_build = _support.CoreHarness.build
+
+    def build(cooldown_ns=500_000, suppress=False):
+        h = orig_build(cooldown_ns=cooldown_ns, suppress=suppress)
+        wrap(h, cooldown_ns, suppress)
+        return h
+
+    _support.CoreHarness.build = staticmethod(build)
+    try:
+        for seed in range(150):
+            _support.run_random_schedule(seed)
+        for seed in range(1000, 1040):
+            _support.run_random_schedule(seed, cooldown_ns=[0, 1, 123_456_789, 2_000_000][seed % 4])
+        scripted()
+        scenario_streams()
+    finally:
+        _support.CoreHarness.build = orig_build
+    # malformed / error paths the schedules never take
+    h = _support.CoreHarness.build(cooldown_ns=500_000)
+    wrap(h, 500_000, False)
+    core = h.core
+
+    def malformed(bad):
+        try:
+            core.handle(bad)  # recorded by the wrapper when it returns an ack
+        except Exception as exc:  # noqa: BLE001
+            transcripts[-1][1]["steps"].append({"msg": msg_doc(bad), "raises": type(exc).__name__, "text": str(exc)})
+
+    malformed(Message(type=MessageType.REGISTER, role="ROBOT"))
+    for m in (Message(type=MessageType.JUMP_REQUEST, client_id="actor9", target=5),
+              Message(type=MessageType.SEAL),
+              Message(type=MessageType.DEREGISTER, client_id="nobody"),
+              Message(type=MessageType.REGISTER, role="OBSERVER"),
+              Message(type=MessageType.REGISTER, role="ACTOR"),
+              Message(type=MessageType.REGISTER, role="ACTOR"),
+              Message(type=MessageType.JUMP_REQUEST, client_id="observer1", target=5),
+              Message(type=MessageType.JUMP_REQUEST, client_id="actor2", target=0),
+              Message(type=MessageType.JUMP_REQUEST, client_id="actor2"),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="observer1", group_id="g", expected=2),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor2", group_id="g", expected=0),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor2", group_id="g"),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor2", group_id="g", expected=2),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor3", group_id="g", expected=3),
+              Message(type=MessageType.SEAL),
+              Message(type=MessageType.SEAL),
+              Message(type=MessageType.REGISTER, role="ACTOR"),
+              Message(type=MessageType.JUMP_REQUEST, client_id="actor3", target=1_500_000_000),
+              Message(type=MessageType.DEREGISTER, client_id="actor2"),
+              Message(type=MessageType.DEREGISTER, client_id="actor2"),
+              Message(type=MessageType.JUMP_REQUEST, client_id="actor2", target=5),
+              Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor3", group_id="g", expected=1),
+              Message(type=MessageType.DEREGISTER, client_id="observer1"),
+              Message(type=MessageType.JUMP_REQUEST, client_id="actor3", target=2_000_000_000)):
+        core.handle(m)
+    for bad in (Message(type=MessageType.REGISTER, role="ROBOT"),  # sealed: RegistrationSealed ack
+                Message(type=MessageType.CLOCK_UPDATE),
+                Message(type=MessageType.COLLECTIVE_ENTER, client_id="actor3", expected=1)):
+        malformed(bad)
+    out = []
+    for h, tr in transcripts:
+        tr["records"] = h.records
+        tr["emitted"] = [msg_doc(m) for m in h.broadcasts]
+        tr["final"] = [h.core.offset_ns, h.core.seq, h.clock.now_ns]
+        out.append(tr)
+    import gzip
+
+    with gzip.open(os.path.join(HERE, "core_log.json.gz"), "wt") as fh:
+        json.dump(out, fh, separators=(",", ":"))
+    print("core_log:", len(out), "transcripts,", sum(len(t["steps"]) for t in out), "messages")
+
+
+# ------------------------------------------------------------------------------
 # metrics (collect_metrics + RunReport.summary over oracle-mode event logs)
 # ------------------------------------------------------------------------------
 
@@ -719,7 +831,7 @@ def make_metrics_golden():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics"}
+    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics", "core"}
     rng = np.random.default_rng(20260100397)
     if "predictor" in which:
         make_predictor_golden(rng)
@@ -733,3 +845,5 @@ if __name__ == "__main__":
         make_tkgrid_golden()
     if "metrics" in which:
         make_metrics_golden()
+    if "core" in which:
+        make_core_golden()
