@@ -1,12 +1,14 @@
-# full evidence capture for profiles/: tests, smoke, bench (N=1, CPU baseline), launch list, ncu of both kernels
+# full evidence capture for profiles/: tests, smoke, bench (N=1 config 4, CPU baseline), reference arm,
+# config-5 sweep on one GPU, launch list, ncu --set full of the three kernels, per-config k_sim profile
 mkdir -p gpurun_out
 nproc > gpurun_out/box.txt; nvidia-smi -L >> gpurun_out/box.txt
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+timeout 1200 python bench.py --sweep 65536 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_65536.log 2>&1; echo "rc=$?" >> gpurun_out/bench_65536.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -o gpurun_out/prof_sim python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_sim.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_features -s 2 -c 1 -o gpurun_out/prof_pred python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_pred.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_metrics -s 1 -c 1 -o gpurun_out/prof_metrics python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_metrics.log 2>&1
 timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim.log 2>&1
-TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_phases.so timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim_phases.log 2>&1
