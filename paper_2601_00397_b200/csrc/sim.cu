@@ -119,10 +119,26 @@ __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
 // measured 10-18% slower than keeping them inline — see profiles/README.md.)
 __device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) { return a / b; }
 
+// Cold paths kept out of line: the loop's SASS is larger than the instruction caches
+// and the kernel is fetch-sensitive (adding inline code to the hot loop measured
+// slower even when it removed work), so rarely taken code should not sit inside it.
+#ifdef TWB_SIM_INLINE_COLD
+#define TWB_COLD __device__ __forceinline__
+#else
+#define TWB_COLD __device__ __noinline__
+#endif
+TWB_COLD int64_t cold_div(int64_t a, int64_t b) { return a / b; }
+TWB_COLD int64_t cold_fake_sleep(int64_t wait_ns) { return fake_sleep_ns(wait_ns); }
+#ifdef TWB_SIM_COLD_DIV_ALL
+#define HOT_DIV cold_div
+#else
+#define HOT_DIV div_nn
+#endif
+
 // floor(a / b) for 0 <= a < 2^52 and b > 0 given rb ~= 1/b (any fp64 approximation):
 // the fp64 estimate is within 2 of the quotient, fixed up with exact int64 checks.
 __device__ __forceinline__ int64_t div_rcp(int64_t a, int64_t b, double rb) {
-  if (a >= (1LL << 52)) return a / b;
+  if (a >= (1LL << 52)) return cold_div(a, b);
   int64_t q = (int64_t)__dmul_rz(__ll2double_rn(a), rb);
   int64_t r = a - q * b;
   while (r < 0) { q--; r += b; }
@@ -192,7 +208,7 @@ __device__ __forceinline__ void tk_resolve(TkGrid& g, int64_t t_min) {
   // timekeeper.py:326-366 with FakeClock sleep (pkg/tests/_support.py:33-34)
   if (g.wall < t_min && g.last_bcast != INT64_MIN && g.cooldown > 0) {
     const int64_t wait = g.last_bcast + g.cooldown - g.wall;
-    if (wait > 0) g.wall += (wait == g.cooldown) ? g.conv_cooldown : fake_sleep_ns(wait);
+    if (wait > 0) g.wall += (wait == g.cooldown) ? g.conv_cooldown : cold_fake_sleep(wait);
   }
   if (g.wall < t_min) {
     const int64_t cand = t_min - g.wall;
@@ -221,7 +237,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
   int64_t per = d;
   if (S == 2) per = d >> 1;
-  else if (S > 2) per = div_nn(d, S);
+  else if (S > 2) per = cold_div(d, S);
   const int64_t end_all = now0 + K * d;
   const int64_t cj = g.conv_cooldown;  // 0 when the cooldown is 0
   const int64_t gap = (S > 1) ? min(per, d - per * (S - 1)) : d;
@@ -259,8 +275,8 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
         int64_t m_x = K * S;  // last deadline we may cover: end_all, or below the target
         if (g.disp_ts <= end_all) {
           const int64_t x = g.disp_ts - 1 - now0;
-          const int64_t fx = div_nn(x, d);
-          const int64_t px = (S > 1) ? min((int64_t)(S - 1), div_nn(x - fx * d, per)) : 0;
+          const int64_t fx = HOT_DIV(x, d);
+          const int64_t px = (S > 1) ? min((int64_t)(S - 1), HOT_DIV(x - fx * d, per)) : 0;
           m_x = fx * S + px;
         }
         const int64_t R = m_x - m_on;
@@ -280,7 +296,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
     // one round, resolved at min(dispatcher's next arrival, first deadline beyond V)
     if (tgt <= g.V) {
       if (d > 0 && g.V - base >= 4 * d) {  // V far ahead: skip whole steps at once
-        const int64_t jump = div_nn(g.V - base, d);
+        const int64_t jump = cold_div(g.V - base, d);
         base += jump * d;
         m_walk += jump * S - s;
         s = 0;
@@ -314,6 +330,11 @@ TWB_TK_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int
 // Prediction cache: 32 entries held one per lane (key = P << 32 | D, for predictors
 // whose duration ignores C); a lookup is one compare + ballot + shuffle. Linear models
 // with a context term keep a single exact (P, D, C) entry.
+TWB_COLD int64_t cold_predict_scalar(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
+  return predict_scalar(ps, id, P, D, C);
+}
+TWB_COLD int64_t cold_nearest_warp(const TableView& t, int64_t P, int64_t D) { return table_nearest_warp(t, P, D); }
+
 TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
 #ifdef TWB_SIM_WARP_PRED
   return predict_warp(ps, id, P, D, C);
@@ -322,7 +343,7 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, i
   // lerps with blob reciprocals); only the rare nearest-row fallback uses the lanes
   if (id < 0 || id >= pset_ndesc(ps)) return TW_PRED_BAD_DESC;
   const tw_pred_desc* d = pset_desc(ps, id);
-  if (d->kind != TW_PRED_TABLE) return predict_scalar(ps, id, P, D, C);
+  if (d->kind != TW_PRED_TABLE) return cold_predict_scalar(ps, id, P, D, C);
   const TableView t = table_view(ps, d);
   int p0, p1, d0, d1;
   int64_t P0, P1, D0, D1;
@@ -330,9 +351,18 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, i
     const int64_t r = table_corners2(t, p0, p1, d0, d1, P0, P1, D0, D1, P, D);
     if (r != TW_PRED_TABLE_MISS) return r;
   }
-  if (d->allow_extrapolation) return table_nearest_warp(t, P, D);
+  if (d->allow_extrapolation) return cold_nearest_warp(t, P, D);
   return TW_PRED_TABLE_MISS;
 #endif
+}
+
+#ifndef TWB_SIM_OUTLINE_COLD2
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+int64_t cold_predict_warp(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
+  return predict_warp(ps, id, P, D, C);
 }
 
 struct PredCache {
@@ -345,9 +375,9 @@ struct PredCache {
 __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, int id, int64_t P, int64_t D,
                                                   int64_t C) {
   const int lane = threadIdx.x & 31;
-  if (pc.uses_c) {
+  if (pc.uses_c) {  // Linear models with a context term: one exact (P, D, C) entry
     if (P == pc.P && D == pc.D && C == pc.C) return pc.d;
-    const int64_t d = predict_miss(ps, id, P, D, C);
+    const int64_t d = cold_predict_warp(ps, id, P, D, C);
     pc.P = P;
     pc.D = D;
     pc.C = C;
@@ -366,6 +396,21 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   return d;
 }
 
+// full event dump (audited configs only)
+// (outlining this and the Linear-with-context predictor measured slower: 11.6 -> 12.2 ms)
+#ifndef TWB_SIM_OUTLINE_COLD2
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void cold_dump_event(tw_event* evp, int64_t pos, int32_t rq, int kind, int64_t ts, int64_t step) {
+  tw_event e;
+  e.ts_ns = ts;
+  e.step = (int32_t)step;
+  e.req_kind = (rq << 2) | kind;
+  evp[pos] = e;
+}
+
 struct Emitter {
   uint64_t dig;  // lane-partial digest
   int64_t* first;
@@ -374,13 +419,7 @@ struct Emitter {
   int64_t ev_cap;
   __device__ __forceinline__ void event(int64_t pos, int32_t rq, int kind, int64_t ts, int64_t step) {
     dig += tw_event_hash((uint64_t)pos, (uint64_t)rq, (uint64_t)kind, ts, step);
-    if (evp && pos < ev_cap) {
-      tw_event e;
-      e.ts_ns = ts;
-      e.step = (int32_t)step;
-      e.req_kind = (rq << 2) | kind;
-      evp[pos] = e;
-    }
+    if (evp && pos < ev_cap) cold_dump_event(evp, pos, rq, kind, ts, step);
   }
 };
 
@@ -458,7 +497,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   g.last_bcast = INT64_MIN;
   g.V = epoch;
   g.cooldown = cfg.tk_cooldown_ns;
-  g.conv_cooldown = g.cooldown > 0 ? fake_sleep_ns(g.cooldown) : 0;
+  g.conv_cooldown = g.cooldown > 0 ? cold_fake_sleep(g.cooldown) : 0;
   g.rcp_cooldown = g.conv_cooldown > 0 ? __drcp_rn(__ll2double_rn(g.conv_cooldown)) : 0.0;
   g.disp = 0;
   g.win.load(ts, n, epoch, 0);
@@ -715,9 +754,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           const unsigned fm = __ballot_sync(kFull, fin);
           if (is_dec) {
             const int64_t my = pos + __popc(dm & lt) + __popc(fm & lt);
-            em.event(my, rq, TW_EV_OUTPUT_TOKEN, nowK, stepK);
+            // one hash call site for OUTPUT_TOKEN (+ FINISHED): less code in the loop
+#pragma unroll 1
+            for (int t = 0; t <= (int)fin; t++) em.event(my + t, rq, t ? TW_EV_FINISHED : TW_EV_OUTPUT_TOKEN, nowK, stepK);
             if (fin) {
-              em.event(my + 1, rq, TW_EV_FINISHED, nowK, stepK);
               if (em.finish) em.finish[rq] = nowK;
             }
           }
@@ -805,12 +845,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       if (nev) {
         const int64_t ps0 = is_chunk ? pos_c + __popc(c1 & lt) + __popc(c2 & lt)
                                      : pos_d + __popc(d1 & lt) + __popc(d2 & lt);
-        em.event(ps0, rq, k0, now, step);
+#pragma unroll 1
+        for (int t = 0; t < nev; t++) em.event(ps0 + t, rq, t ? TW_EV_FINISHED : k0, now, step);
         if (k0 == TW_EV_FIRST_TOKEN && em.first) em.first[rq] = now;
-        if (nev == 2) {
-          em.event(ps0 + 1, rq, TW_EV_FINISHED, now, step);
-          if (em.finish) em.finish[rq] = now;
-        }
+        if (nev == 2 && em.finish) em.finish[rq] = now;
       }
       pos_c += __popc(c1) + __popc(c2);
       pos_d += __popc(d1) + __popc(d2);
