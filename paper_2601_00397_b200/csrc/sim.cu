@@ -699,115 +699,57 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     // included), a chunk reaches its prompt's last chunk (excluded), or a new arrival
     // becomes visible to an empty queue; a blocked queue head stays blocked (slots and
     // budget constant, KV free non-increasing). P and D are constant, so is d.
+    // One code path for both: a normal step is the K = 1 case (the loop is fetch-bound,
+    // so a single Timekeeper walk and a single apply block beat specialised copies).
+    int64_t K = 1;
     if (macro_ok) {
-      int64_t K = __reduce_min_sync(kFull, min_rem);
+      K = __reduce_min_sync(kFull, min_rem);
       // an emptied queue can admit the next arrival; a non-empty one stays blocked
       if (w_head + n_adm == fut && fut < n && d > 0 && next_arr - now <= (K - 1) * d) {
         // the plan after step j sees arrivals <= now + j*d: stop at the first crossing
         const int64_t ka = div_rcp(next_arr - now + d - 1, d, __drcp_rn(__ll2double_rn(d)));
         if (ka < K) K = ka;
       }
-      if (K >= 2) {
-        const int D = n_dec;  // events per step: one OUTPUT_TOKEN per decode slot
-        const int64_t now0 = now;
-        const int32_t step0 = step;
-        long long c0 = TWB_CLK();
-        if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);
-        long long c1 = TWB_CLK();
-        tk_cyc += c1 - c0;
-        // events of steps 1..K-1, flattened over the lanes: e -> (step j, decode rank i)
-        const int64_t body = (K - 1) * (int64_t)D;
-        if (body > 0) {
-          const int q32 = 32 / D, r32 = 32 % D;
-          int64_t j = lane / D;
-          int i = lane - (int)j * D;
-          for (int64_t e = lane; e < body; e += 32) {
-            em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
-            i += r32;
-            j += q32;
-            if (i >= D) { i -= D; j++; }
-          }
-        }
-        // step K: decoders emit (and may finish), chunks advance K takes; compact
-        const int64_t nowK = now0 + K * d;
-        const int32_t stepK = step0 + (int32_t)K;
-        int64_t pos = n_events + body;
-        int kept = 0;
-        const int n_tot = n_act + n_adm;  // admitted this step: chunk slots at the end
-        for (int b = 0; b < n_tot; b += 32) {
-          const int i = b + lane;
-          const bool v = i < n_tot;
-          int32_t rq = 0, pr = 0, op = 0, dn = 0, e = 0, plan = -2;
-          if (v) {
-            rq = sl.req[i];
-            pr = sl.prompt[i];
-            op = sl.output[i];
-            dn = sl.done[i];
-            e = sl.emit[i];
-            plan = sl.plan[i];
-          }
-          const bool is_dec = plan == -1;
-          if (is_dec) e += (int32_t)K;
-          if (plan >= 0) dn += plan * (int32_t)K;
-          const bool fin = is_dec && e >= op;
-          const unsigned dm = __ballot_sync(kFull, is_dec);
-          const unsigned fm = __ballot_sync(kFull, fin);
-          if (is_dec) {
-            const int64_t my = pos + __popc(dm & lt) + __popc(fm & lt);
-            // one hash call site for OUTPUT_TOKEN (+ FINISHED): less code in the loop
-#pragma unroll 1
-            for (int t = 0; t <= (int)fin; t++) em.event(my + t, rq, t ? TW_EV_FINISHED : TW_EV_OUTPUT_TOKEN, nowK, stepK);
-            if (fin) {
-              if (em.finish) em.finish[rq] = nowK;
-            }
-          }
-          pos += __popc(dm) + __popc(fm);
-          const bool keep = v && !fin;
-          const unsigned km = __ballot_sync(kFull, keep);
-          __syncwarp();
-          if (keep) {
-            const int np = kept + __popc(km & lt);
-            sl.req[np] = rq;
-            sl.prompt[np] = pr;
-            sl.output[np] = op;
-            sl.done[np] = dn;
-            sl.emit[np] = e;
-          }
-          kept += __popc(km);
-          __syncwarp();
-        }
-        n_events = pos;
-        n_act = kept;
-        if (n_adm) {
-          w_head += n_adm;
-          qbase = w_head;
-          q_pr = (qbase + lane < n) ? __ldg(prm + qbase + lane) : 0;
-          q_op = (qbase + lane < n) ? __ldg(outp + qbase + lane) : 0;
-        }
-        now = nowK;
-        step = stepK;
-        ev_cyc += TWB_CLK() - c1;
-        n_runs++;
-        n_run_steps += K;
-        continue;
-      }
+      if (K < 1) K = 1;
     }
-
-    step += 1;
-    n_normal++;
-    const int64_t base = now;
-    now += d;
+    const int64_t now0 = now;
+    const int32_t step0 = step;
     {
       const long long c0 = TWB_CLK();
-      if (tk_on) tk_run(g, ts, n, epoch, S, base, d, 1);  // WorkerGrid stage deadlines
+      if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);  // WorkerGrid stage deadlines
       tk_cyc += TWB_CLK() - c0;
     }
-
-    // ---- apply (oracle.py:88-112): chunks' events first, then decodes', in slot order
     const long long q4 = TWB_CLK();
+    // events of steps 1..K-1 (decodes only), flattened over the lanes: e -> (step j, rank i)
+    const int64_t body = (K - 1) * (int64_t)n_dec;
+    if (body > 0) {
+      const int D = n_dec;
+      const int q32 = 32 / D, r32 = 32 % D;
+      int64_t j = lane / D;
+      int i = lane - (int)j * D;
+#pragma unroll 1  // one copy of the event hash in the loop
+      for (int64_t e = lane; e < body; e += 32) {
+        em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
+        i += r32;
+        j += q32;
+        if (i >= D) { i -= D; j++; }
+      }
+    }
+    if (K >= 2) {
+      n_runs++;
+      n_run_steps += K;
+    } else {
+      n_normal++;
+    }
+    now = now0 + K * d;
+    step = step0 + (int32_t)K;
+
+    // ---- apply step K (oracle.py:88-112): chunks' events first, then decodes', in slot
+    // order. Chunks advance K takes; in a run (K >= 2) none completes (run horizon), so
+    // chunk events only occur when K == 1.
     const int n_tot = n_act + n_adm;
     const int chunk_ev_total = __reduce_add_sync(kFull, (unsigned)chunk_ev);
-    int64_t pos_c = n_events, pos_d = n_events + chunk_ev_total;
+    int64_t pos_c = n_events + body, pos_d = pos_c + chunk_ev_total;
     int kept = 0;
     for (int b = 0; b < n_tot; b += 32) {
       const int i = b + lane;
@@ -825,7 +767,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       bool fin = false;
       const bool is_chunk = plan >= 0, is_dec = plan == -1;
       if (is_chunk) {
-        dn += plan;
+        dn += plan * (int32_t)K;
         if (dn >= pr) {
           e = 1;
           nev = 1;
@@ -833,7 +775,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           if (e >= op) { nev = 2; fin = true; }
         }
       } else if (is_dec) {
-        e += 1;
+        e += (int32_t)K;
         nev = 1;
         k0 = TW_EV_OUTPUT_TOKEN;
         if (e >= op) { nev = 2; fin = true; }
