@@ -356,7 +356,7 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, i
 #endif
 }
 
-#ifndef TWB_SIM_OUTLINE_COLD2
+#ifndef TWB_SIM_OUTLINE_CTXPRED
 __device__ __forceinline__
 #else
 __device__ __noinline__
