@@ -210,6 +210,57 @@ def predictor_roofline(device, peak_gbs):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
 
 
+def extraction_roofline(device, peak_gbs, nb: int = 1 << 25):
+    """Fused batch-feature extraction + prediction (tw_predict_batches) over 2^25 CSR
+    batches of 1-8 slots (70% decode slots): algorithmic bytes = 8 (offset) + 4 (desc
+    id) + 8 (ns out) per batch + 8 (token, context) per slot; inputs far exceed L2."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib, presets
+    from paper_2601_00397_b200._device import stream_handle
+
+    pset = presets.calibration_set()
+    g = torch.Generator(device=device).manual_seed(1)
+    counts = torch.randint(1, 9, (nb,), device=device, generator=g)
+    off = torch.zeros(nb + 1, dtype=torch.int64, device=device)
+    off[1:] = torch.cumsum(counts, 0)
+    ns = int(off[-1].item())
+    ns_pad = (ns + 3) // 4 * 4
+    tok = torch.randint(1, 700, (ns_pad,), dtype=torch.int32, device=device, generator=g)
+    tok[torch.rand(ns_pad, device=device, generator=g) < 0.7] = -1
+    ctx = torch.randint(0, 3000, (ns_pad,), dtype=torch.int32, device=device, generator=g)
+    ids = torch.randint(0, 16, (nb,), dtype=torch.int32, device=device, generator=g)
+    out = torch.empty(nb, dtype=torch.int64, device=device)
+    blob = pset.device_blob(device)
+    lib = _lib.load()
+    s = torch.cuda.current_stream()
+
+    def run():
+        _lib.check(lib.tw_predict_batches(blob.data_ptr(), pset.nbytes, off.data_ptr(), tok.data_ptr(),
+                                          ctx.data_ptr(), ids.data_ptr(), nb, None, out.data_ptr(),
+                                          stream_handle(s)), "extract")
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    durs = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        run()
+        b.record(s)
+        b.synchronize()
+        durs.append(a.elapsed_time(b))
+    ms = statistics.median(durs)
+    alg = nb * (8 + 4 + 8) + ns * 8
+    gbs = alg / (ms / 1e3) / 1e9
+    del off, tok, ctx, ids, out
+    return {"kernel": "k_predict_batches", "bound": "hbm", "achieved": round(gbs, 1), "peak": peak_gbs,
+            "unit": "GB/s", "frac": round(gbs / peak_gbs, 4), "batches_per_launch": nb, "slots_per_launch": ns,
+            "bytes_per_batch": round(alg / nb, 2), "ms_per_launch": round(ms, 4),
+            "batches_per_s": round(nb / (ms / 1e3), 1), "traffic": measured_traffic("k_predict_batches")}
+
+
 def metrics_roofline(dev, args, flush, stream, peak_gbs):
     """tw_metrics_many over the sweep's stamps: every config's
     RunReport.summary() numbers. Algorithmic bytes: first + finish stamps (16 B),
@@ -403,6 +454,10 @@ def main():
             extra["predictor_roofline"] = predictor_roofline(device, peak_gbs)
         except Exception as exc:  # report, never hide
             extra["predictor_roofline"] = {"error": repr(exc)}
+        try:
+            extra["extraction_roofline"] = extraction_roofline(device, peak_gbs)
+        except Exception as exc:
+            extra["extraction_roofline"] = {"error": repr(exc)}
         try:
             extra["metrics_reduction"] = metrics_roofline(dev, args, flush, stream, peak_gbs)
         except Exception as exc:

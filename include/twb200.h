@@ -116,6 +116,8 @@ int tw_predict_features(const void* pset, int64_t pset_bytes, const int32_t* P,
  * Batch b owns slots [batch_off[b], batch_off[b+1]); a slot is a PrefillChunk
  * (slot_tok >= 0: chunk_tokens, slot_ctx: context_len_before) or a DecodeSlot
  * (slot_tok == -1, slot_ctx: context_len) — predictor.py:47-61.
+ * slot_tok / slot_ctx must be 16-byte aligned and readable up to the next multiple
+ * of 4 elements past the last slot (tiles of slots move with TMA bulk copies).
  * feat_out (optional, may be NULL) receives int64 {P, D, C} per batch. */
 int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batch_off,
                        const int32_t* slot_tok, const int32_t* slot_ctx,

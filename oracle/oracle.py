@@ -149,6 +149,22 @@ def sim_many(blob, cfgs, wl_off, ts, prompt, output, n_threads=None, per_request
     return res, req_base, first, finish
 
 
+def extract_features(off, tok, ctx) -> np.ndarray:
+    """BatchComposition totals per CSR batch (predictor.py:69-84): int64 [nb, 3] of
+    P = sum of prefill chunk tokens, D = number of decode slots, C = sum of contexts."""
+    off = np.asarray(off, np.int64)
+    nb = len(off) - 1
+    n = int(off[-1]) if nb >= 0 else 0
+    tok = np.asarray(tok, np.int64)[:n]
+    ctx = np.asarray(ctx, np.int64)[:n]
+    seg = np.repeat(np.arange(nb), np.diff(off))
+    out = np.zeros((nb, 3), np.int64)
+    np.add.at(out[:, 0], seg, np.where(tok >= 0, tok, 0))
+    np.add.at(out[:, 1], seg, (tok < 0).astype(np.int64))
+    np.add.at(out[:, 2], seg, ctx)
+    return out
+
+
 def metrics(offset_ns, output, first, finish, epoch_ns: int) -> np.ndarray:
     """RunReport.summary() numbers of one oracle-mode run (one RUN_METRICS_DTYPE record)."""
     ts = np.ascontiguousarray(offset_ns, np.int64)

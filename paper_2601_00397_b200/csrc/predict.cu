@@ -127,34 +127,199 @@ __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_f
   for (int64_t i = (n4 << 2) + tid; i < n; i += nthreads) out[i] = predict_one(ps, qh, n_desc, P[i], D[i], C[i], id[i]);
 }
 
-// Fused extraction + prediction. One thread per batch; its slots are a contiguous
-// run (CSR), so a warp reads one contiguous region and L1 merges the sectors.
-__global__ void __launch_bounds__(kPredThreads) k_predict_batches(
-    const void* __restrict__ pset, uint32_t pset_bytes, const int64_t* __restrict__ off,
-    const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx, const int32_t* __restrict__ id,
-    int64_t nb, int64_t* __restrict__ feat, int64_t* __restrict__ out) {
-  const char* ps = PsetSmem::stage(pset, pset_bytes);
+// Fused batch-feature extraction + prediction (north-star kernels 1 + 2) over CSR batches.
+//
+// Warp-specialised TMA pipeline, one 1024-thread CTA per SM:
+//  * warp 31 is the producer: for each tile of 992 batches it reads the tile's slot
+//    range from batch_off and moves the contiguous slot_tok / slot_ctx runs into a
+//    shared-memory stage with two cp.async.bulk copies (TMA bulk-copy engine) that
+//    complete on the stage's "full" mbarrier; it reuses a stage once all consumer
+//    warps have arrived on its "empty" mbarrier (kExtStages stages in flight);
+//  * warps 0-30 consume: each thread owns one batch per tile, prefetches its
+//    offsets and descriptor id for the next tile while the current one is reduced,
+//    sums its slots from shared memory (predictor.py:69-84) and predicts through the
+//    bulk-lookup section.
+// So every HBM read of the CSR arrays is a bulk transfer or a coalesced row of
+// offsets, and no CTA-wide barrier sits in the loop. A tile whose slots exceed a
+// stage is flagged and its consumers load slots directly.
+constexpr int kExtThreads = 1024;
+#ifndef TWB_EXT_BPT
+#define TWB_EXT_BPT 1
+#endif
+constexpr int kExtBpt = TWB_EXT_BPT;                        // batches per consumer thread per tile
+constexpr int kExtConsumers = (kExtThreads - 32) * kExtBpt;  // batches per tile
+#ifndef TWB_EXT_STAGES
+#define TWB_EXT_STAGES 4
+#endif
+constexpr int kExtStages = TWB_EXT_STAGES;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+struct ExtTile {
+  int64_t a0;      // first staged slot (tile's first slot rounded down to 4)
+  int32_t staged;  // 1: slots in shared memory, 0: direct loads
+  int32_t pad;
+};
+
+__global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
+    const void* __restrict__ pset, uint32_t pset_bytes, uint32_t pset_smem, int32_t cap,
+    const int64_t* __restrict__ off, const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx,
+    const int32_t* __restrict__ id, int64_t nb, int64_t* __restrict__ feat, int64_t* __restrict__ out) {
+  extern __shared__ __align__(128) char smem[];
+  const char* ps = PsetSmem::stage(pset, pset_bytes);  // ends with a CTA barrier
   const int n_desc = pset_ndesc(ps);
   const uint2* qh = pset_qhdr(ps);
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += nthreads) {
-    const int64_t s0 = off[b], s1 = off[b + 1];
-    int64_t Pt = 0, Dn = 0, Ct = 0;
-    for (int64_t s = s0; s < s1; s++) {
-      const int32_t t = __ldg(tok + s);
-      const int32_t c = __ldg(ctx + s);
-      if (t >= 0) Pt += t; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
-      Ct += c;
+  char* area = smem + 128 + pset_smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(area);  // full[kExtStages], empty[kExtStages]
+  ExtTile* meta = reinterpret_cast<ExtTile*>(area + 16 * kExtStages);
+  int32_t* slots = reinterpret_cast<int32_t*>(area + 256);  // stage s: tok at 2*s*cap, ctx at (2*s+1)*cap
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (nb + kExtConsumers - 1) / kExtConsumers;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kExtStages; s++) {
+      mbar_init(smem_u32(&bars[s]), 1);                             // full: producer + tx bytes
+      mbar_init(smem_u32(&bars[kExtStages + s]), kExtThreads / 32 - 1);  // empty: one per consumer warp
     }
-    if (feat) {
-      feat[3 * b] = Pt;
-      feat[3 * b + 1] = Dn;
-      feat[3 * b + 2] = Ct;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kExtThreads / 32 - 1) {  // ---------------- producer warp
+    int k = 0;
+    int64_t w0 = 0, w1 = 0;  // lane i: slot range of this CTA's tile k + i (window of 32 tiles)
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
+      const int s = k % kExtStages;
+      if ((k & 31) == 0) {  // prefetch the next 32 tiles' slot ranges, one per lane
+        const int64_t tt = t + (int64_t)lane * gridDim.x;
+        if (tt < ntiles) {
+          const int64_t b0 = tt * kExtConsumers;
+          w0 = __ldg(off + b0);
+          w1 = __ldg(off + min(b0 + kExtConsumers, nb));
+        }
+      }
+      const int64_t s0 = __shfl_sync(kFull, w0, k & 31), s1 = __shfl_sync(kFull, w1, k & 31);
+      if (k >= kExtStages) mbar_wait(smem_u32(&bars[kExtStages + s]), ((k / kExtStages) - 1) & 1);
+      if (lane == 0) {
+        const int64_t a0 = s0 & ~3LL, n = ((s1 + 3) & ~3LL) - a0;  // readable to a multiple of 4 (twb200.h)
+        const uint32_t full = smem_u32(&bars[s]);
+        meta[s].a0 = a0;
+        meta[s].staged = n <= cap;
+        if (n <= cap && n > 0) {
+          const uint32_t bytes = (uint32_t)(n * 4);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(full),
+                       "r"(2 * bytes)
+                       : "memory");
+          bulk_g2s(slots + (size_t)(2 * s) * cap, tok + a0, bytes, full);
+          bulk_g2s(slots + (size_t)(2 * s + 1) * cap, ctx + a0, bytes, full);
+        } else {
+          mbar_arrive(full);
+        }
+      }
+      __syncwarp();
     }
-    const int32_t ib = id[b];
-    if (s1 == s0) out[b] = TW_PRED_EMPTY_BATCH;
-    else if (((Pt | Dn) >> 31) == 0 && Ct >= 0) out[b] = predict_one(ps, qh, n_desc, (int32_t)Pt, (int32_t)Dn, Ct, ib);
-    else out[b] = predict_scalar(ps, ib, Pt, Dn, Ct);
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumer warps
+  constexpr int kC = kExtThreads - 32;
+  int64_t t = blockIdx.x;
+  int64_t s0[kExtBpt], s1[kExtBpt];
+  int32_t ib[kExtBpt];
+#pragma unroll
+  for (int j = 0; j < kExtBpt; j++) {
+    const int64_t b = t * kExtConsumers + j * kC + threadIdx.x;
+    s0[j] = s1[j] = 0;
+    ib[j] = 0;
+    if (t < ntiles && b < nb) {
+      s0[j] = __ldg(off + b);
+      s1[j] = __ldg(off + b + 1);
+      ib[j] = __ldg(id + b);
+    }
+  }
+  for (int k = 0; t < ntiles; t += gridDim.x, k++) {
+    const int s = k % kExtStages;
+    // prefetch the next tile's offsets and descriptor ids before waiting on this one
+    const int64_t tn = t + gridDim.x;
+    int64_t n0[kExtBpt], n1[kExtBpt];
+    int32_t nid[kExtBpt];
+#pragma unroll
+    for (int j = 0; j < kExtBpt; j++) {
+      const int64_t bn = tn * kExtConsumers + j * kC + threadIdx.x;
+      n0[j] = n1[j] = 0;
+      nid[j] = 0;
+      if (tn < ntiles && bn < nb) {
+        n0[j] = __ldg(off + bn);
+        n1[j] = __ldg(off + bn + 1);
+        nid[j] = __ldg(id + bn);
+      }
+    }
+    mbar_wait(smem_u32(&bars[s]), (k / kExtStages) & 1);
+    const int64_t a0 = meta[s].a0;
+    const bool staged = meta[s].staged;
+    int64_t Pt[kExtBpt], Dn[kExtBpt], Ct[kExtBpt];
+#pragma unroll
+    for (int j = 0; j < kExtBpt; j++) {
+      Pt[j] = Dn[j] = Ct[j] = 0;
+      if (staged) {
+        const int32_t* tt = slots + (size_t)(2 * s) * cap - a0;
+        const int32_t* cc = slots + (size_t)(2 * s + 1) * cap - a0;
+        for (int64_t q = s0[j]; q < s1[j]; q++) {
+          const int32_t x = tt[q];
+          if (x >= 0) Pt[j] += x; else Dn[j] += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+          Ct[j] += cc[q];
+        }
+      } else {
+        for (int64_t q = s0[j]; q < s1[j]; q++) {
+          const int32_t x = __ldg(tok + q);
+          if (x >= 0) Pt[j] += x; else Dn[j] += 1;
+          Ct[j] += __ldg(ctx + q);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars[kExtStages + s]));  // this warp is done with stage s
+#pragma unroll
+    for (int j = 0; j < kExtBpt; j++) {
+      const int64_t b = t * kExtConsumers + j * kC + threadIdx.x;
+      if (b < nb) {
+        if (feat) {
+          feat[3 * b] = Pt[j];
+          feat[3 * b + 1] = Dn[j];
+          feat[3 * b + 2] = Ct[j];
+        }
+        int64_t r;
+        if (s1[j] == s0[j]) r = TW_PRED_EMPTY_BATCH;
+        else if (((Pt[j] | Dn[j]) >> 31) == 0 && Ct[j] >= 0)
+          r = predict_one(ps, qh, n_desc, (int32_t)Pt[j], (int32_t)Dn[j], Ct[j], ib[j]);
+        else r = predict_scalar(ps, ib[j], Pt[j], Dn[j], Ct[j]);
+        __stcs(out + b, r);
+      }
+      s0[j] = n0[j];
+      s1[j] = n1[j];
+      ib[j] = nid[j];
+    }
   }
 }
 
@@ -261,10 +426,30 @@ extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const in
     return TW_EINVAL;
   }
   if (n_batches == 0) return TW_OK;
-  cudaFuncSetAttribute(k_predict_batches, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = pred_grid(n_batches, smem, (const void*)k_predict_batches);
-  k_predict_batches<<<grid, kPredThreads, smem, (cudaStream_t)stream>>>(
-      pset, (uint32_t)pset_bytes, batch_off, slot_tok, slot_ctx, desc_id, n_batches, feat_out, out_ns);
+  if (((uintptr_t)slot_tok | (uintptr_t)slot_ctx) & 15) {
+    set_error("tw_predict_batches: slot arrays must be 16-byte aligned");
+    return TW_EINVAL;
+  }
+  // shared memory: pset | 2 mbarriers (128 B) | 2 stages x (tok, ctx) x cap slots
+  int dev = 0, max_optin = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t pset_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
+  const int64_t room = (int64_t)max_optin - 1024 /* static */ - 128 - (int64_t)pset_smem - 256;
+  int32_t cap = (int32_t)((room / (8 * kExtStages)) & ~3LL);  // slots per stage (tok + ctx)
+  if (cap > 16 * kExtConsumers) cap = 16 * kExtConsumers;
+  if (cap < kExtConsumers) {
+    set_error("tw_predict_batches: predictor blob leaves no room for slot tiles");
+    return TW_ENOSMEM;
+  }
+  const size_t esmem = 128 + pset_smem + 256 + (size_t)cap * 8 * kExtStages;
+  cudaFuncSetAttribute(k_predict_batches, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem);
+  const int64_t ntiles = (n_batches + kExtConsumers - 1) / kExtConsumers;
+  const int grid = (int)(ntiles < sms ? ntiles : sms);
+  k_predict_batches<<<grid, kExtThreads, esmem, (cudaStream_t)stream>>>(
+      pset, (uint32_t)pset_bytes, pset_smem, cap, batch_off, slot_tok, slot_ctx, desc_id, n_batches, feat_out,
+      out_ns);
   count_launch();
   return check_launch("tw_predict_batches");
 }

@@ -512,6 +512,46 @@ class PredictorSet:
         return out.cpu().numpy() if host else out
 
     # -- CSR batches -> features -> ns ------------------------------------------------
+    def predict_csr(self, off, tok, ctx, desc_id, device=None, return_features=False, stream=None):
+        """Fused extraction + prediction over CSR batches given as arrays (torch or numpy).
+
+        off: int64 [nb + 1]; tok / ctx: int32 per slot (tok -1 = DecodeSlot), padded to
+        a multiple of 4 elements here when needed (twb200.h); desc_id: int32 [nb].
+        Returns (ns [, features [nb, 3]]) as CUDA tensors for CUDA inputs, else numpy.
+        """
+        import torch
+
+        from ._device import require_cuda, stream_handle
+
+        dev = require_cuda(device)
+        host = not isinstance(off, torch.Tensor)
+
+        def dv(x, dt):
+            if isinstance(x, torch.Tensor):
+                return x.to(device=dev, dtype=dt).contiguous()
+            return torch.as_tensor(np.ascontiguousarray(x)).to(device=dev, dtype=dt)
+
+        t_off, t_id = dv(off, torch.int64), dv(desc_id, torch.int32)
+        t_tok, t_ctx = dv(tok, torch.int32), dv(ctx, torch.int32)
+        pad = (-t_tok.numel()) % 4 or (4 if t_tok.numel() == 0 else 0)
+        if pad:
+            z = torch.zeros(pad, dtype=torch.int32, device=dev)
+            t_tok, t_ctx = torch.cat([t_tok, z]), torch.cat([t_ctx, z])
+        nb = t_off.numel() - 1
+        out = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
+        feat = torch.empty(max(3 * nb, 3), dtype=torch.int64, device=dev) if return_features else None
+        rc = _lib.load().tw_predict_batches(
+            self.device_blob(dev).data_ptr(), self.nbytes, t_off.data_ptr(), t_tok.data_ptr(), t_ctx.data_ptr(),
+            t_id.data_ptr(), nb, feat.data_ptr() if feat is not None else None, out.data_ptr(),
+            stream_handle(stream),
+        )
+        _lib.check(rc, "tw_predict_batches")
+        res, f = out[:nb], (feat[: 3 * nb].view(nb, 3) if feat is not None else None)
+        if host:
+            res = res.cpu().numpy()
+            f = f.cpu().numpy() if f is not None else None
+        return (res, f) if return_features else res
+
     def predict_batches(self, batches: Sequence, desc_id, device=None, return_features=False):
         """Fused feature extraction + prediction for reference-style batch objects."""
         import torch
@@ -556,6 +596,7 @@ def pack_batches(batches: Sequence):
             toks.append(-1)
             ctxs.append(int(d.context_len))
         off[i + 1] = len(toks)
-    tok = np.asarray(toks if toks else [0], np.int32)
-    ctx = np.asarray(ctxs if ctxs else [0], np.int32)
+    pad = (-len(toks)) % 4 or (4 if not toks else 0)  # readable to a multiple of 4 (twb200.h)
+    tok = np.asarray(toks + [0] * pad, np.int32)
+    ctx = np.asarray(ctxs + [0] * pad, np.int32)
     return off, tok, ctx

@@ -99,6 +99,35 @@ def test_predict_features_random_tables_equals_oracle():
     assert bad.size == 0, [(int(ids[i]), int(P[i]), int(D[i]), int(got[i]), int(want[i])) for i in bad[:5]]
 
 
+def test_fused_extraction_equals_oracle_on_csr_batches():
+    """tw_predict_batches (TMA-staged CSR tiles) vs the oracle's feature sums and
+    predictions: 3 M batches of 0-12 slots, prefill/decode mixes, plus tiles whose
+    slots overflow a shared-memory stage (direct-load path) and all-empty tiles."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+
+    pset = presets.calibration_set()
+    rng = np.random.default_rng(5)
+    nb = 3_000_000
+    counts = rng.integers(0, 13, nb)
+    counts[1_000_000:1_004_096] = 0            # four empty tiles
+    counts[2_000_000:2_001_024] = 40           # one tile far beyond a stage: direct loads
+    off = np.zeros(nb + 1, np.int64)
+    np.cumsum(counts, out=off[1:])
+    ns = int(off[-1])
+    tok = np.where(rng.random(ns) < 0.7, -1, rng.integers(1, 700, ns)).astype(np.int32)
+    ctx = rng.integers(0, 3000, ns).astype(np.int32)
+    ids = rng.integers(0, len(pset.predictors), nb).astype(np.int32)
+    got, feat = pset.predict_csr(off, tok, ctx, ids, return_features=True)
+    want_f = orc.extract_features(off, tok, ctx)
+    assert np.array_equal(feat, want_f)
+    empty = counts == 0
+    P, D, C = want_f[:, 0], want_f[:, 1], np.where(empty, -1, want_f[:, 2])
+    want = orc.predict_many(pset.blob, P.astype(np.int32), D.astype(np.int32), C, ids)
+    assert np.array_equal(got, want)
+    assert (got[empty] == -1).all()
+
+
 def test_reciprocal_division_equals_hardware_division():
     """div_rn_rcp (multiply + 2 FMA corrections) == __ddiv_rn on 2^28 operand pairs."""
     import torch
