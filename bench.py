@@ -261,6 +261,58 @@ def extraction_roofline(device, peak_gbs, nb: int = 1 << 25):
             "batches_per_s": round(nb / (ms / 1e3), 1), "traffic": measured_traffic("k_predict_batches")}
 
 
+def timekeeper_roofline(device, peak_gbs, A: int = 17):
+    """Bulk Timekeeper min-advance (tw_tk_resolve): one BarrierCore round for C
+    independent Timekeepers of A actors (dispatcher + TP8 x PP2 workers), every actor
+    eligible with a pending target, so every round resolves. Reported as
+    latency per advance step at C = 65,536 (the config-5 sweep) and as GB/s at C = 2^21
+    (algorithmic bytes per Timekeeper: 8A pending + 4 mask + 32 state read, 8A pending
+    clear + 32 state + 1 flag written). Pending targets are restored before each round
+    (not timed)."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200._device import stream_handle
+
+    lib = _lib.load()
+    s = torch.cuda.current_stream()
+    out = {"kernel": "k_tk_resolve", "bound": "hbm", "actors": A, "peak": peak_gbs, "unit": "GB/s"}
+    for C in (65536, 1 << 21):
+        g = torch.Generator(device=device).manual_seed(C)
+        base = 1_790_000_000_000_000_000
+        pend0 = base + torch.randint(1, 10**9, (C * A,), dtype=torch.int64, device=device, generator=g)
+        pending = pend0.clone()
+        elig = torch.full((C,), (1 << A) - 1, dtype=torch.int32, device=device)
+        offset = torch.zeros(C, dtype=torch.int64, device=device)
+        seq = torch.zeros(C, dtype=torch.int64, device=device)
+        wall = torch.full((C,), base, dtype=torch.int64, device=device)
+        last = torch.full((C,), base - 1_000_000, dtype=torch.int64, device=device)
+        bc = torch.empty(C, dtype=torch.int8, device=device)
+        durs = []
+        for i in range(13):
+            pending.copy_(pend0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            _lib.check(lib.tw_tk_resolve(pending.data_ptr(), elig.data_ptr(), C, A, 500_000, offset.data_ptr(),
+                                         seq.data_ptr(), wall.data_ptr(), last.data_ptr(), bc.data_ptr(),
+                                         stream_handle(s)), "tk_resolve")
+            b.record(s)
+            b.synchronize()
+            if i >= 3:
+                durs.append(a.elapsed_time(b))
+        assert bool((bc >= 0).all())  # every round resolves (|pending| == eligible)
+        ms = statistics.median(durs)
+        alg = C * (16 * A + 4 + 32 + 33)
+        key = "config5" if C == 65536 else "bulk"
+        out[key] = {"timekeepers": C, "us_per_advance_step": round(ms * 1e3, 2),
+                    "achieved": round(alg / (ms / 1e3) / 1e9, 1)}
+        del pend0, pending, elig, offset, seq, wall, last, bc
+    out["achieved"] = out["bulk"]["achieved"]
+    out["frac"] = round(out["achieved"] / peak_gbs, 4)
+    out["traffic"] = measured_traffic("k_tk_resolve")
+    return out
+
+
 def metrics_roofline(dev, args, flush, stream, peak_gbs):
     """tw_metrics_many over the sweep's stamps: every config's
     RunReport.summary() numbers. Algorithmic bytes: first + finish stamps (16 B),
@@ -458,6 +510,10 @@ def main():
             extra["extraction_roofline"] = extraction_roofline(device, peak_gbs)
         except Exception as exc:
             extra["extraction_roofline"] = {"error": repr(exc)}
+        try:
+            extra["timekeeper_roofline"] = timekeeper_roofline(device, peak_gbs)
+        except Exception as exc:
+            extra["timekeeper_roofline"] = {"error": repr(exc)}
         try:
             extra["metrics_reduction"] = metrics_roofline(dev, args, flush, stream, peak_gbs)
         except Exception as exc:

@@ -10,6 +10,8 @@
 //   tw_tk_resolve : one round of _try_resolve/_resolve for C Timekeepers x A actor
 //                   slots; A is padded to a power of two and 32/A Timekeepers share
 //                   a warp, reduced with shuffles inside their lane segment.
+#include <cmath>
+
 #include "common.cuh"
 
 namespace twb {
@@ -207,33 +209,46 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_replay(
   }
 }
 
-// One round of min-advance for n_cfg Timekeepers with A actor slots each.
-template <int AP>
-__global__ void __launch_bounds__(kTkThreads) k_tk_resolve(
+// One round of min-advance for n_cfg Timekeepers with A <= 32 actor slots each: one
+// warp resolves 32 consecutive Timekeepers. Their 32*A pending
+// targets are one contiguous run, read with coalesced loads into the warp's slice of
+// shared memory; lane l then owns Timekeeper c0 + l (eligibility bits, pending count,
+// t_min over its A entries) and its state (wall, last broadcast, offset, seq) is read
+// and written as coalesced rows; resolved Timekeepers' targets are cleared with
+// coalesced stores (timekeeper.py:318-366). (A warp-per-Timekeeper segmented-min form
+// reached 18% of HBM bandwidth against 83% for this one; profiles/README.md.)
+constexpr int kTkWarps2 = 8;
+__global__ void __launch_bounds__(32 * kTkWarps2) k_tk_resolve_rows(
     int64_t* __restrict__ pending, const uint32_t* __restrict__ elig, int32_t n_cfg, int32_t A,
-    int64_t cooldown, int64_t* __restrict__ offset, int64_t* __restrict__ seq,
+    int64_t cooldown, int64_t conv_cooldown, int64_t* __restrict__ offset, int64_t* __restrict__ seq,
     int64_t* __restrict__ wall, int64_t* __restrict__ last_bcast, int8_t* __restrict__ bcast) {
-  constexpr int kPerWarp = 32 / AP;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int seg = lane / AP, a = lane % AP;
-  const int64_t c = warp * kPerWarp + seg;
-  const bool live = c < n_cfg;
+  extern __shared__ int64_t tk_rows[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t c0 = ((int64_t)blockIdx.x * kTkWarps2 + wib) * 32;
+  if (c0 >= n_cfg) return;
+  const int n_here = (int)min((int64_t)32, (int64_t)n_cfg - c0);
+  const int total = n_here * A;
+  int64_t* buf = tk_rows + (size_t)wib * 32 * A;
+  int64_t* row = pending + c0 * A;
+  for (int q = lane; q < total; q += 32) buf[q] = row[q];
+  __syncwarp();
+  const int64_t c = c0 + lane;
+  const bool live = lane < n_here;
   const uint32_t m = live ? __ldg(elig + c) : 0u;
-  const bool el = live && a < A && ((m >> a) & 1u);
-  int64_t p = el ? pending[c * A + a] : INT64_MAX;
-  const unsigned seg_mask = (AP == 32) ? kFull : (((1u << AP) - 1u) << (seg * AP));
-  const unsigned has = __ballot_sync(kFull, el && p != INT64_MAX) & seg_mask;
-  const unsigned els = __ballot_sync(kFull, el) & seg_mask;
-  // segmented int64 min inside the AP-lane segment
-  int64_t t = p;
-#pragma unroll
-  for (int o = AP / 2; o > 0; o >>= 1) {
-    const int64_t w = __shfl_xor_sync(kFull, t, o);
-    t = w < t ? w : t;
+  int64_t t = INT64_MAX;
+  int nel = 0, nhas = 0;
+  for (int a = 0; a < A; a++) {
+    if ((m >> a) & 1u) {
+      const int64_t v = buf[lane * A + a];
+      nel++;
+      if (v != INT64_MAX) {
+        nhas++;
+        t = v < t ? v : t;
+      }
+    }
   }
-  const bool resolves = live && els != 0 && has == els;  // sealed assumed; |pending| == eligible
-  if (live && a == 0) {
+  const bool resolves = live && nel > 0 && nhas == nel;  // sealed assumed; |pending| == eligible
+  if (live) {
     if (!resolves) {
       bcast[c] = -1;
     } else {
@@ -241,12 +256,13 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_resolve(
       const int64_t lb = last_bcast[c];
       if (w < t && lb != INT64_MIN && cooldown > 0) {
         const int64_t wait = lb + cooldown - w;
-        if (wait > 0) w += fake_sleep_ns(wait);
+        if (wait > 0) w += (wait == cooldown) ? conv_cooldown : fake_sleep_ns(wait);
       }
       wall[c] = w;
       if (w < t) {
         const int64_t cand = t - w;
-        if (cand > offset[c]) offset[c] = cand;
+        const int64_t o = offset[c];
+        if (cand > o) offset[c] = cand;
         seq[c] += 1;
         last_bcast[c] = w;
         bcast[c] = 1;
@@ -255,7 +271,12 @@ __global__ void __launch_bounds__(kTkThreads) k_tk_resolve(
       }
     }
   }
-  if (resolves && a < A) pending[c * A + a] = INT64_MAX;  // pending.clear()
+  const unsigned rmask = __ballot_sync(kFull, resolves);
+  if (rmask) {  // pending.clear() of the resolved Timekeepers
+    const uint32_t inv = (65536u + (uint32_t)A - 1u) / (uint32_t)A;  // q / A for q < 32 A, A <= 32
+    for (int q = lane; q < total; q += 32)
+      if ((rmask >> ((uint32_t)q * inv >> 16)) & 1u) row[q] = INT64_MAX;
+  }
 }
 
 }  // namespace twb
@@ -288,23 +309,24 @@ extern "C" int tw_tk_resolve(int64_t* pending, const uint32_t* eligible_mask, in
     return TW_EINVAL;
   }
   if (n_cfg == 0) return TW_OK;
-  int ap = 1;
-  while (ap < A) ap <<= 1;
-  const int64_t warps = ((int64_t)n_cfg * ap + 31) / 32;
-  const int grid = (int)((warps * 32 + kTkThreads - 1) / kTkThreads);
   cudaStream_t s = (cudaStream_t)stream;
-#define TW_RESOLVE(APV)                                                                      \
-  k_tk_resolve<APV><<<grid, kTkThreads, 0, s>>>(pending, eligible_mask, n_cfg, A, cooldown_ns, \
-                                                offset_ns, seq, wall_ns, last_bcast_ns, broadcast)
-  switch (ap) {
-    case 1: TW_RESOLVE(1); break;
-    case 2: TW_RESOLVE(2); break;
-    case 4: TW_RESOLVE(4); break;
-    case 8: TW_RESOLVE(8); break;
-    case 16: TW_RESOLVE(16); break;
-    default: TW_RESOLVE(32); break;
+  // FakeClock.sleep(cooldown / 1e9) -> int(round(seconds * 1e9)) in host IEEE fp64
+  // (SSE2: each op rounds once, nearest-even), the same ops as fake_sleep_ns
+  const double secs = (double)cooldown_ns / 1e9;
+  const int64_t conv = cooldown_ns > 0 ? (int64_t)nearbyint(secs * 1e9) : 0;
+  {
+    const int64_t warps = ((int64_t)n_cfg + 31) / 32;
+    const int blocks = (int)((warps + kTkWarps2 - 1) / kTkWarps2);
+    const size_t smem = (size_t)kTkWarps2 * 32 * A * sizeof(int64_t);
+    static bool attr_set = false;  // up to 64 KB for A = 32: opt in once
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_tk_resolve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kTkWarps2 * 32 * 32 * (int)sizeof(int64_t));
+      attr_set = true;
+    }
+    k_tk_resolve_rows<<<blocks, 32 * kTkWarps2, smem, s>>>(pending, eligible_mask, n_cfg, A, cooldown_ns, conv,
+                                                           offset_ns, seq, wall_ns, last_bcast_ns, broadcast);
   }
-#undef TW_RESOLVE
   count_launch();
   return check_launch("tw_tk_resolve");
 }
