@@ -313,6 +313,57 @@ def timekeeper_roofline(device, peak_gbs, A: int = 17):
     return out
 
 
+def workload_generation(device, n_wl: int = 65536, n_req: int = 1000):
+    """tw_generate_poisson: config-5-shaped workloads (qps 8, prompt U[64, 2048], output
+    U[16, 256], 1,000 requests) for n_wl distinct seeds in one launch, against the
+    reference's host generator (numpy, one process) timed on a sample."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200._device import stream_handle
+    from paper_2601_00397_b200.workload import WorkloadSpec, poisson_arrays, wl_specs
+
+    doc = {"source": "poisson", "qps": 8, "num_requests": n_req,
+           "prompt_tokens": {"kind": "uniform", "low": 64, "high": 2048},
+           "output_tokens": {"kind": "uniform", "low": 16, "high": 256}}
+    specs = [WorkloadSpec.from_doc({**doc, "seed": 1000 + i}) for i in range(n_wl)]
+    sp = torch.from_numpy(wl_specs(specs).view(np.uint8).copy()).to(device)
+    off = torch.arange(n_wl + 1, dtype=torch.int64, device=device) * n_req
+    ts = torch.empty(n_wl * n_req, dtype=torch.int64, device=device)
+    pr = torch.empty(n_wl * n_req, dtype=torch.int32, device=device)
+    op = torch.empty(n_wl * n_req, dtype=torch.int32, device=device)
+    st = torch.empty(n_wl, dtype=torch.int32, device=device)
+    lib = _lib.load()
+    s = torch.cuda.current_stream()
+
+    def run():
+        _lib.check(lib.tw_generate_poisson(sp.data_ptr(), n_wl, off.data_ptr(), ts.data_ptr(), pr.data_ptr(),
+                                           op.data_ptr(), st.data_ptr(), stream_handle(s)), "generate")
+
+    run()
+    torch.cuda.synchronize()
+    durs = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        run()
+        b.record(s)
+        b.synchronize()
+        durs.append(a.elapsed_time(b))
+    ms = statistics.median(durs)
+    ok = bool((st == 0).all()) and np.array_equal(ts[:n_req].cpu().numpy(), poisson_arrays(specs[0])[0])
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 2.0:
+        poisson_arrays(specs[k % n_wl])
+        k += 1
+    host_rps = k * n_req / (time.perf_counter() - t0)
+    del ts, pr, op
+    return {"kernel": "k_generate_poisson", "workloads": n_wl, "requests": n_wl * n_req, "ms_per_launch": round(ms, 3),
+            "requests_per_s": round(n_wl * n_req / (ms / 1e3), 1), "host_numpy_requests_per_s_one_core": round(host_rps, 1),
+            "matches_host": ok, "bound": "latency", "note": "one thread per workload runs its sequential PCG64 stream"}
+
+
 def metrics_roofline(dev, args, flush, stream, peak_gbs):
     """tw_metrics_many over the sweep's stamps: every config's
     RunReport.summary() numbers. Algorithmic bytes: first + finish stamps (16 B),
@@ -514,6 +565,10 @@ def main():
             extra["timekeeper_roofline"] = timekeeper_roofline(device, peak_gbs)
         except Exception as exc:
             extra["timekeeper_roofline"] = {"error": repr(exc)}
+        try:
+            extra["workload_generation"] = workload_generation(device)
+        except Exception as exc:
+            extra["workload_generation"] = {"error": repr(exc)}
         try:
             extra["metrics_reduction"] = metrics_roofline(dev, args, flush, stream, peak_gbs)
         except Exception as exc:

@@ -432,6 +432,30 @@ int tw_core_group(const tw_core* core, int32_t group, int64_t* generation, int64
                   int64_t* open_since_ns, int32_t* flags, int32_t* members, int32_t cap,
                   int32_t* n_members);
 
+/* ---- bulk Poisson workload generation ------------------- */
+/* generate_arrivals for source "poisson" (workload.py:118-144), one thread per
+ * workload, bit-exact with numpy's Generator (PCG64, ziggurat exponential, Lemire
+ * bounded integers). The host seeds each workload: state/inc are
+ * np.random.default_rng(seed).bit_generator.state (128-bit values split hi/lo). */
+#define TW_TOKENS_FIXED 0   /* TokenDist kind "fixed": value a, no draw */
+#define TW_TOKENS_UNIFORM 1 /* TokenDist kind "uniform": integers(a, b + 1) */
+
+typedef struct tw_wl_spec {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo; /* PCG64 state after seeding */
+  double scale;                                /* 1.0 / qps (exponential scale) */
+  int32_t prompt_kind, prompt_a, prompt_b;
+  int32_t output_kind, output_a, output_b;
+  int32_t has_uint32;  /* PCG64 32-bit buffer (0 after seeding) */
+  uint32_t uinteger;
+} tw_wl_spec;          /* 72 B */
+
+/* Workload w fills requests [wl_off[w], wl_off[w+1]) of offset_ns (cumulative
+ * int(round(gap_s * 1e9))), prompt, output. status[w] = 0, or 1 + the index of the
+ * first request with a non-positive token count (WorkloadError, workload.py:137-140). */
+int tw_generate_poisson(const tw_wl_spec* specs, int32_t n_wl, const int64_t* wl_off,
+                        int64_t* offset_ns, int32_t* prompt, int32_t* output, int32_t* status,
+                        void* stream);
+
 /* ---- misc ------------------------------------------------------------------ */
 int tw_abi_version(void);
 const char* tw_last_error(void);

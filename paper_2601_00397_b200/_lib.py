@@ -135,6 +135,24 @@ RUN_METRICS_DTYPE = np.dtype(
         ("n_missing", "<i4"),
     ]
 )
+WL_SPEC_DTYPE = np.dtype(
+    [
+        ("state_hi", "<u8"),
+        ("state_lo", "<u8"),
+        ("inc_hi", "<u8"),
+        ("inc_lo", "<u8"),
+        ("scale", "<f8"),
+        ("prompt_kind", "<i4"),
+        ("prompt_a", "<i4"),
+        ("prompt_b", "<i4"),
+        ("output_kind", "<i4"),
+        ("output_a", "<i4"),
+        ("output_b", "<i4"),
+        ("has_uint32", "<i4"),
+        ("uinteger", "<u4"),
+    ]
+)
+TW_TOKENS_FIXED, TW_TOKENS_UNIFORM = 0, 1
 TW_METRICS_OK, TW_METRICS_INCOMPLETE, TW_METRICS_SIM_FAILED, TW_METRICS_TOO_LARGE = 0, 1, 2, 3
 
 assert PRED_DESC_DTYPE.itemsize == 64
@@ -145,6 +163,7 @@ assert SIM_CFG_DTYPE.itemsize == 64
 assert SIM_RESULT_DTYPE.itemsize == 64
 assert EVENT_DTYPE.itemsize == 16
 assert RUN_METRICS_DTYPE.itemsize == 160
+assert WL_SPEC_DTYPE.itemsize == 72
 
 # every symbol include/twb200.h declares (tests check the .so exports all of them)
 EXPORTED_SYMBOLS = (
@@ -157,6 +176,7 @@ EXPORTED_SYMBOLS = (
     "tw_sim_last_launch",
     "tw_sim_set_profile",
     "tw_metrics_many",
+    "tw_generate_poisson",
     "tw_core_new",
     "tw_core_free",
     "tw_core_handle",
@@ -195,6 +215,7 @@ _SIGNATURES = {
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
     "tw_sim_set_profile": (_I32, [_P]),
     "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "tw_generate_poisson": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "tw_abi_version": (_I32, []),
     "tw_last_error": (ctypes.c_char_p, []),
     "tw_launch_count": (_I64, []),

@@ -128,6 +128,47 @@ def test_fused_extraction_equals_oracle_on_csr_batches():
     assert (got[empty] == -1).all()
 
 
+def test_device_workload_generation_matches_reference_arrivals():
+    """tw_generate_poisson (numpy's PCG64 + ziggurat + Lemire in CUDA) reproduces the
+    reference's generate_arrivals: the 34 golden workloads by sha256 (32 sweep seeds,
+    the 10 k-request config 3 trace, a fixed-token workload) and 400 more specs against
+    the host restatement (qps 0.5-500, fixed and uniform tokens, full 31-bit ranges that
+    exercise Lemire rejections)."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2601_00397_b200.workload import WorkloadError, WorkloadSpec, generate_device, poisson_arrays
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "arrivals.json")) as fh:
+        shas = json.load(fh)
+    names = list(shas)
+    specs = [WorkloadSpec.from_doc(shas[k]["doc"]) for k in names]
+    out = generate_device(specs)
+    for w, name in enumerate(names):
+        ts, pr, op = out.workload(w)
+        assert hashlib.sha256(ts.tobytes() + pr.tobytes() + op.tobytes()).hexdigest() == shas[name]["sha"], name
+    rng = np.random.default_rng(3)
+    more = []
+    for k in range(400):
+        tok = lambda: {"kind": "fixed", "value": int(rng.integers(1, 5000))} if rng.random() < 0.2 else (  # noqa: E731
+            {"kind": "uniform", "low": 1, "high": 2**31 - 1} if rng.random() < 0.1 else
+            {"kind": "uniform", "low": int(rng.integers(1, 100)), "high": int(rng.integers(100, 9000))})
+        more.append(WorkloadSpec.from_doc({"source": "poisson", "qps": float(rng.choice([0.5, 3.7, 8, 40, 500])),
+                                           "seed": int(rng.integers(0, 2**31)), "num_requests": int(rng.integers(0, 700)),
+                                           "prompt_tokens": tok(), "output_tokens": tok()}))
+    out = generate_device(more)
+    for w, sp in enumerate(more):
+        want = poisson_arrays(sp)
+        got = out.workload(w)
+        for g, x in zip(got, want):
+            assert np.array_equal(g, x), (w, sp)
+    with pytest.raises(WorkloadError):
+        generate_device([WorkloadSpec.from_doc({"source": "poisson", "qps": 2, "seed": 1, "num_requests": 5,
+                                                "prompt_tokens": {"kind": "uniform", "low": -3, "high": 1},
+                                                "output_tokens": 4})])
+
+
 def test_reciprocal_division_equals_hardware_division():
     """div_rn_rcp (multiply + 2 FMA corrections) == __ddiv_rn on 2^28 operand pairs."""
     import torch

@@ -280,3 +280,34 @@ def test_bulk_lookup_section_decodes_to_the_tables():
                 assert q.tolist() == [grid[i, j], grid[i1, j], grid[i, j1], grid[i1, j1]]
     assert n_fast >= 16
     assert int(hdr["n_axis_sets"]) < 2 * n_fast  # calibration tables share their axes
+
+
+def test_ziggurat_tables_and_numpy_draw_restatement():
+    """csrc/ziggurat_tables.h holds the installed numpy's tables, and the restated draw
+    algorithms (oracle/numpy_rng.py, the basis of csrc/workload.cu) reproduce numpy's
+    Generator.exponential / integers streams exactly, slow paths included."""
+    import importlib.util
+    import re as _re
+
+    spec = importlib.util.spec_from_file_location("gen_zig", os.path.join(ROOT, "scripts", "gen_ziggurat.py"))
+    gz = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gz)
+    ke, we, fe = gz.locate()
+    text = open(os.path.join(ROOT, "paper_2601_00397_b200", "csrc", "ziggurat_tables.h")).read()
+    blocks = _re.findall(r"\{([^}]*)\}", text)
+    assert [int(v, 16) for v in _re.findall(r"0x[0-9a-f]+", blocks[0])] == list(ke)
+    assert [float(v) for v in blocks[1].replace("\n", "").split(",") if v.strip()] == list(we)
+    assert [float(v) for v in blocks[2].replace("\n", "").split(",") if v.strip()] == list(fe)
+
+    from oracle.numpy_rng import Pcg64, integers_closed, standard_exponential
+
+    n = 0
+    for seed in (1, 7, 99, 2601):
+        rng = np.random.default_rng(seed)
+        g = Pcg64(rng.bit_generator.state)
+        for i in range(2500):
+            assert rng.exponential(0.25) == 0.25 * standard_exponential(g, ke, we, fe)
+            lo, hi = [(64, 2048), (1, 1), (0, 2**31 - 1), (5, 6)][i % 4]
+            assert int(rng.integers(lo, hi + 1)) == integers_closed(g, lo, hi)
+            n += 1
+    assert n == 10_000
