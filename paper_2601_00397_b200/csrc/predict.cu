@@ -28,6 +28,17 @@ struct PsetSmem {
   }
 };
 
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
 // Exact RN(a / g) for an integer gap g > 0: a power-of-two gap scales exactly (a is an
 // integer or a product of magnitude >= 1, so no underflow); any other gap takes the
 // reciprocal division (div_rn_rcp, == __ddiv_rn).
@@ -56,14 +67,15 @@ __device__ __forceinline__ int64_t predict_one(const char* ps, const uint2* qh, 
                                                int64_t c, int32_t id) {
   if ((p | d) == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
   if ((unsigned)id < (unsigned)n_desc && (p | d) >= 0) {
-    const uint2 h = qh[id];
+    const uint2 h = lds_u2(smem_u32(qh) + 8u * (uint32_t)id);
     if (h.y & TW_QHDR_FAST) {
-      const int4* rec = reinterpret_cast<const int4*>(ps);
-      const int4 rp = rec[(h.x >> 16) + (32 - __clz(p))];
-      const int4 rd = rec[(h.y & 0xffffu) + (32 - __clz(d))];
+      // 32-bit shared-memory addresses: records and quads are 16-byte units of the blob
+      const uint32_t base = smem_u32(ps);
+      const int4 rp = lds_i4(base + 16u * ((h.x >> 16) + (32u - __clz(p))));
+      const int4 rd = lds_i4(base + 16u * ((h.y & 0xffffu) + (32u - __clz(d))));
       if ((rp.z | rd.z) >= 0 && p >= rp.x && p <= rp.y && d >= rd.x && d <= rd.y) {
         const int nd = (int)((h.y >> 16) & 0x7fffu);
-        const int4 q = rec[(h.x & 0xffffu) + rp.z * nd + rd.z];
+        const int4 q = lds_i4(base + 16u * ((h.x & 0xffffu) + (uint32_t)(rp.z * nd + rd.z)));
         const bool pex = p == rp.x, dex = d == rd.x;
         const int32_t c00 = q.x;
         const int32_t c10 = pex ? c00 : q.y;
@@ -283,13 +295,18 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
     for (int j = 0; j < kExtBpt; j++) {
       Pt[j] = Dn[j] = Ct[j] = 0;
       if (staged) {
-        const int32_t* tt = slots + (size_t)(2 * s) * cap - a0;
-        const int32_t* cc = slots + (size_t)(2 * s + 1) * cap - a0;
-        for (int64_t q = s0[j]; q < s1[j]; q++) {
-          const int32_t x = tt[q];
-          if (x >= 0) Pt[j] += x; else Dn[j] += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
-          Ct[j] += cc[q];
+        // 32-bit shared-memory addressing; the slot index is tile-relative (< cap)
+        const uint32_t tbase = smem_u32(slots + (size_t)(2 * s) * cap), cbase = tbase + 4u * (uint32_t)cap;
+        const uint32_t q1 = 4u * (uint32_t)(s1[j] - a0);
+        int32_t dn = 0;
+        for (uint32_t q = 4u * (uint32_t)(s0[j] - a0); q < q1; q += 4u) {
+          int32_t x, c;
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x) : "r"(tbase + q));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(c) : "r"(cbase + q));
+          if (x >= 0) Pt[j] += x; else dn++;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+          Ct[j] += c;
         }
+        Dn[j] = dn;
       } else {
         for (int64_t q = s0[j]; q < s1[j]; q++) {
           const int32_t x = __ldg(tok + q);
