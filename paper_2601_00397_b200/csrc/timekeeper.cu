@@ -318,12 +318,8 @@ extern "C" int tw_tk_resolve(int64_t* pending, const uint32_t* eligible_mask, in
     const int64_t warps = ((int64_t)n_cfg + 31) / 32;
     const int blocks = (int)((warps + kTkWarps2 - 1) / kTkWarps2);
     const size_t smem = (size_t)kTkWarps2 * 32 * A * sizeof(int64_t);
-    static bool attr_set = false;  // up to 64 KB for A = 32: opt in once
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_tk_resolve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kTkWarps2 * 32 * 32 * (int)sizeof(int64_t));
-      attr_set = true;
-    }
+    if (smem > 48 * 1024)  // A > 24: opt in to more than the default dynamic shared memory
+      cudaFuncSetAttribute(k_tk_resolve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_tk_resolve_rows<<<blocks, 32 * kTkWarps2, smem, s>>>(pending, eligible_mask, n_cfg, A, cooldown_ns, conv,
                                                            offset_ns, seq, wall_ns, last_bcast_ns, broadcast);
   }
