@@ -406,6 +406,43 @@ def test_sweep_1024_equals_oracle_on_every_config():
     assert int(out.results["events"].sum()) == events_expected
 
 
+def test_sweep_65536_equals_oracle_on_every_config():
+    """BASELINE config 5 at full size (65,536 configs: 8B + 70B tables x 32 workload
+    seeds, Timekeeper grid on): every record and every per-request stamp of the GPU
+    sweep equals the C oracle's (run on all host threads, ~20-40 s), and every run
+    summary equals the oracle's summary of those stamps on a strided sample."""
+    import os
+
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    sw = presets.sweep_65536()
+    assert len(sw) == 65536
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+    dev.run()
+    dev.run_metrics()
+    out = dev.fetch()
+    met = dev.fetch_metrics()
+    res, req_base, first, finish = orc.sim_many(
+        sw.pset.blob, sw.cfgs, sw.workloads.wl_off, sw.workloads.offset_ns, sw.workloads.prompt,
+        sw.workloads.output, per_request=True, n_threads=os.cpu_count(),
+    )
+    assert (out.results["status"] == 0).all()
+    for f in ("final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns", "status"):
+        assert np.array_equal(out.results[f], res[f]), f
+    assert np.array_equal(out.first_ns, first[: len(out.first_ns)])
+    assert np.array_equal(out.finish_ns, finish[: len(out.finish_ns)])
+    assert (met["status"] == 0).all()
+    for c in range(0, len(sw), 97):
+        w = int(sw.cfgs[c]["workload_id"])
+        lo, hi = int(sw.workloads.wl_off[w]), int(sw.workloads.wl_off[w + 1])
+        rb = int(req_base[c])
+        want = orc.metrics(sw.workloads.offset_ns[lo:hi], sw.workloads.output[lo:hi], first[rb : rb + hi - lo],
+                           finish[rb : rb + hi - lo], int(sw.cfgs[c]["epoch_ns"]))
+        assert met[c].tobytes() == want.tobytes(), c
+
+
 # ---------------------------------------------------------------------------------
 # metrics (SURVEY §8f row 1): on-device RunReport.summary()
 # ---------------------------------------------------------------------------------
