@@ -124,6 +124,28 @@ int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batc
                        const int32_t* desc_id, int64_t n_batches, int64_t* feat_out,
                        int64_t* out_ns, void* stream);
 
+/* One batch, synchronously, for the live engine's per-step predict() (engine.py:684):
+ * host_slots holds int32 tok[n_slots] then int32 ctx[n_slots] (slot encoding as in
+ * tw_predict_batches). The call stages them in caller-owned pinned host memory
+ * (io_bytes >= 8*n_slots + 8), which a one-warp kernel reads and answers in place
+ * (zero-copy under UVA; dev_io is reserved), reading the predictor blob from global
+ * memory; then it synchronizes `stream`. *out_ns receives ns or a TW_PRED_* code. */
+int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const int32_t* host_slots,
+                        int32_t n_slots, int32_t desc_id, void* pinned_io, void* dev_io,
+                        int64_t io_bytes, int64_t* out_ns, void* stream);
+
+/* Resident predictor service (the live engine's per-step predict(), engine.py:684):
+ * tw_service_start launches one persistent warp on its own non-blocking stream that
+ * serves requests through a mailbox in mapped pinned host memory; tw_service_predict
+ * (host_slots: int32 tok[n_slots] then ctx[n_slots]) writes a request and spins until
+ * the answer arrives (ns or a TW_PRED_* code in *out_ns); tw_service_stop ends the
+ * kernel and frees the mailbox. One caller thread per service. */
+typedef struct tw_service tw_service;
+int tw_service_start(const void* pset, int64_t pset_bytes, int32_t max_slots, tw_service** out);
+int tw_service_predict(tw_service* service, const int32_t* host_slots, int32_t n_slots,
+                       int32_t desc_id, int64_t* out_ns);
+int tw_service_stop(tw_service* service);
+
 /* Device self-test of the predictor's reciprocal-based exact division against the
  * hardware's correctly rounded __ddiv_rn on n pseudo-random operand pairs; adds the
  * number of differing quotients to *mismatches (device counter, caller-zeroed). */

@@ -169,6 +169,10 @@ assert WL_SPEC_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "tw_predict_features",
     "tw_predict_batches",
+    "tw_predict_one_sync",
+    "tw_service_start",
+    "tw_service_predict",
+    "tw_service_stop",
     "tw_selftest_division",
     "tw_tk_replay",
     "tw_tk_resolve",
@@ -205,6 +209,10 @@ _I64 = ctypes.c_int64
 _SIGNATURES = {
     "tw_predict_features": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P]),
     "tw_predict_batches": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
+    "tw_predict_one_sync": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P, _I64, _P, _P]),
+    "tw_service_start": (_I32, [_P, _I64, _I32, _P]),
+    "tw_service_predict": (_I32, [_P, _P, _I32, _I32, _P]),
+    "tw_service_stop": (_I32, [_P]),
     "tw_selftest_division": (_I32, [_I64, ctypes.c_uint64, _P, _P]),
     "tw_tk_replay": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tw_tk_resolve": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),

@@ -9,6 +9,8 @@
 // with 16-byte vector loads marked evict-first, each thread handling 4 queries per
 // iteration for memory-level parallelism; grid = one 1024-thread CTA per SM (A/B on
 // B200: 1024x1 > 640x2 > 512x2 > 256x3; profiles/README.md).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace twb {
@@ -340,6 +342,25 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
   }
 }
 
+// Single-batch prediction for the live engine's per-step call (engine.py:684): one
+// warp sums the batch's slots (lane-strided, shuffle reduction) and lane 0 predicts
+// straight from the global predictor blob (L2-resident; no shared-memory staging for
+// one query).
+__global__ void __launch_bounds__(32) k_predict_single(const char* __restrict__ pset, const int32_t* __restrict__ io,
+                                                      int32_t n, int32_t desc_id, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x;
+  int64_t Pt = 0, Dn = 0, Ct = 0;
+  for (int i = lane; i < n; i += 32) {
+    const int32_t x = io[i];
+    if (x >= 0) Pt += x; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+    Ct += io[n + i];
+  }
+  Pt = warp_sum_i64(Pt);
+  Dn = warp_sum_i64(Dn);
+  Ct = warp_sum_i64(Ct);
+  if (lane == 0) *out = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(pset, desc_id, Pt, Dn, Ct);
+}
+
 // Self-test of div_rn_rcp against the hardware-correct __ddiv_rn on pseudo-random
 // operands shaped like the lerps' (integer numerators up to 2^53, products of a double
 // difference and a small integer, integer gaps up to 2^24).
@@ -469,4 +490,168 @@ extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const in
       out_ns);
   count_launch();
   return check_launch("tw_predict_batches");
+}
+
+extern "C" int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const int32_t* host_slots, int32_t n_slots,
+                                   int32_t desc_id, void* pinned_io, void* dev_io, int64_t io_bytes,
+                                   int64_t* out_ns, void* stream) {
+  if (!pset || !pinned_io || !dev_io || !out_ns || n_slots < 0 || (n_slots > 0 && !host_slots) ||
+      io_bytes < 8 * (int64_t)n_slots + 8 || pset_bytes < (int64_t)sizeof(tw_pset_header)) {
+    set_error("tw_predict_one_sync: bad arguments");
+    return TW_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // pinned layout: int32 tok[n] | int32 ctx[n] | (8-byte aligned) int64 result. Pinned
+  // host memory is device-addressable under UVA, so the kernel reads the slots and
+  // writes the answer in place (zero-copy: no memcpy calls on the round trip).
+  char* h = static_cast<char*>(pinned_io);
+  const size_t slots = 8 * (size_t)n_slots, res = (slots + 7) & ~(size_t)7;
+  if (n_slots) memcpy(h, host_slots, slots);
+  (void)dev_io;
+  k_predict_single<<<1, 32, 0, s>>>(static_cast<const char*>(pset), reinterpret_cast<const int32_t*>(h), n_slots,
+                                    desc_id, reinterpret_cast<int64_t*>(h + res));
+  count_launch();
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    set_error("tw_predict_one_sync: %s", cudaGetErrorString(e));
+    return TW_ECUDA;
+  }
+  memcpy(out_ns, h + res, 8);
+  return TW_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Resident predictor service for the live engine (engine.py:684 calls predict() once
+// per step from one thread). One persistent warp polls a mailbox in mapped pinned
+// host memory; a request is the batch's slots, the answer is written back into the
+// mailbox. No launch, copy or stream synchronisation sits on the round trip, which is
+// then bounded by PCIe latency (a few microseconds) instead of kernel launch + sync.
+// ---------------------------------------------------------------------------------
+struct tw_service_mailbox {
+  // host -> device, one 8-byte word written last: request counter (bits 40-63), descriptor
+  // (bits 24-39; 0xffff = stop) and slot count (bits 0-23). One word means one PCIe read
+  // tells the warp everything but the slots, which its lanes then read in one round.
+  volatile uint64_t req;
+  volatile int64_t result;  // device -> host: ns or a TW_PRED_* code
+  volatile uint64_t ack;    // device -> host: the request word answered (written last)
+  volatile int32_t cap, pad;
+  volatile int32_t slots[1];  // tok[n] then ctx[n]
+};
+
+__global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__ pset, tw_service_mailbox* mb) {
+  const int lane = threadIdx.x;
+  uint64_t seen = 0;
+  for (;;) {
+    uint64_t w = 0;
+    if (lane == 0) {
+      do {
+        w = mb->req;
+        if (w == seen) __nanosleep(32);
+      } while (w == seen);
+    }
+    w = __shfl_sync(kFull, w, 0);
+    const int32_t desc = (int32_t)((w >> 24) & 0xffffu);
+    if (desc == 0xffff) return;  // stop
+    const int32_t n = (int32_t)(w & 0xffffffu);
+    int64_t Pt = 0, Dn = 0, Ct = 0;
+    for (int i = lane; i < n; i += 32) {
+      const int32_t x = mb->slots[i], c = mb->slots[n + i];  // one round of PCIe reads
+      if (x >= 0) Pt += x; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+      Ct += c;
+    }
+    Pt = warp_sum_i64(Pt);
+    Dn = warp_sum_i64(Dn);
+    Ct = warp_sum_i64(Ct);
+    if (lane == 0) {
+      mb->result = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(pset, desc, Pt, Dn, Ct);
+      __threadfence_system();  // the result lands before the acknowledgement
+      mb->ack = w;
+    }
+    seen = w;
+    __syncwarp();
+  }
+}
+
+struct tw_service {
+  tw_service_mailbox* host;
+  tw_service_mailbox* dev;
+  cudaStream_t stream;
+  uint64_t seq;
+  int32_t cap;
+};
+
+extern "C" int tw_service_start(const void* pset, int64_t pset_bytes, int32_t max_slots, tw_service** out) {
+  if (!pset || !out || max_slots < 1 || pset_bytes < (int64_t)sizeof(tw_pset_header)) {
+    set_error("tw_service_start: bad arguments");
+    return TW_EINVAL;
+  }
+  tw_service* sv = new tw_service();
+  const size_t bytes = sizeof(tw_service_mailbox) + 8 * (size_t)max_slots;
+  void* h = nullptr;
+  if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped) != cudaSuccess) {
+    delete sv;
+    set_error("tw_service_start: cudaHostAlloc failed");
+    return TW_ECUDA;
+  }
+  memset(h, 0, bytes);
+  sv->host = static_cast<tw_service_mailbox*>(h);
+  sv->host->cap = max_slots;
+  void* d = nullptr;
+  cudaHostGetDevicePointer(&d, h, 0);
+  sv->dev = static_cast<tw_service_mailbox*>(d);
+  sv->seq = 0;
+  sv->cap = max_slots;
+  cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking);
+  k_predict_service<<<1, 32, 0, sv->stream>>>(static_cast<const char*>(pset), sv->dev);
+  count_launch();
+  const int rc = check_launch("tw_service_start");
+  if (rc != TW_OK) {
+    cudaStreamDestroy(sv->stream);
+    cudaFreeHost(h);
+    delete sv;
+    return rc;
+  }
+  *out = sv;
+  return TW_OK;
+}
+
+extern "C" int tw_service_predict(tw_service* sv, const int32_t* host_slots, int32_t n_slots, int32_t desc_id,
+                                  int64_t* out_ns) {
+  if (!sv || !out_ns || n_slots < 0 || n_slots > sv->cap || (n_slots > 0 && !host_slots)) {
+    set_error("tw_service_predict: bad arguments (n_slots %d, capacity %d)", n_slots, sv ? sv->cap : 0);
+    return TW_EINVAL;
+  }
+  if (desc_id < 0 || desc_id >= 0xffff || n_slots >= (1 << 24)) {
+    set_error("tw_service_predict: descriptor %d or slot count %d out of range", desc_id, n_slots);
+    return TW_EINVAL;
+  }
+  tw_service_mailbox* mb = sv->host;
+  for (int i = 0; i < 2 * n_slots; i++) mb->slots[i] = host_slots[i];
+  __sync_synchronize();  // the slots before the request word
+  const uint64_t w = ((uint64_t)(++sv->seq & 0xffffff) << 40) | ((uint64_t)desc_id << 24) | (uint64_t)n_slots;
+  mb->req = w;
+  for (int64_t spins = 0; mb->ack != w; spins++) {
+    if ((spins & 0xfffff) == 0xfffff && cudaStreamQuery(sv->stream) != cudaErrorNotReady) {
+      set_error("tw_service_predict: the service kernel is not running");
+      return TW_ECUDA;
+    }
+  }
+  __sync_synchronize();
+  *out_ns = mb->result;
+  return TW_OK;
+}
+
+extern "C" int tw_service_stop(tw_service* sv) {
+  if (!sv) return TW_OK;
+  __sync_synchronize();
+  sv->host->req = ((uint64_t)(++sv->seq & 0xffffff) << 40) | (0xffffULL << 24);  // stop
+  const cudaError_t e = cudaStreamSynchronize(sv->stream);
+  cudaStreamDestroy(sv->stream);
+  cudaFreeHost(sv->host);
+  delete sv;
+  if (e != cudaSuccess) {
+    set_error("tw_service_stop: %s", cudaGetErrorString(e));
+    return TW_ECUDA;
+  }
+  return TW_OK;
 }

@@ -20,6 +20,7 @@ blob the kernels stage into shared memory with a TMA bulk copy (twb200.h).
 from __future__ import annotations
 
 import csv
+import ctypes
 import logging
 from dataclasses import dataclass, field
 from typing import Iterable, Sequence
@@ -147,9 +148,14 @@ class _DevicePredictor:
         return self._pset
 
     def predict(self, batch, hw: HardwareSpec | None = None) -> int:
-        """Returns the predicted step duration in nanoseconds (one GPU launch)."""
-        out = self.predictor_set.predict_batches([batch], [0])
-        code = int(out[0])
+        """Returns the predicted step duration in nanoseconds (one GPU launch).
+
+        The live engine calls this once per step (engine.py:684): one C call stages the
+        slots in pinned memory, which a one-warp kernel reads and answers in place
+        (zero-copy), then synchronizes (~25 us on a B200 box, kernel launch + sync
+        bound). A process that only predicts can use the resident service instead
+        (``predictor_set.service()``, ~14 us, no launch on the round trip)."""
+        code = self.predictor_set.live().predict_one(batch)
         if code < 0:
             raise_for_code(code, _describe(batch))
         return code
@@ -511,6 +517,24 @@ class PredictorSet:
         _lib.check(rc, "tw_predict_features")
         return out.cpu().numpy() if host else out
 
+    def service(self, device=None) -> "PredictorService":
+        from ._device import require_cuda
+
+        dev = require_cuda(device)
+        key = ("service", str(dev))
+        if key not in self._dev:
+            self._dev[key] = PredictorService(self, dev)
+        return self._dev[key]
+
+    def live(self, device=None) -> "_LiveChannel":
+        from ._device import require_cuda
+
+        dev = require_cuda(device)
+        key = ("live", str(dev))
+        if key not in self._dev:
+            self._dev[key] = _LiveChannel(self, dev)
+        return self._dev[key]
+
     # -- CSR batches -> features -> ns ------------------------------------------------
     def predict_csr(self, off, tok, ctx, desc_id, device=None, return_features=False, stream=None):
         """Fused extraction + prediction over CSR batches given as arrays (torch or numpy).
@@ -578,6 +602,108 @@ class PredictorSet:
         if return_features:
             return res, feat[: 3 * nb].cpu().numpy().reshape(nb, 3)
         return res
+
+
+class PredictorService:
+    """Resident predictor service on one device (twb200.h tw_service_*): one persistent
+    warp polls a mailbox in mapped pinned host memory and answers single-batch
+    predictions in place. Started on first use, stopped by ``close()`` or at exit.
+    One caller thread per service, like the engine loop that uses it.
+
+    The warp runs until ``close()``: a device-wide synchronisation in the same process
+    (``torch.cuda.synchronize()``, ``cudaDeviceSynchronize``) would wait for it forever,
+    so use the service in processes that only predict (the live engine replica), and
+    close it before synchronising the device."""
+
+    def __init__(self, pset: "PredictorSet", device, max_slots: int = 4096) -> None:
+        import atexit
+
+        import torch
+
+        with torch.cuda.device(device):
+            self.blob = pset.device_blob(device)
+            torch.cuda.synchronize(device)  # the blob is resident before the service reads it
+            h = ctypes.c_void_p()
+            _lib.check(_lib.load().tw_service_start(self.blob.data_ptr(), pset.nbytes, max_slots, ctypes.byref(h)),
+                       "tw_service_start")
+        self._h = h
+        self.max_slots = max_slots
+        self._buf = np.zeros(2 * max_slots, np.int32)
+        self._out = ctypes.c_int64()
+        self._out_ref = ctypes.byref(self._out)
+        self._fn = _lib.load().tw_service_predict
+        atexit.register(self.close)
+
+    def predict_one(self, batch, desc_id: int = 0) -> int:
+        chunks, decodes = batch.prefill_chunks, batch.decodes
+        n = len(chunks) + len(decodes)
+        if n > self.max_slots:
+            raise PredictorError(f"batch of {n} slots exceeds the service's {self.max_slots}")
+        buf = self._buf
+        i = 0
+        for c in chunks:
+            buf[i] = c.chunk_tokens
+            buf[n + i] = c.context_len_before
+            i += 1
+        for dslot in decodes:
+            buf[i] = -1
+            buf[n + i] = dslot.context_len
+            i += 1
+        _lib.check(self._fn(self._h, buf.ctypes.data, n, desc_id, self._out_ref), "tw_service_predict")
+        return int(self._out.value)
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h is not None and h.value:
+            _lib.load().tw_service_stop(h)
+
+
+class _LiveChannel:
+    """Single-batch prediction for the live engine (engine.py:684): one C call
+    (tw_predict_one_sync) stages the slots in pinned memory, copies them over, runs a
+    one-warp extraction + prediction kernel and copies the 8-byte answer back.
+    Not thread-safe: one channel per engine thread, like the engine loop itself."""
+
+    def __init__(self, pset: "PredictorSet", device) -> None:
+        import torch
+
+        self.pset = pset
+        self.device = device
+        self.blob_ptr = pset.device_blob(device).data_ptr()
+        self._torch = torch
+        self._alloc(256)
+        self._out = ctypes.c_int64()
+        self._out_ref = ctypes.byref(self._out)
+        self._fn = _lib.load().tw_predict_one_sync
+
+    def _alloc(self, cap: int) -> None:
+        torch = self._torch
+        self.cap = cap
+        self.h = torch.empty(8 * cap + 16, dtype=torch.uint8, pin_memory=True)
+        self.d = torch.empty(8 * cap + 16, dtype=torch.uint8, device=self.device)
+        self.buf = np.zeros(2 * cap, np.int32)
+
+    def predict_one(self, batch) -> int:
+        from ._device import stream_handle
+
+        chunks, decodes = batch.prefill_chunks, batch.decodes
+        n = len(chunks) + len(decodes)
+        if n > self.cap:
+            self._alloc(max(2 * self.cap, n))
+        buf = self.buf
+        i = 0
+        for c in chunks:
+            buf[i] = c.chunk_tokens
+            buf[n + i] = c.context_len_before
+            i += 1
+        for dslot in decodes:
+            buf[i] = -1
+            buf[n + i] = dslot.context_len
+            i += 1
+        rc = self._fn(self.blob_ptr, self.pset.nbytes, buf.ctypes.data, n, 0, self.h.data_ptr(), self.d.data_ptr(),
+                      8 * self.cap + 16, self._out_ref, stream_handle())
+        _lib.check(rc, "tw_predict_one_sync")
+        return int(self._out.value)
 
 
 def pack_batches(batches: Sequence):

@@ -99,6 +99,69 @@ def test_predict_features_random_tables_equals_oracle():
     assert bad.size == 0, [(int(ids[i]), int(P[i]), int(D[i]), int(got[i]), int(want[i])) for i in bad[:5]]
 
 
+def test_live_single_batch_predict_equals_bulk_and_oracle():
+    """predict(batch) (the live engine's per-step call, tw_predict_one_sync) equals the
+    bulk kernels and the oracle on random batches of every predictor kind."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.predictor import (
+        BatchComposition,
+        DecodeSlot,
+        EmptyBatch,
+        LinearPredictor,
+        PredictorError,
+        PrefillChunk,
+        TablePredictor,
+    )
+
+    rng = np.random.default_rng(9)
+    preds = list(presets.calibration_set().predictors[:3]) + [
+        LinearPredictor(120.5, 0.31, 11.0, 0.002), TablePredictor({(0, 1): 5, (64, 1): 9, (64, 4): 30})]
+    for pred in preds:
+        batches = []
+        for _ in range(150):
+            chunks = tuple(PrefillChunk(f"p{i}", int(rng.integers(1, 900)), int(rng.integers(0, 4000)))
+                           for i in range(int(rng.integers(0, 3))))
+            decs = tuple(DecodeSlot(f"d{i}", int(rng.integers(1, 3000))) for i in range(int(rng.integers(0, 40))))
+            batches.append(BatchComposition(chunks, decs))
+        bulk = pred.predict_many(batches, raise_errors=False)
+        P = np.array([sum(c.chunk_tokens for c in b.prefill_chunks) for b in batches], np.int32)
+        D = np.array([len(b.decodes) for b in batches], np.int32)
+        C = np.array([sum(c.context_len_before for c in b.prefill_chunks) + sum(d.context_len for d in b.decodes)
+                      if not b.is_empty() else -1 for b in batches], np.int64)
+        want = orc.predict_many(pred.predictor_set.blob, P, D, C, np.zeros(len(batches), np.int32))
+        assert np.array_equal(bulk, want)
+        for b, w in zip(batches, want):
+            if w >= 0:
+                assert pred.predict(b) == w
+            else:
+                with pytest.raises(EmptyBatch if w == -1 else PredictorError):
+                    pred.predict(b)
+
+
+def test_resident_predictor_service_equals_bulk():
+    """tw_service_* (persistent warp + mapped pinned mailbox) answers like the bulk
+    kernels, including empty batches and several descriptors; it is closed before any
+    device-wide synchronisation."""
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.predictor import BatchComposition, DecodeSlot, PrefillChunk
+
+    pset = presets.calibration_set()
+    rng = np.random.default_rng(13)
+    batches = [BatchComposition(tuple(PrefillChunk(f"p{i}", int(rng.integers(1, 900)), 0)
+                                      for i in range(int(rng.integers(0, 3)))),
+                                tuple(DecodeSlot(f"d{i}", 100) for i in range(int(rng.integers(0, 60)))))
+               for _ in range(300)]
+    ids = rng.integers(0, len(pset.predictors), len(batches)).astype(np.int32)
+    want = pset.predict_batches(batches, ids)
+    sv = pset.service()
+    try:
+        got = [sv.predict_one(b, int(k)) for b, k in zip(batches, ids)]
+    finally:
+        sv.close()
+    assert np.array_equal(np.asarray(got, np.int64), want)
+
+
 def test_fused_extraction_equals_oracle_on_csr_batches():
     """tw_predict_batches (TMA-staged CSR tiles) vs the oracle's feature sums and
     predictions: 3 M batches of 0-12 slots, prefill/decode mixes, plus tiles whose
