@@ -660,8 +660,8 @@ class PredictorService:
 
 class _LiveChannel:
     """Single-batch prediction for the live engine (engine.py:684): one C call
-    (tw_predict_one_sync) stages the slots in pinned memory, copies them over, runs a
-    one-warp extraction + prediction kernel and copies the 8-byte answer back.
+    (tw_predict_one_sync) stages the slots in pinned host memory, which a one-warp
+    kernel reads and answers in place (zero-copy), then synchronizes the stream.
     Not thread-safe: one channel per engine thread, like the engine loop itself."""
 
     def __init__(self, pset: "PredictorSet", device) -> None:
@@ -677,10 +677,8 @@ class _LiveChannel:
         self._fn = _lib.load().tw_predict_one_sync
 
     def _alloc(self, cap: int) -> None:
-        torch = self._torch
         self.cap = cap
-        self.h = torch.empty(8 * cap + 16, dtype=torch.uint8, pin_memory=True)
-        self.d = torch.empty(8 * cap + 16, dtype=torch.uint8, device=self.device)
+        self.h = self._torch.empty(8 * cap + 16, dtype=self._torch.uint8, pin_memory=True)
         self.buf = np.zeros(2 * cap, np.int32)
 
     def predict_one(self, batch) -> int:
@@ -700,8 +698,9 @@ class _LiveChannel:
             buf[i] = -1
             buf[n + i] = dslot.context_len
             i += 1
-        rc = self._fn(self.blob_ptr, self.pset.nbytes, buf.ctypes.data, n, 0, self.h.data_ptr(), self.d.data_ptr(),
-                      8 * self.cap + 16, self._out_ref, stream_handle())
+        hp = self.h.data_ptr()
+        rc = self._fn(self.blob_ptr, self.pset.nbytes, buf.ctypes.data, n, 0, hp, hp, 8 * self.cap + 16,
+                      self._out_ref, stream_handle())
         _lib.check(rc, "tw_predict_one_sync")
         return int(self._out.value)
 
