@@ -122,6 +122,11 @@ __device__ __forceinline__ int64_t us_to_ns_rn(double us) { return __double2ll_r
 // __ddiv_rn(a, b) bit for bit; tw_selftest_division checks it on device.
 __device__ __forceinline__ double div_rn_rcp(double a, double b, double rb) {
   double q = __dmul_rn(a, rb);
+#ifndef TWB_NO_POW2_RCP
+  // RN(1/b) is a power of two only for b = 2^k (b an integer < 2^52): then a * rb is the
+  // exact quotient and the corrections are no-ops (calibration axes are mostly 2^k gaps)
+  if ((__double_as_longlong(rb) & 0xFFFFFFFFFFFFFLL) == 0) return q;
+#endif
   double r = __fma_rn(-q, b, a);
   q = __fma_rn(r, rb, q);
   r = __fma_rn(-q, b, a);

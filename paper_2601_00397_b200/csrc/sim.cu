@@ -366,6 +366,7 @@ int64_t cold_predict_warp(const char* ps, int id, int64_t P, int64_t D, int64_t 
 }
 
 struct PredCache {
+  int64_t misses;      // profiling only
   int64_t key, val;    // this lane's entry
   int64_t P, D, C, d;  // single entry (uses_c)
   bool uses_c;
@@ -388,6 +389,9 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const unsigned hit = __ballot_sync(kFull, pc.key == key);
   if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
   const int64_t d = predict_miss(ps, id, P, D, C);
+#ifdef TWB_PROFILE_PHASES
+  pc.misses++;
+#endif
   if (lane == pc.victim) {
     pc.key = key;
     pc.val = d;
@@ -480,6 +484,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   // predictor: cache + whether a decode-only run has a constant duration
   const tw_pred_desc* pd = pset_desc(ps, cfg.pred_id < pset_ndesc(ps) ? cfg.pred_id : 0);
   PredCache pc;
+  pc.misses = 0;
   pc.key = -1;
   pc.val = 0;
   pc.victim = 0;
@@ -851,6 +856,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       q[9] = adm_cyc;
       q[10] = pred_cyc;
       q[11] = apply_cyc;
+      q[12] = pc.misses;
     }
   }
 }
