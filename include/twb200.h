@@ -67,7 +67,9 @@ extern "C" {
  *   int32 quads[np][nd][4] per fast table = {c[i][j], c[i+1][j], c[i][j+1],
  *     c[i+1][j+1]} (indices clamped at the last row/column; holes = -1)
  * The event loop needs only the first core_bytes (pass that as pset_bytes to
- * tw_sim_many); the bulk predictor kernels take the whole blob. The blob is built on
+ * tw_sim_many; passing the whole blob lets its prediction-cache misses use the
+ * bulk-lookup section, at the cost of shared memory per CTA); the bulk predictor
+ * kernels take the whole blob. The blob is built on
  * host (paper_2601_00397_b200/predictor.py::PredictorSet) and staged into shared
  * memory by each CTA with cp.async.bulk (TMA). */
 #define TW_QHDR_FAST 0x80000000u

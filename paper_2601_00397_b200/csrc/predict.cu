@@ -30,29 +30,6 @@ struct PsetSmem {
   }
 };
 
-__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ int4 lds_i4(uint32_t a) {
-  int4 v;
-  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-
-// Exact RN(a / g) for an integer gap g > 0: a power-of-two gap scales exactly (a is an
-// integer or a product of magnitude >= 1, so no underflow); any other gap takes the
-// reciprocal division (div_rn_rcp, == __ddiv_rn).
-__device__ __forceinline__ double div_gap(double a, int32_t g) {
-  if ((g & (g - 1)) == 0) {
-    const int k = __ffs(g) - 1;
-    return __dmul_rn(a, __hiloint2double((1023 - k) << 20, 0));
-  }
-  const double gd = (double)g;
-  return div_rn_rcp(a, gd, __drcp_rn(gd));
-}
-
 // Everything the bulk-lookup section cannot answer (non-table kinds, int64 grids,
 // ambiguous axis buckets, out-of-range keys, holes): the generic predictor, kept out
 // of line so the common path stays short.
@@ -68,47 +45,11 @@ __device__ __noinline__ int64_t predict_generic(const char* ps, int n_desc, int3
 __device__ __forceinline__ int64_t predict_one(const char* ps, const uint2* qh, int n_desc, int32_t p, int32_t d,
                                                int64_t c, int32_t id) {
   if ((p | d) == 0 && c < 0) return TW_PRED_EMPTY_BATCH;  // "no slots" marker
-  if ((unsigned)id < (unsigned)n_desc && (p | d) >= 0) {
-    const uint2 h = lds_u2(smem_u32(qh) + 8u * (uint32_t)id);
-    if (h.y & TW_QHDR_FAST) {
-      // 32-bit shared-memory addresses: records and quads are 16-byte units of the blob
-      const uint32_t base = smem_u32(ps);
-      const int4 rp = lds_i4(base + 16u * ((h.x >> 16) + (32u - __clz(p))));
-      const int4 rd = lds_i4(base + 16u * ((h.y & 0xffffu) + (32u - __clz(d))));
-      if ((rp.z | rd.z) >= 0 && p >= rp.x && p <= rp.y && d >= rd.x && d <= rd.y) {
-        const int nd = (int)((h.y >> 16) & 0x7fffu);
-        const int4 q = lds_i4(base + 16u * ((h.x & 0xffffu) + (uint32_t)(rp.z * nd + rd.z)));
-        const bool pex = p == rp.x, dex = d == rd.x;
-        const int32_t c00 = q.x;
-        const int32_t c10 = pex ? c00 : q.y;
-        const int32_t c01 = dex ? c00 : q.z;
-        const int32_t c11 = pex ? c01 : (dex ? c10 : q.w);
-        if ((c00 | c10 | c01 | c11) >= 0) {  // holes are the only negative entries
-          double us;
-          if (pex) {
-            us = dex ? (double)c00
-                     : __dadd_rn((double)c00, div_gap(__ll2double_rn((int64_t)(c01 - c00) * (d - rd.x)), rd.y - rd.x));
-          } else {
-            const int32_t gp = rp.y - rp.x, xp = p - rp.x;
-            const double a0 = __dadd_rn((double)c00, div_gap(__ll2double_rn((int64_t)(c10 - c00) * xp), gp));
-            if (dex) {
-              us = a0;
-            } else {
-              const double a1 = __dadd_rn((double)c01, div_gap(__ll2double_rn((int64_t)(c11 - c01) * xp), gp));
-              us = __dadd_rn(a0, div_gap(__dmul_rn(__dsub_rn(a1, a0), (double)(d - rd.x)), rd.y - rd.x));
-            }
-          }
-          return __double2ll_rn(us) * 1000;
-        }
-      }
-    }
-  }
+  int64_t r;
+  if (predict_fast(ps, qh, n_desc, p, d, id, r)) return r;
   return predict_generic(ps, n_desc, id, p, d, c);
 }
 
-__device__ __forceinline__ const uint2* pset_qhdr(const char* ps) {
-  return reinterpret_cast<const uint2*>(ps + reinterpret_cast<const tw_pset_header*>(ps)->fast_off);
-}
 
 #ifndef TWB_PRED_MIN_BLOCKS
 #define TWB_PRED_MIN_BLOCKS 1

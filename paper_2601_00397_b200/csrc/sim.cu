@@ -335,10 +335,15 @@ TWB_COLD int64_t cold_predict_scalar(const char* ps, int id, int64_t P, int64_t 
 }
 TWB_COLD int64_t cold_nearest_warp(const TableView& t, int64_t P, int64_t D) { return table_nearest_warp(t, P, D); }
 
-TWB_PRED_FN int64_t predict_miss(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
+TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_t P, int64_t D, int64_t C) {
 #ifdef TWB_SIM_WARP_PRED
   return predict_warp(ps, id, P, D, C);
 #else
+  // with the bulk-lookup section staged (latency regime): four shared-memory loads
+  if (qh != nullptr && ((P | D) >> 31) == 0) {
+    int64_t r;
+    if (predict_fast(ps, qh, pset_ndesc(ps), (int32_t)P, (int32_t)D, id, r)) return r;
+  }
   // every lane runs the same scalar lookup (bit-length LUT bracketing, exact int
   // lerps with blob reciprocals); only the rare nearest-row fallback uses the lanes
   if (id < 0 || id >= pset_ndesc(ps)) return TW_PRED_BAD_DESC;
@@ -373,8 +378,8 @@ struct PredCache {
   int victim;
 };
 
-__device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, int id, int64_t P, int64_t D,
-                                                  int64_t C) {
+__device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, const uint2* qh, int id, int64_t P,
+                                                  int64_t D, int64_t C) {
   const int lane = threadIdx.x & 31;
   if (pc.uses_c) {  // Linear models with a context term: one exact (P, D, C) entry
     if (P == pc.P && D == pc.D && C == pc.C) return pc.d;
@@ -388,7 +393,7 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const int64_t key = (P << 32) | D;
   const unsigned hit = __ballot_sync(kFull, pc.key == key);
   if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
-  const int64_t d = predict_miss(ps, id, P, D, C);
+  const int64_t d = predict_miss(ps, qh, id, P, D, C);
 #ifdef TWB_PROFILE_PHASES
   pc.misses++;
 #endif
@@ -493,6 +498,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   pc.C = -1;
   pc.d = 0;
   pc.uses_c = pd->kind == TW_PRED_LINEAR && pd->per_context_token_us != 0.0;
+  // the caller staged the whole blob (bulk-lookup section included) or only the core
+  const tw_pset_header* hdr = reinterpret_cast<const tw_pset_header*>(ps);
+  const uint2* qh = (hdr->fast_off > 0 && p.pset_bytes >= (uint32_t)hdr->total_bytes) ? pset_qhdr(ps) : nullptr;
   const bool macro_ok = !pc.uses_c && cfg.pred_id >= 0 && cfg.pred_id < pset_ndesc(ps);
 
   TkGrid g;
@@ -689,7 +697,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     adm_cyc += q3 - q2;
     const int64_t P = (int64_t)__reduce_add_sync(kFull, (unsigned)p_l);  // P <= max_batch_tokens
     const int64_t C = pc.uses_c ? warp_sum_i64_redux(c_l) : 0;
-    const int64_t d = predict_cached(pc, ps, cfg.pred_id, P, n_dec, C);
+    const int64_t d = predict_cached(pc, ps, qh, cfg.pred_id, P, n_dec, C);
     pred_cyc += TWB_CLK() - q3;
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
