@@ -102,15 +102,23 @@ __device__ __forceinline__ int64_t warp_sum_i64_redux(int64_t v) {
   const unsigned sh = __reduce_add_sync(kFull, hi);
   return ((int64_t)sh << 24) + (int64_t)sl;
 }
-// inclusive int64 scan across the warp
-__device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
+// Inclusive saturating scan of non-negative int32 counts (token takes, KV blocks):
+// partial sums clamp at INT32_MAX. Every decision compares an exclusive prefix against a
+// budget or free-block count <= INT32_MAX, and a clamped prefix is >= that bound exactly
+// when the true one is, so the decisions equal the exact 64-bit scan's (and totals of
+// admitted prefixes, which stay below the bound, are exact). 32-bit shuffles, less code.
+__device__ __forceinline__ int32_t warp_incl_scan_sat(int32_t v) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int64_t w = __shfl_up_sync(kFull, v, o);
-    if (lane >= o) v += w;
+    const int32_t w = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v = (int32_t)min((uint32_t)v + (uint32_t)w, 0x7fffffffu);
   }
   return v;
+}
+__device__ __forceinline__ int32_t warp_excl_from_incl(int32_t incl) {
+  const int32_t e = __shfl_up_sync(kFull, incl, 1);
+  return (threadIdx.x & 31) ? e : 0;
 }
 
 // a / b for a >= 0, b > 0. (A hand-made 32-bit fast path measured 13% slower than
@@ -611,8 +619,8 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       }
       if (do_chunks && __any_sync(kFull, mid)) {
         const int64_t want = mid ? min((int64_t)chunk, (int64_t)(pr - dn)) : 0;
-        const int64_t incl = warp_incl_scan_i64(want);
-        const int64_t E = want_before + incl - want;  // tokens taken by earlier chunks
+        const int32_t incl = warp_incl_scan_sat((int32_t)want);
+        const int64_t E = want_before + warp_excl_from_incl(incl);  // tokens taken by earlier chunks
         const bool chosen = mid && budget - E > 0;
         if (chosen) {
           const int64_t take = min(want, budget - E);
@@ -645,9 +653,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         const int32_t pr = cand ? (inwin ? q_pr : __ldg(prm + idx)) : 0;
         const int64_t need = blk.ceil_div(pr);
         const int64_t want = min((int64_t)chunk, (int64_t)pr);
-        const int64_t NEi = warp_incl_scan_i64(cand ? need : 0);
-        const int64_t WEi = warp_incl_scan_i64(cand ? want : 0);
-        const int64_t NE = NEi - need, WE = WEi - want;
+        const int32_t NEi = warp_incl_scan_sat(cand ? (int32_t)need : 0);
+        const int32_t WEi = warp_incl_scan_sat(cand ? (int32_t)want : 0);
+        const int64_t NE = warp_excl_from_incl(NEi), WE = warp_excl_from_incl(WEi);
         const bool ok = cand && (budget - WE > 0) && (need <= free_l - NE);
         const unsigned bad = __ballot_sync(kFull, !ok);
         const int k = bad ? __ffs(bad) - 1 : 32;
@@ -667,10 +675,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           min_rem = min(min_rem, take > 0 ? (int)((uint32_t)(pr - 1) / (uint32_t)take) : 0);
         }
         if (k == 0) break;
-        const int64_t tot_need = __shfl_sync(kFull, NEi, k - 1);
-        const int64_t tot_want = __shfl_sync(kFull, WEi, k - 1);
+        const int64_t tot_need = __shfl_sync(kFull, NEi, k - 1);  // <= free: exact
         const int64_t last_want = __shfl_sync(kFull, want, k - 1);
-        const int64_t last_we = tot_want - last_want;
+        const int64_t last_we = __shfl_sync(kFull, WE, k - 1);    // < budget: exact
         const int64_t last_take = min(last_want, budget - last_we);
         budget -= last_we + last_take;
         free_l -= tot_need;

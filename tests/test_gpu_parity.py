@@ -444,6 +444,44 @@ def test_sim_timekeeper_grid_matches_reference_barriercore(case):
     assert (int(r["tk_seq"]), int(r["tk_offset_ns"]), int(r["tk_wall_ns"])) == (case["seq"], case["offset"], case["wall"])
 
 
+def test_sim_huge_token_counts_equal_oracle():
+    """Prompts and chunks near 2^28-2^30 tokens: 32-lane sums of chunk takes and KV
+    blocks exceed int32, which the saturating warp scans must decide exactly like the
+    oracle's 64-bit arithmetic (budgets, KV gates, head-of-line blocking)."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import ConstantPredictor, PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SchedulingPolicy, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(17)
+    arrays, cfgs = [], []
+    for k in range(12):
+        n = int(rng.integers(20, 90))
+        ts = np.sort(rng.integers(0, 5_000_000, n)).astype(np.int64) * (k % 3)
+        pr = rng.integers(1 << 26, 1 << 29, n).astype(np.int32)
+        pr[:: 5] = rng.integers(1, 100, len(pr[:: 5]))
+        op = rng.integers(1, 6, n).astype(np.int32)
+        arrays.append((ts, pr, op))
+        chunk = int(rng.choice([1 << 28, 1 << 30, 2**31 - 1]))
+        eng = EngineConfig(chunk_size=chunk, max_batch_tokens=2**31 - 1, max_running=int(rng.choice([32, 64, 256])),
+                           kv_block_tokens=int(rng.choice([1, 7, 1024])), kv_capacity_blocks=2**31 - 1,
+                           policy=SchedulingPolicy.MIXED if k % 2 else SchedulingPolicy.PREFILL_PRIORITIZED)
+        cfgs.append(SweepConfig(engine=eng, pred_id=0, workload_id=k, timekeeper=bool(k % 3)))
+    wl = pack_arrays(arrays)
+    ca = config_array(cfgs)
+    pset = PredictorSet([ConstantPredictor(250)])
+    dev = DeviceSweep(pset, wl, ca, per_request=True)
+    dev.run()
+    out = dev.fetch()
+    for k in range(len(cfgs)):
+        ts, pr, op = wl.workload(k)
+        res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
+        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+            assert out.results[k][f] == res[f], (k, f)
+        lo, hi = out.req_base[k], out.req_base[k + 1]
+        assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
+
+
 def test_sweep_1024_equals_oracle_on_every_config():
     """BASELINE config 4 at full size: every record bit-identical to the C oracle."""
     from oracle import oracle as orc
