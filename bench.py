@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--share-device", action="store_true",
+                    help="all ranks on cuda:0 with gloo collectives: a one-GPU dry run of the multi-rank path")
     return ap.parse_args()
 
 
@@ -71,10 +73,14 @@ def build_workload(args, world, rank):
                   "grid": "mbt{1024..8192} x chunk{128..1024} x max_running{32..256} x (TP,PP) x 8 x policy x 2",
                   "timekeeper": "dispatcher + TP*PP workers, cooldown 500us", "parallelism": f"configs sharded, dp{world}",
                   "l2": "flushed (512 MiB write) between timed iterations"}
+        sw.global_ids = np.arange(len(sw), dtype=np.int64) + rank * len(sw)
+        sw.n_global = len(sw) * world
         return sw, config, "weak"
     full = presets.sweep_65536()
     shards = partition(estimate_cost(full.pset, full.cfgs, full.workloads), world)
     sw = full.subset(shards[rank])
+    sw.global_ids = shards[rank]
+    sw.n_global = len(full)
     config = {"workload": "BASELINE config 5: 65,536-config sweep sharded over GPUs (strong scaling)",
               "model": "Llama-3-8B/70B calibration tables (synthetic)", "configs_total": len(full),
               "configs_this_rank": len(sw), "parallelism": f"configs sharded, dp{world}",
@@ -459,8 +465,12 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_device:
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(device)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -496,20 +506,21 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        cdev = "cpu" if args.share_device else device  # gloo collectives on host tensors
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-        s = torch.tensor([vsec_local, float(steps_local)], dtype=torch.float64, device=device)
+        s = torch.tensor([vsec_local, float(steps_local)], dtype=torch.float64, device=cdev)
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
         vsec, steps_total = float(s[0].item()), float(s[1].item())
         # merge the per-config records on every rank (the sweep's only collective)
         from paper_2601_00397_b200.distributed import gather_results
 
-        n_local = torch.tensor([len(sw)], device=device)
+        n_local = torch.tensor([len(sw)], device=cdev)
         dist.all_reduce(n_local, op=dist.ReduceOp.MAX)
-        ids = np.arange(len(sw), dtype=np.int64) + rank * len(sw) if args.sweep == "1024" else None
-        if ids is not None:
-            gather_results(ids, out.results, len(sw) * world, int(n_local.item()), device)
+        # every rank ends with all records ordered by global config id
+        merged = gather_results(sw.global_ids, out.results, sw.n_global, int(n_local.item()), cdev)
+        assert int((merged["status"] == 0).sum()) == sw.n_global
 
     value = vsec / (ms_max / 1e3)
     preds_per_s = steps_total / (ms_max / 1e3)
@@ -530,7 +541,7 @@ def main():
                 e_durs.append(a.elapsed_time(b))
         e_ms = sum(e_durs) / len(e_durs)
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=device)
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cpu" if args.share_device else device)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
