@@ -137,6 +137,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def n_req_e2e(host) -> int:
+    return int(host.req_base[-1])
+
+
 def flush_l2(buf):
     buf.fill_(1)  # a plain write larger than L2
 
@@ -540,19 +544,26 @@ def main():
             if i >= args.warmup:
                 e_durs.append(a.elapsed_time(b))
         e_ms = sum(e_durs) / len(e_durs)
+        # the records and stamps the kernel wrote into pinned host memory are the device run's
+        hr = host.host_results()
+        if not (hr == out.results).all() or not np.array_equal(host._pairs_out[2][1].numpy()[: n_req_e2e(host)],
+                                                                  out.finish_ns):
+            raise SystemExit(f"rank {rank}: e2e host results differ from the device run")
         if world > 1:
             t = torch.tensor([e_ms], dtype=torch.float64, device="cpu" if args.share_device else device)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
                "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": host.d2h_bytes,
-               "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps_total / (e_ms / 1e3), 1)}
+               "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps_total / (e_ms / 1e3), 1),
+               "outputs": "zero-copy: the kernel stores records and stamps into pinned host memory"
+                          if host.zero_copy else "copied back after the kernel"}
 
     # ---- roofline of the dominant kernel (k_sim): algorithmic bytes / device time
     n_req = int(dev.req_base[-1])
     alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req  # configs in, records out, stamps out
                  + 16 * n_req  # each config reads its workload (ts 8 + prompt 4 + output 4 B/request)
-                 + dev.pset.core_nbytes * _lib.last_sim_launch()["grid"])
+                 + dev.stage_bytes * _lib.last_sim_launch()["grid"])
     achieved = alg_bytes / (ms / 1e3) / 1e9
     launch = _lib.last_sim_launch()
     roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
