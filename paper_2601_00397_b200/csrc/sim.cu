@@ -343,17 +343,10 @@ TWB_COLD int64_t cold_predict_scalar(const char* ps, int id, int64_t P, int64_t 
 }
 TWB_COLD int64_t cold_nearest_warp(const TableView& t, int64_t P, int64_t D) { return table_nearest_warp(t, P, D); }
 
-TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_t P, int64_t D, int64_t C) {
-#ifdef TWB_SIM_WARP_PRED
-  return predict_warp(ps, id, P, D, C);
-#else
-  // with the bulk-lookup section staged (latency regime): four shared-memory loads
-  if (qh != nullptr && ((P | D) >> 31) == 0) {
-    int64_t r;
-    if (predict_fast(ps, qh, pset_ndesc(ps), (int32_t)P, (int32_t)D, id, r)) return r;
-  }
-  // every lane runs the same scalar lookup (bit-length LUT bracketing, exact int
-  // lerps with blob reciprocals); only the rare nearest-row fallback uses the lanes
+#define TWB_LUT_FN __device__ __forceinline__  // outlining it: 65,536 configs 345 -> 392 ms
+// every lane runs the same scalar lookup (bit-length LUT bracketing, exact int lerps
+// with blob reciprocals); only the rare nearest-row fallback uses the lanes
+TWB_LUT_FN int64_t predict_lut(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
   if (id < 0 || id >= pset_ndesc(ps)) return TW_PRED_BAD_DESC;
   const tw_pred_desc* d = pset_desc(ps, id);
   if (d->kind != TW_PRED_TABLE) return cold_predict_scalar(ps, id, P, D, C);
@@ -366,10 +359,24 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_
   }
   if (d->allow_extrapolation) return cold_nearest_warp(t, P, D);
   return TW_PRED_TABLE_MISS;
+}
+
+TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_t P, int64_t D, int64_t C) {
+#ifdef TWB_SIM_WARP_PRED
+  return predict_warp(ps, id, P, D, C);
+#else
+  // with the bulk-lookup section staged (latency regime): four shared-memory loads
+  if (qh != nullptr && ((P | D) >> 31) == 0) {
+    int64_t r;
+    if (predict_fast(ps, qh, pset_ndesc(ps), (int32_t)P, (int32_t)D, id, r)) return r;
+  }
+  return predict_lut(ps, id, P, D, C);
 #endif
 }
 
-#ifndef TWB_SIM_OUTLINE_CTXPRED
+// Linear models with a context term only (never in the Table sweeps): out of line
+// (A/B: 1,024 configs 8.68 -> 8.63 ms, 65,536 configs 345 -> 335 ms)
+#ifdef TWB_SIM_INLINE_CTXPRED
 __device__ __forceinline__
 #else
 __device__ __noinline__
