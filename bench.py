@@ -175,6 +175,16 @@ def measured_traffic(kernel: str):
         return None
 
 
+def measured_issue(kernel: str):
+    """What bounds a latency-bound kernel, from the committed ncu capture
+    (profiles/traffic.json): issue-slot use and the dominant stall reasons."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)[kernel].get("issue")
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def predictor_roofline(device, peak_gbs):
     """Bulk predictor kernel (tw_predict_features) at 2^27 queries: achieved GB/s vs HBM peak."""
     import torch
@@ -570,8 +580,9 @@ def main():
             "frac": round(achieved / peak_gbs, 6), "traffic": measured_traffic("k_sim"),
             "algorithmic_bytes_per_launch": int(alg_bytes),
             "note": "serial per-config event loop: latency-bound (one warp per config), not HBM-bound; "
-                    "see ns_per_step_per_config", "launch": launch,
-            "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2)}
+                    "see ns_per_step_per_config and latency_bound", "launch": launch,
+            "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2),
+            "latency_bound": measured_issue("k_sim")}
 
     extra = {}
     if rank == 0:

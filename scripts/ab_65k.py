@@ -10,6 +10,10 @@ from paper_2601_00397_b200.sweep import DeviceSweep  # noqa: E402
 
 sw = presets.sweep_65536()
 dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+import os  # noqa: E402
+
+if os.environ.get("STAGE") == "full":  # A/B: whole blob (bulk-lookup misses) at lower occupancy
+    dev.stage_bytes = sw.pset.nbytes
 dev.run()
 torch.cuda.synchronize()
 ms = []
