@@ -580,6 +580,42 @@ def test_device_metrics_match_reference_summaries():
     assert int(got[len(recs)]["status"]) == TW_METRICS_SIM_FAILED  # stalled config: no summary
 
 
+def test_device_metrics_edge_workloads():
+    """Run summaries of degenerate workloads against the oracle: no requests, one
+    request, every output a single token (no TPOT values), identical latencies
+    (percentile ties), a 16,384-request workload (largest supported), an epoch offset."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import ConstantPredictor, PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(23)
+    arrays = [
+        (np.zeros(0, np.int64), np.zeros(0, np.int32), np.zeros(0, np.int32)),
+        (np.array([5_000], np.int64), np.array([300], np.int32), np.array([7], np.int32)),
+        (np.sort(rng.integers(0, 10**9, 200)).astype(np.int64), rng.integers(1, 900, 200).astype(np.int32),
+         np.ones(200, np.int32)),
+        (np.zeros(64, np.int64), np.full(64, 128, np.int32), np.full(64, 3, np.int32)),
+        (np.sort(rng.integers(0, 10**12, 16384)).astype(np.int64), rng.integers(1, 600, 16384).astype(np.int32),
+         rng.integers(1, 40, 16384).astype(np.int32)),
+    ]
+    eng = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
+                       kv_capacity_blocks=1 << 20)
+    cfgs = config_array([SweepConfig(engine=eng, pred_id=0, workload_id=w, epoch_ns=[0, 7, 10**15, 3, 0][w])
+                         for w in range(len(arrays))])
+    dev = DeviceSweep(PredictorSet([ConstantPredictor(900)]), pack_arrays(arrays), cfgs, per_request=True)
+    dev.run()
+    dev.run_metrics()
+    got = dev.fetch_metrics()
+    out = dev.fetch()
+    for w, (ts, pr, op) in enumerate(arrays):
+        rb = int(out.req_base[w])
+        want = orc.metrics(ts, op, out.first_ns[rb : rb + len(ts)], out.finish_ns[rb : rb + len(ts)],
+                           int(cfgs[w]["epoch_ns"]))
+        assert got[w].tobytes() == want.tobytes(), w
+    assert int(got[2]["tpot"]["count"]) == 0 and int(got[0]["num_requests"]) == 0
+
+
 def test_device_metrics_equal_oracle_on_sweep_1024():
     from oracle import oracle as orc
     from paper_2601_00397_b200 import presets
