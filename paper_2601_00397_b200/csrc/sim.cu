@@ -558,6 +558,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     int total_dec = 0;
     bool any_mid = false;
     if (n_act > 32) {
+#pragma unroll 1
       for (int b = 0; b < n_act; b += 32) {
         const int i = b + lane;
         const bool v = i < n_act;
@@ -573,6 +574,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const bool need_free = waiting;
     if (need_free) {
       int64_t held_l = 0;
+#pragma unroll 1
       for (int b = 0; b < n_act; b += 32) {
         const int i = b + lane;
         if (i < n_act) {
@@ -590,6 +592,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     int dec_before = 0;
     int64_t want_before = 0, budget = mbt;
     int min_rem = 0x7fffffff;  // macro-step horizon: decoders' remaining outputs, chunks' repeats
+#pragma unroll 1
     for (int b = 0; b < (n_act > 0 ? n_act : 1); b += 32) {
       const int i = b + lane;
       const bool v = i < n_act;
@@ -778,6 +781,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int chunk_ev_total = __reduce_add_sync(kFull, (unsigned)chunk_ev);
     int64_t pos_c = n_events + body, pos_d = pos_c + chunk_ev_total;
     int kept = 0;
+#pragma unroll 1
     for (int b = 0; b < n_tot; b += 32) {
       const int i = b + lane;
       const bool v = i < n_tot;
