@@ -12,7 +12,7 @@ the assertions of pkg/tests/test_harness_integration.py:77-84.
 
 Needs the reference package installed under ``baseline/_ref`` (the task's one offline
 ``pip install --target``; git-ignored, shipped to the GPU box with the snapshot) and a
-GPU; skipped otherwise.
+GPU; skipped otherwise. The native-BarrierCore test (§8f row 3) needs no GPU.
 """
 
 from __future__ import annotations
@@ -25,14 +25,13 @@ import textwrap
 
 import pytest
 
+from paper_2601_00397_b200 import calibration
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 
-pytestmark = [
-    pytest.mark.gpu,
-    pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "timewarp")),
-                       reason="reference not installed under baseline/_ref"),
-]
+pytestmark = pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "timewarp")),
+                                reason="reference not installed under baseline/_ref")
 
 # engine-process hook: the reference's factory, answered by this engine's predictors
 SITECUSTOMIZE = textwrap.dedent('''
@@ -64,13 +63,29 @@ SITECUSTOMIZE = textwrap.dedent('''
     atexit.register(_report)
 ''')
 
+# runner process: optionally the native BarrierCore inside the reference's TimekeeperServer
+# (timekeeper.py:435 constructs it by module-global name); run_benchmark's verify_log then
+# replays the server's log through the reference's own BarrierCore (runner.py:182)
 RUNNER = textwrap.dedent('''
     import json, os, sys
+    cores = []
+    if os.environ.get("TWB200_NATIVE_CORE"):
+        sys.path.insert(0, os.environ["TWB200_ROOT"])
+        import timewarp.timekeeper as _tk
+        from paper_2601_00397_b200.barrier_core import NativeBarrierCore
+
+        class _Core(NativeBarrierCore):
+            def __init__(self, *a, **k):
+                super().__init__(*a, **k)
+                cores.append(type(self).__mro__[1].__name__)
+
+        _tk.BarrierCore = _Core
     from timewarp.runner import run_benchmark, run_oracle
     doc = json.loads(sys.argv[1]); out = sys.argv[2]
-    rep = run_benchmark(doc, "timewarp", os.path.join(out, "live"))
+    rep = run_benchmark(doc, "timewarp", os.path.join(out, "live"), verify_log=True)
     run_oracle(doc, os.path.join(out, "oracle"))
-    json.dump({"epoch_ns": rep.epoch_ns, "mode": rep.mode}, open(os.path.join(out, "live.json"), "w"))
+    json.dump({"epoch_ns": rep.epoch_ns, "mode": rep.mode, "cores": cores},
+              open(os.path.join(out, "live.json"), "w"))
 ''')
 
 
@@ -79,16 +94,19 @@ def _load(path):
         return [json.loads(line) for line in fh if line.strip()]
 
 
-def _run_live(tmp_path, doc):
+def _run_live(tmp_path, doc, device_predictor=True, native_core=False):
     site = tmp_path / "site"
     site.mkdir()
-    (site / "sitecustomize.py").write_text(SITECUSTOMIZE)
+    if device_predictor:
+        (site / "sitecustomize.py").write_text(SITECUSTOMIZE)
     out = tmp_path / "runs"
     out.mkdir()
     log = tmp_path / "live_log.json"
     env = dict(os.environ)
     env["TWB200_ROOT"] = ROOT
     env["TWB200_LIVE_LOG"] = str(log)
+    if native_core:
+        env["TWB200_NATIVE_CORE"] = "1"
     # the runner (and the oracle leg) run plain reference code; only the engine
     # subprocess's predictor factory is swapped
     runner_env = dict(env)
@@ -115,7 +133,7 @@ def _run_live(tmp_path, doc):
     live = _load(out / "live" / "engine_events.jsonl")
     ref = _load(out / "oracle" / "engine_events.jsonl")
     meta = json.loads((out / "live.json").read_text())
-    hook = json.loads(log.read_text())
+    hook = json.loads(log.read_text()) if device_predictor else None
     return live, ref, meta, hook
 
 
@@ -137,6 +155,7 @@ SMOKE = {  # pkg/tests/test_harness_integration.py:16-34
 }
 
 
+@pytest.mark.gpu
 def test_live_engine_constant_predictor_matches_oracle(tmp_path):
     live, ref, meta, hook = _run_live(tmp_path, SMOKE)
     assert meta["mode"] == "timewarp"
@@ -147,20 +166,40 @@ def test_live_engine_constant_predictor_matches_oracle(tmp_path):
     assert hook["native"].startswith(ROOT)
 
 
-def test_live_engine_table_predictor_matches_oracle(tmp_path):
-    from paper_2601_00397_b200 import calibration
+TABLE_DOC = {
+    "workload": {"source": "poisson", "qps": 16, "seed": 7, "num_requests": 40,
+                 "prompt_tokens": {"kind": "uniform", "low": 64, "high": 2048},
+                 "output_tokens": {"kind": "uniform", "low": 4, "high": 48}},
+    "engine": {"chunk_size": 256, "max_batch_tokens": 1024, "max_running": 16,
+               "kv_block_tokens": 16, "kv_capacity_blocks": 2048, "policy": "prefill_prioritized"},
+    "predictor": {"kind": "table", "path": calibration.csv_path("8b", 2, 2), "allow_extrapolation": True},
+    "timekeeper": {"jitter_cooldown_us": 500},
+}
 
-    doc = {
-        "workload": {"source": "poisson", "qps": 16, "seed": 7, "num_requests": 40,
-                     "prompt_tokens": {"kind": "uniform", "low": 64, "high": 2048},
-                     "output_tokens": {"kind": "uniform", "low": 4, "high": 48}},
-        "engine": {"chunk_size": 256, "max_batch_tokens": 1024, "max_running": 16,
-                   "kv_block_tokens": 16, "kv_capacity_blocks": 2048, "policy": "prefill_prioritized"},
-        "predictor": {"kind": "table", "path": calibration.csv_path("8b", 2, 2), "allow_extrapolation": True},
-        "timekeeper": {"jitter_cooldown_us": 500},
-    }
+
+@pytest.mark.gpu
+def test_live_engine_table_predictor_matches_oracle(tmp_path):
+    doc = TABLE_DOC
     live, ref, meta, hook = _run_live(tmp_path, doc)
     assert len(live) == len(ref) > 0
     _assert_same(live, ref, meta)
     assert hook["kinds"] == ["table"]
+    assert hook["predict_calls"] == max(e["step"] for e in ref)
+
+
+def test_live_timekeeper_with_native_core_matches_oracle(tmp_path):
+    """SURVEY §8f row 3 in the live stack (CPU: host C++ core, reference predictor): the
+    reference's TimekeeperServer drives the native BarrierCore over TCP; the events equal
+    the oracle's and the server log replays through the reference's BarrierCore."""
+    live, ref, meta, _ = _run_live(tmp_path, TABLE_DOC, device_predictor=False, native_core=True)
+    assert meta["cores"] == ["NativeBarrierCore"]
+    assert len(live) == len(ref) > 0
+    _assert_same(live, ref, meta)
+
+
+@pytest.mark.gpu
+def test_live_stack_native_core_and_device_predictor_match_oracle(tmp_path):
+    live, ref, meta, hook = _run_live(tmp_path, TABLE_DOC, device_predictor=True, native_core=True)
+    assert meta["cores"] == ["NativeBarrierCore"]
+    _assert_same(live, ref, meta)
     assert hook["predict_calls"] == max(e["step"] for e in ref)
