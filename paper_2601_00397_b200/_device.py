@@ -30,6 +30,8 @@ def to_device(arr: np.ndarray, device, non_blocking: bool = False) -> torch.Tens
     a = np.ascontiguousarray(arr)
     if a.dtype.fields is not None or a.dtype == np.uint64:
         a = a.view(np.uint8).reshape(-1)
+    if not a.flags.writeable:  # torch.from_numpy wants a writable buffer; the copy is host-side
+        a = a.copy()
     t = torch.from_numpy(a)
     if non_blocking:
         t = t.pin_memory()
