@@ -296,7 +296,7 @@ def timekeeper_roofline(device, peak_gbs, A: int = 17):
 
     lib = _lib.load()
     s = torch.cuda.current_stream()
-    out = {"kernel": "k_tk_resolve", "bound": "hbm", "actors": A, "peak": peak_gbs, "unit": "GB/s"}
+    out = {"kernel": "k_tk_resolve_rows", "bound": "hbm", "actors": A, "peak": peak_gbs, "unit": "GB/s"}
     for C in (65536, 1 << 21):
         g = torch.Generator(device=device).manual_seed(C)
         base = 1_790_000_000_000_000_000
