@@ -573,7 +573,8 @@ def main():
     n_req = int(dev.req_base[-1])
     alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req  # configs in, records out, stamps out
                  + 16 * n_req  # each config reads its workload (ts 8 + prompt 4 + output 4 B/request)
-                 + dev.stage_bytes * _lib.last_sim_launch()["grid"])
+                 + dev.stage_bytes * (_lib.last_sim_launch()["grid"]
+                                      if _lib.last_sim_launch()["variant"] == "latency" else 1))
     achieved = alg_bytes / (ms / 1e3) / 1e9
     launch = _lib.last_sim_launch()
     roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",

@@ -66,12 +66,12 @@ extern "C" {
  *     is outside the axis
  *   int32 quads[np][nd][4] per fast table = {c[i][j], c[i+1][j], c[i][j+1],
  *     c[i+1][j+1]} (indices clamped at the last row/column; holes = -1)
- * The event loop needs only the first core_bytes (pass that as pset_bytes to
- * tw_sim_many; passing the whole blob lets its prediction-cache misses use the
- * bulk-lookup section, at the cost of shared memory per CTA); the bulk predictor
- * kernels take the whole blob. The blob is built on
- * host (paper_2601_00397_b200/predictor.py::PredictorSet) and staged into shared
- * memory by each CTA with cp.async.bulk (TMA). */
+ * The event loop needs only the first core_bytes (tw_sim_many accepts that as
+ * pset_bytes; passing the whole blob lets its prediction-cache misses use the
+ * bulk-lookup section); the bulk predictor kernels take the whole blob. The blob is
+ * built on host (paper_2601_00397_b200/predictor.py::PredictorSet) and staged into
+ * shared memory by each CTA with cp.async.bulk (TMA), except in tw_sim_many's
+ * throughput variant, which reads it from global memory. */
 #define TW_QHDR_FAST 0x80000000u
 #define TW_PSET_MAGIC 0x54534550u /* "PEST" little-endian */
 #define TW_PRED_CONSTANT 0        /* predictor.py:100-111 */
@@ -296,7 +296,12 @@ typedef struct tw_event {
  * ev[ev_off[c] .. ev_off[c+1]). slot_capacity: per-warp active-list capacity,
  * normally max(max_running) over the configs (configs above it finish with
  * TW_SIM_CAPACITY; at most 4096). scratch: >= 16 bytes of device memory, zeroed by
- * the call (work counter). */
+ * the call (work counter).
+ * Two variants of the same kernel, picked by n_cfg: up to 8 configs per SM (every
+ * config resident on its own warp: latency-bound), each CTA stages pset_bytes of the
+ * blob in shared memory; above that (throughput-bound), the blob is read from global
+ * memory so that shared memory holds only slot state and 4 CTAs of <= 128 registers
+ * fit per SM. Results are identical. */
 int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
                 int32_t n_cfg, const int32_t* order, const int64_t* wl_off,
                 const int64_t* req_offset_ns, const int32_t* req_prompt,

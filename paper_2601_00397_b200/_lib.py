@@ -274,4 +274,6 @@ def last_sim_launch() -> dict:
         "block": vals[1].value,
         "smem_bytes": vals[2].value,
         "slot_capacity": vals[3].value,
+        # the throughput variant keeps only slot state in shared memory (twb200.h)
+        "variant": "throughput" if vals[2].value == 128 + 4 * 7 * 4 * vals[3].value else "latency",
     }

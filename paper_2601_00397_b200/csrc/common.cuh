@@ -339,20 +339,30 @@ __device__ __forceinline__ double div_gap(double a, int32_t g) {
 // on different tables mostly hit the same records), one 16-byte corner quad; exact
 // fp64 lerps in the reference's order (predictor.py:209-236). Returns false when the
 // section cannot answer (non-table kinds, int64-grid tables, straddling buckets,
-// out-of-range keys, holes): the caller then takes the generic path. ps must be the
-// blob staged in shared memory, including the section.
+// out-of-range keys, holes): the caller then takes the generic path. With kShared, ps
+// is the blob staged in shared memory (32-bit ld.shared addressing); otherwise ps is the
+// blob in global memory, read through the read-only path. Either way the section must
+// be present (the blob's full total_bytes).
+template <bool kShared = true>
+__device__ __forceinline__ int4 pset_unit16(const char* ps, uint32_t base, uint32_t unit) {
+  if constexpr (kShared) return lds_i4(base + 16u * unit);
+  else return __ldg(reinterpret_cast<const int4*>(ps) + unit);
+}
+template <bool kShared = true>
 __device__ __forceinline__ bool predict_fast(const char* ps, const uint2* qh, int n_desc, int32_t p, int32_t d,
                                              int32_t id, int64_t& out) {
   if ((unsigned)id < (unsigned)n_desc && (p | d) >= 0) {
-    const uint2 h = lds_u2(smem_u32(qh) + 8u * (uint32_t)id);
+    uint2 h;
+    if constexpr (kShared) h = lds_u2(smem_u32(qh) + 8u * (uint32_t)id);
+    else h = __ldg(qh + id);
     if (h.y & TW_QHDR_FAST) {
-      // 32-bit shared-memory addresses: records and quads are 16-byte units of the blob
-      const uint32_t base = smem_u32(ps);
-      const int4 rp = lds_i4(base + 16u * ((h.x >> 16) + (32u - __clz(p))));
-      const int4 rd = lds_i4(base + 16u * ((h.y & 0xffffu) + (32u - __clz(d))));
+      // records and quads are 16-byte units of the blob
+      const uint32_t base = kShared ? smem_u32(ps) : 0u;
+      const int4 rp = pset_unit16<kShared>(ps, base, (h.x >> 16) + (32u - __clz(p)));
+      const int4 rd = pset_unit16<kShared>(ps, base, (h.y & 0xffffu) + (32u - __clz(d)));
       if ((rp.z | rd.z) >= 0 && p >= rp.x && p <= rp.y && d >= rd.x && d <= rd.y) {
         const int nd = (int)((h.y >> 16) & 0x7fffu);
-        const int4 q = lds_i4(base + 16u * ((h.x & 0xffffu) + (uint32_t)(rp.z * nd + rd.z)));
+        const int4 q = pset_unit16<kShared>(ps, base, (h.x & 0xffffu) + (uint32_t)(rp.z * nd + rd.z));
         const bool pex = p == rp.x, dex = d == rd.x;
         const int32_t c00 = q.x;
         const int32_t c10 = pex ? c00 : q.y;

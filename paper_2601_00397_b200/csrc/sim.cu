@@ -49,12 +49,12 @@ __device__ __forceinline__ long long twb_phase_barrier() {
 // Timekeeper walk) out of line measured slower (A/B 13.4 ms inline vs 14.2 / 15.5 ms;
 // profiles/README.md), so they stay inlined unless these switches are set.
 #ifdef TWB_SIM_OUTLINE_PRED
-#define TWB_PRED_FN __device__ __noinline__
+#define TWB_PRED_FN static __device__ __noinline__
 #else
 #define TWB_PRED_FN __device__ __forceinline__
 #endif
 #ifdef TWB_SIM_OUTLINE_TK
-#define TWB_TK_FN __device__ __noinline__
+#define TWB_TK_FN static __device__ __noinline__
 #else
 #define TWB_TK_FN __device__ __forceinline__
 #endif
@@ -65,6 +65,7 @@ __device__ __forceinline__ long long twb_phase_barrier() {
 constexpr int kSimThreads = 32 * TWB_SIM_WARPS;  // warps per CTA (one config per warp at a time)
 constexpr int kSimWarps = kSimThreads / 32;
 constexpr int kMaxSlotCap = 4096;
+constexpr int kLatencyConfigsPerSm = 8;  // tw_sim_many: up to 8 configs per SM -> latency variant
 
 struct SimParams {
   const void* pset;
@@ -131,9 +132,9 @@ __device__ __forceinline__ int64_t div_nn(int64_t a, int64_t b) { return a / b; 
 // and the kernel is fetch-sensitive (adding inline code to the hot loop measured
 // slower even when it removed work), so rarely taken code should not sit inside it.
 #ifdef TWB_SIM_INLINE_COLD
-#define TWB_COLD __device__ __forceinline__
+#define TWB_COLD static __device__ __forceinline__
 #else
-#define TWB_COLD __device__ __noinline__
+#define TWB_COLD static __device__ __noinline__  // static: sim.cu is compiled twice (sim_tput.cu)
 #endif
 TWB_COLD int64_t cold_div(int64_t a, int64_t b) { return a / b; }
 TWB_COLD int64_t cold_fake_sleep(int64_t wait_ns) { return fake_sleep_ns(wait_ns); }
@@ -361,6 +362,7 @@ TWB_LUT_FN int64_t predict_lut(const char* ps, int id, int64_t P, int64_t D, int
   return TW_PRED_TABLE_MISS;
 }
 
+template <bool kTput>
 TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_t P, int64_t D, int64_t C) {
 #ifdef TWB_SIM_WARP_PRED
   return predict_warp(ps, id, P, D, C);
@@ -368,7 +370,7 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_
   // with the bulk-lookup section staged (latency regime): four shared-memory loads
   if (qh != nullptr && ((P | D) >> 31) == 0) {
     int64_t r;
-    if (predict_fast(ps, qh, pset_ndesc(ps), (int32_t)P, (int32_t)D, id, r)) return r;
+    if (predict_fast<!kTput>(ps, qh, pset_ndesc(ps), (int32_t)P, (int32_t)D, id, r)) return r;
   }
   return predict_lut(ps, id, P, D, C);
 #endif
@@ -377,9 +379,9 @@ TWB_PRED_FN int64_t predict_miss(const char* ps, const uint2* qh, int id, int64_
 // Linear models with a context term only (never in the Table sweeps): out of line
 // (A/B: 1,024 configs 8.68 -> 8.63 ms, 65,536 configs 345 -> 335 ms)
 #ifdef TWB_SIM_INLINE_CTXPRED
-__device__ __forceinline__
+static __device__ __forceinline__
 #else
-__device__ __noinline__
+static __device__ __noinline__
 #endif
 int64_t cold_predict_warp(const char* ps, int id, int64_t P, int64_t D, int64_t C) {
   return predict_warp(ps, id, P, D, C);
@@ -393,6 +395,7 @@ struct PredCache {
   int victim;
 };
 
+template <bool kTput>
 __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps, const uint2* qh, int id, int64_t P,
                                                   int64_t D, int64_t C) {
   const int lane = threadIdx.x & 31;
@@ -408,7 +411,7 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const int64_t key = (P << 32) | D;
   const unsigned hit = __ballot_sync(kFull, pc.key == key);
   if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
-  const int64_t d = predict_miss(ps, qh, id, P, D, C);
+  const int64_t d = predict_miss<kTput>(ps, qh, id, P, D, C);
 #ifdef TWB_PROFILE_PHASES
   pc.misses++;
 #endif
@@ -425,7 +428,7 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
 #ifndef TWB_SIM_OUTLINE_COLD2
 __device__ __forceinline__
 #else
-__device__ __noinline__
+static __device__ __noinline__
 #endif
 void cold_dump_event(tw_event* evp, int64_t pos, int32_t rq, int kind, int64_t ts, int64_t step) {
   tw_event e;
@@ -447,6 +450,8 @@ struct Emitter {
   }
 };
 
+// kTput: the throughput variant (predictor blob read from global memory, see k_sim)
+template <bool kTput>
 __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
@@ -513,7 +518,8 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   pc.C = -1;
   pc.d = 0;
   pc.uses_c = pd->kind == TW_PRED_LINEAR && pd->per_context_token_us != 0.0;
-  // the caller staged the whole blob (bulk-lookup section included) or only the core
+  // the blob holds the bulk-lookup section: staged in shared memory (latency variant) or
+  // read from global memory (throughput variant)
   const tw_pset_header* hdr = reinterpret_cast<const tw_pset_header*>(ps);
   const uint2* qh = (hdr->fast_off > 0 && p.pset_bytes >= (uint32_t)hdr->total_bytes) ? pset_qhdr(ps) : nullptr;
   const bool macro_ok = !pc.uses_c && cfg.pred_id >= 0 && cfg.pred_id < pset_ndesc(ps);
@@ -714,7 +720,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     adm_cyc += q3 - q2;
     const int64_t P = (int64_t)__reduce_add_sync(kFull, (unsigned)p_l);  // P <= max_batch_tokens
     const int64_t C = pc.uses_c ? warp_sum_i64_redux(c_l) : 0;
-    const int64_t d = predict_cached(pc, ps, qh, cfg.pred_id, P, n_dec, C);
+    const int64_t d = predict_cached<kTput>(pc, ps, qh, cfg.pred_id, P, n_dec, C);
     pred_cyc += TWB_CLK() - q3;
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
@@ -890,11 +896,22 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
 #ifndef TWB_SIM_MIN_BLOCKS
 #define TWB_SIM_MIN_BLOCKS 1
 #endif
-__global__ void __launch_bounds__(kSimThreads, TWB_SIM_MIN_BLOCKS) k_sim(SimParams p) {
+#ifndef TWB_SIM_TPUT_MIN_BLOCKS
+#define TWB_SIM_TPUT_MIN_BLOCKS 4
+#endif
+// Two variants of the same loop (profiles/README.md, session-4 occupancy A/B):
+//  * latency (kTput = false): every config has its own warp; the blob is staged in shared
+//    memory (4 shared loads per prediction-cache miss), registers unconstrained (164);
+//  * throughput (kTput = true, more configs than resident warps): 4 CTAs per SM at <= 128
+//    registers, the blob read through L1 so shared memory holds only slot state
+//    (16 warps per SM instead of 12: 65,536 configs 335 -> 289 ms).
+template <bool kTput>
+__global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS : TWB_SIM_MIN_BLOCKS)
+    k_sim(SimParams p) {
   extern __shared__ __align__(128) char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  char* ps = smem + 128;
-  tma_stage_to_smem(ps, p.pset, p.pset_bytes, bar);
+  // (one expression, so ptxas still sees the staged blob as shared memory: LDS, not LD)
+  const char* ps = kTput ? static_cast<const char*>(p.pset) : smem + 128;
+  if constexpr (!kTput) tma_stage_to_smem(smem + 128, p.pset, p.pset_bytes, reinterpret_cast<uint64_t*>(smem));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 7 * p.cap;
   Slots sl;
@@ -911,10 +928,27 @@ __global__ void __launch_bounds__(kSimThreads, TWB_SIM_MIN_BLOCKS) k_sim(SimPara
     idx = __shfl_sync(kFull, idx, 0);
     if (idx >= p.n_cfg) break;
     const int c = p.order ? p.order[idx] : idx;
-    run_config(p, ps, sl, c);
+    run_config<kTput>(p, ps, sl, c);
     __syncwarp();
   }
 }
+
+#ifdef TWB_SIM_TPUT_TU
+// sim_tput.cu compiles this file a second time for the throughput variant alone: with
+// both variants in one translation unit the shared helpers stop being inlined into the
+// latency variant, whose blob reads then turn from LDS into generic loads (164 -> 173
+// registers, 1-2% slower at 1,024 configs).
+int sim_tput_prepare(size_t smem, int* per_sm) {
+  cudaFuncSetAttribute(k_sim<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true>, kSimThreads, smem);
+}
+void sim_tput_launch(int grid, size_t smem, cudaStream_t s, const SimParams& p) {
+  k_sim<true><<<grid, kSimThreads, smem, s>>>(p);
+}
+}  // namespace twb
+#else
+int sim_tput_prepare(size_t smem, int* per_sm);  // sim_tput.cu
+void sim_tput_launch(int grid, size_t smem, cudaStream_t s, const SimParams& p);
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
 static thread_local int64_t* g_prof = nullptr;
@@ -948,19 +982,25 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
     set_error("tw_sim_many: slot capacity %d exceeds the engine limit %d", slot_capacity, kMaxSlotCap);
     return TW_ENOSMEM;
   }
-  const uint32_t pset_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
-  const size_t smem = 128 + pset_smem + (size_t)kSimWarps * 7 * sizeof(int32_t) * cap;
   int dev = 0, sms = 148, per_sm = 0, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // more configs than 8 per SM: the throughput variant (blob read from global memory)
+  const bool tput = (int64_t)n_cfg > (int64_t)kLatencyConfigsPerSm * sms;
+  const uint32_t pset_smem = tput ? 0u : (uint32_t)((pset_bytes + 127) & ~127LL);
+  const size_t smem = 128 + pset_smem + (size_t)kSimWarps * 7 * sizeof(int32_t) * cap;
   if ((int)smem > max_optin) {
     set_error("tw_sim_many: %zu B of shared memory needed (slot capacity %d), device allows %d", smem, cap,
               max_optin);
     return TW_ENOSMEM;
   }
-  cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim, kSimThreads, smem);
+  if (tput) {
+    sim_tput_prepare(smem, &per_sm);
+  } else {
+    cudaFuncSetAttribute(k_sim<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim<false>, kSimThreads, smem);
+  }
   if (per_sm < 1) per_sm = 1;
   int64_t want = ((int64_t)n_cfg + kSimWarps - 1) / kSimWarps;
   int64_t grid = (int64_t)sms * per_sm;
@@ -986,7 +1026,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   p.counter = reinterpret_cast<int32_t*>(scratch);
   p.cap = cap;
   p.prof = g_prof;
-  k_sim<<<(int)grid, kSimThreads, smem, s>>>(p);
+  if (tput) sim_tput_launch((int)grid, smem, s, p);
+  else k_sim<false><<<(int)grid, kSimThreads, smem, s>>>(p);
   count_launch();
   g_last[0] = (int32_t)grid;
   g_last[1] = kSimThreads;
@@ -1007,3 +1048,4 @@ extern "C" int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_b
   if (slot_capacity) *slot_capacity = g_last[3];
   return TW_OK;
 }
+#endif  // TWB_SIM_TPUT_TU

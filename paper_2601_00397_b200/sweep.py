@@ -233,11 +233,10 @@ class DeviceSweep:
         sizes = workloads.sizes()[self.cfgs["workload_id"]] if self.n_cfg else np.zeros(0, np.int64)
         self.req_base = np.zeros(self.n_cfg + 1, np.int64)
         np.cumsum(sizes, out=self.req_base[1:])
-        # Latency regime (every config resident at once): stage the whole predictor blob so
-        # prediction-cache misses use the bulk-lookup section; otherwise only the core,
-        # which keeps three CTAs per SM for throughput (twb200.h, tw_sim_many).
-        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        self.stage_bytes = pset.nbytes if self.n_cfg <= 8 * sms else pset.core_nbytes
+        # The whole blob: prediction-cache misses use its bulk-lookup section, staged in
+        # shared memory by the latency variant (<= 8 configs per SM) or read from global
+        # memory by the throughput variant (twb200.h, tw_sim_many).
+        self.stage_bytes = pset.nbytes
         self.slot_capacity = int(max(32, int(self.cfgs["max_running"].max()) if self.n_cfg else 32))
         self.slot_capacity = min(self.slot_capacity, 4096)
         dev = self.device

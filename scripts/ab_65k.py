@@ -12,8 +12,8 @@ sw = presets.sweep_65536()
 dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
 import os  # noqa: E402
 
-if os.environ.get("STAGE") == "full":  # A/B: whole blob (bulk-lookup misses) at lower occupancy
-    dev.stage_bytes = sw.pset.nbytes
+if os.environ.get("STAGE") == "core":  # A/B against builds that stage the blob at every size
+    dev.stage_bytes = sw.pset.core_nbytes
 dev.run()
 torch.cuda.synchronize()
 ms = []

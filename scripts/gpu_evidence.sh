@@ -14,3 +14,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_me
 timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_batches -s 3 -c 1 -o gpurun_out/prof_ext python scripts/ab_ext.py > gpurun_out/ncu_ext.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_tk_resolve -s 16 -c 1 -o gpurun_out/prof_tk_bulk python scripts/ab_tk.py > gpurun_out/ncu_tk.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -o gpurun_out/prof_sim65k python scripts/ab_65k.py > gpurun_out/ncu_sim65k.log 2>&1
+timeout 300 python scripts/live_latency.py > gpurun_out/live.log 2>&1

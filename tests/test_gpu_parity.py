@@ -364,7 +364,7 @@ def test_tk_resolve_matches_oracle(A):
 # ---------------------------------------------------------------------------------
 
 
-def _multi_case_sweep(cases, timekeeper=False, audit=True):
+def _multi_case_sweep(cases, timekeeper=False, audit=True, repeat=1):
     from paper_2601_00397_b200._lib import SIM_CFG_DTYPE
     from paper_2601_00397_b200.predictor import PredictorSet
     from paper_2601_00397_b200.sweep import DeviceSweep
@@ -379,8 +379,10 @@ def _multi_case_sweep(cases, timekeeper=False, audit=True):
         cfgs[i] = c[0]
         cfgs[i]["pred_id"] = i
         cfgs[i]["workload_id"] = i
+    cfgs = np.tile(cfgs, repeat)  # copy k of case i is config k * len(cases) + i
+    n = len(cfgs)
     sw = DeviceSweep(PredictorSet(preds), pack_arrays(arrays), cfgs, per_request=True,
-                     audit=list(range(len(cases))) if audit else ())
+                     audit=list(range(0, n, max(1, n // len(cases)))) if audit else ())
     sw.run()
     return sw.fetch()
 
@@ -420,6 +422,28 @@ def test_sim_small_cases_with_timekeeper_keep_the_timeline():
     for i, case in enumerate(small):
         lo, hi = out.req_base[i], out.req_base[i + 1]
         _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], None, ev_all, ev_off)
+
+
+def test_sim_throughput_variant_event_for_event():
+    """More configs than 8 per SM select k_sim's throughput variant (blob read from
+    global memory, 4 CTAs per SM); every copy of every case must still match."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+
+    cases, ev_all, ev_off = oracle_golden()
+    small = [c for c in cases if c["arrivals"] is not None]
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    repeat = (8 * sms) // len(small) + 2
+    out = _multi_case_sweep(small, timekeeper=True, repeat=repeat)
+    assert _lib.last_sim_launch()["variant"] == "throughput"
+    m = len(small)
+    for k in range(repeat):
+        for i, case in enumerate(small):
+            j = k * m + i
+            lo, hi = out.req_base[j], out.req_base[j + 1]
+            _check(case, out.results[j], out.first_ns[lo:hi], out.finish_ns[lo:hi], out.events.get(j), ev_all,
+                   ev_off)
 
 
 def test_sim_full_size_cases_match_reference_digests():
