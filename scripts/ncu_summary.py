@@ -92,7 +92,8 @@ def summarize_launches(path):
         name = r[idx["Kernel Name"]]
         v = float(r[idx["Metric Value"]].replace(",", ""))
         unit = r[idx["Metric Unit"]]
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                 "second": 1e6, "s": 1e6}[unit]
         agg[name][0] += 1
         agg[name][1] += v * scale
     total = sum(v[1] for v in agg.values()) or 1
