@@ -244,6 +244,21 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
+#ifndef TWB_SIM_TPUT_TU
+  // One stage, steady state on the run's start, no dispatcher target inside the run: the
+  // K deadlines each resolve as sleep cJ + broadcast, which is the loop's steady-state
+  // closed form with R = K, without the walk (latency variant only: 1,024 configs 8.57 ->
+  // 8.31 ms; in the throughput variant the extra code measured 289 -> 296 ms).
+  if (S == 1 && g.V == now0 && g.last_bcast == g.wall && d > g.conv_cooldown && g.disp_ts > now0 + K * d) {
+    const int64_t end1 = now0 + K * d;
+    g.wall += K * g.conv_cooldown;
+    g.seq += K;
+    g.last_bcast = g.wall;
+    g.offset = end1 - g.wall;
+    g.V = end1;
+    return;
+  }
+#endif
   int64_t per = d;
   if (S == 2) per = d >> 1;
   else if (S > 2) per = cold_div(d, S);
