@@ -245,14 +245,16 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
                                        int S, int64_t now0, int64_t d, int64_t K) {
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
 #ifndef TWB_SIM_TPUT_TU
-  // One stage, steady state on the run's start, no dispatcher target inside the run: the
-  // K deadlines each resolve as sleep cJ + broadcast, which is the loop's steady-state
-  // closed form with R = K, without the walk (latency variant only: 1,024 configs 8.57 ->
-  // 8.31 ms; in the throughput variant the extra code measured 289 -> 296 ms).
-  if (S == 1 && g.V == now0 && g.last_bcast == g.wall && d > g.conv_cooldown && g.disp_ts > now0 + K * d) {
-    const int64_t end1 = now0 + K * d;
-    g.wall += K * g.conv_cooldown;
-    g.seq += K;
+  // One or two stages, steady state on the run's start (every stage gap > cJ), no
+  // dispatcher target inside the run: the K*S deadlines each resolve as sleep cJ +
+  // broadcast, which is the loop's steady-state closed form with R = K*S, without the
+  // walk (latency variant only: 1,024 configs 8.57 -> 8.31 ms for S = 1, 8.37 -> 8.08 ms
+  // with S = 2; in the throughput variant the extra code measured 289 -> 296 ms).
+  if (S <= 2 && g.V == now0 && g.last_bcast == g.wall && (S == 1 ? d : d >> 1) > g.conv_cooldown &&
+      g.disp_ts > now0 + K * d) {
+    const int64_t end1 = now0 + K * d, R = K * S;
+    g.wall += R * g.conv_cooldown;
+    g.seq += R;
     g.last_bcast = g.wall;
     g.offset = end1 - g.wall;
     g.V = end1;
