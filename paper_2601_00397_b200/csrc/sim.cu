@@ -211,6 +211,9 @@ struct TkGrid {
   int64_t disp_ts;
   int32_t disp;
   ArrWindow win;
+#ifdef TWB_PROFILE_PHASES
+  int64_t prof_calls, prof_fast, prof_loops;
+#endif
 };
 
 __device__ __forceinline__ void tk_resolve(TkGrid& g, int64_t t_min) {
@@ -244,6 +247,9 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
+#ifdef TWB_PROFILE_PHASES
+  g.prof_calls++;
+#endif
 #ifndef TWB_SIM_TPUT_TU
   // One or two stages, steady state on the run's start (every stage gap > cJ), no
   // dispatcher target inside the run: the K*S deadlines each resolve as sleep cJ +
@@ -258,6 +264,9 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
     g.last_bcast = g.wall;
     g.offset = end1 - g.wall;
     g.V = end1;
+#ifdef TWB_PROFILE_PHASES
+    g.prof_fast++;
+#endif
     return;
   }
 #endif
@@ -276,6 +285,9 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
   int64_t tgt = (S == 1) ? now0 + d : now0 + per;
   int64_t m_on = g.V == now0 ? 0 : -1;  // index of the deadline V sits on, or -1
   for (;;) {
+#ifdef TWB_PROFILE_PHASES
+    g.prof_loops++;
+#endif
     tk_dispatch(g, ts, n, epoch);
     if (g.V >= end_all) return;
     if (g.last_bcast == g.wall) {
@@ -551,6 +563,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   g.conv_cooldown = g.cooldown > 0 ? cold_fake_sleep(g.cooldown) : 0;
   g.rcp_cooldown = g.conv_cooldown > 0 ? __drcp_rn(__ll2double_rn(g.conv_cooldown)) : 0.0;
   g.disp = 0;
+#ifdef TWB_PROFILE_PHASES
+  g.prof_calls = g.prof_fast = g.prof_loops = 0;
+#endif
   g.win.load(ts, n, epoch, 0);
   g.disp_ts = n > 0 ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
 
@@ -906,6 +921,11 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       q[10] = pred_cyc;
       q[11] = apply_cyc;
       q[12] = pc.misses;
+#ifdef TWB_PROFILE_PHASES
+      q[13] = g.prof_calls;
+      q[14] = g.prof_fast;
+      q[15] = g.prof_loops;
+#endif
     }
   }
 }

@@ -22,7 +22,7 @@ ms = s.elapsed_time(e)
 _lib.load().tw_sim_set_profile(None)
 pr = prof.view(-1, 16).cpu().numpy()
 res = dev.fetch().results
-cyc, normal, runs, run_steps, tkc, evc, rounds, arc, plc, adc, prc, apc, misses = pr.T[:13]
+cyc, normal, runs, run_steps, tkc, evc, rounds, arc, plc, adc, prc, apc, misses, tcalls, tfast, tloops = pr.T[:16]
 order = np.argsort(-cyc)
 print(f"kernel {ms:.2f} ms; max config {cyc.max()/1.965e6:.2f} ms @1.965GHz, median {np.median(cyc)/1.965e6:.2f} ms")
 print(f"steps total {res['steps'].sum()}, normal {normal.sum()}, runs {runs.sum()}, run steps {run_steps.sum()}")
@@ -32,7 +32,7 @@ for c in order[:12]:
     print(c, f"{cyc[c]/1.965e6:.2f}ms", "steps", res['steps'][c], "normal", normal[c], "runs", runs[c], "runsteps", run_steps[c],
           f"tk {100*tkc[c]/cyc[c]:.0f}% ev {100*evc[c]/cyc[c]:.0f}% arr {100*arc[c]/cyc[c]:.0f}% plan {100*plc[c]/cyc[c]:.0f}% "
           f"adm {100*adc[c]/cyc[c]:.0f}% pred {100*prc[c]/cyc[c]:.0f}% apply {100*apc[c]/cyc[c]:.0f}% bcasts {rounds[c]} "
-          f"pred-misses {misses[c]}", lab)
+          f"pred-misses {misses[c]} tk calls/fast/loop-iters {tcalls[c]}/{tfast[c]}/{tloops[c]}", lab)
 # fit cycles ~ a*normal + b*runs + c*run_steps
 A = np.stack([normal, runs, run_steps], 1).astype(float)
 coef, *_ = np.linalg.lstsq(A, cyc.astype(float), rcond=None)
