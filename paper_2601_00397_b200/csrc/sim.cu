@@ -327,6 +327,11 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
           g.offset = tR - g.wall;
           g.V = tR;
           m_on = m_x;
+          // the walk resumes at deadline m_x + 1 (no catch-up through the skipped ones)
+          base = now0 + fx * d;
+          s = (int)(m_x - fx * S);
+          m_walk = m_x + 1;
+          tgt = (s == S - 1) ? base + d : base + per * (s + 1);
           continue;
         }
       }
