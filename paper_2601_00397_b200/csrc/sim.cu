@@ -637,7 +637,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     }
     // KV: free = cap - sum(_held) (oracle.py:122), only needed when a queue head is probed
     int64_t free0 = 0;
-    const bool need_free = waiting;
+    const bool need_free = waiting && n_act > 32;  // <= 32 active: summed in pass 1b below
     if (need_free) {
       int64_t held_l = 0;
 #pragma unroll 1
@@ -671,6 +671,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         if (n_act <= 32) {
           total_dec = __popc(dm);
           any_mid = __any_sync(kFull, mid);
+          if (waiting) {  // free KV blocks from this pass's loads (oracle.py:122)
+            const int32_t h0 = blk.ceil_div(pr), h1 = blk.ceil_div(dn + e);  // 0 for idle lanes
+            free0 = (int64_t)cfg.kv_capacity_blocks - warp_sum_i64_redux(h0 > h1 ? h0 : h1);
+          }
         }
         if (cfg.policy == TW_POLICY_PREFILL_PRIORITIZED) {  // oracle.py:168-178
           bool have_prefill = any_mid;
