@@ -275,5 +275,5 @@ def last_sim_launch() -> dict:
         "smem_bytes": vals[2].value,
         "slot_capacity": vals[3].value,
         # the throughput variant keeps only slot state in shared memory (twb200.h)
-        "variant": "throughput" if vals[2].value == 128 + 4 * 7 * 4 * vals[3].value else "latency",
+        "variant": "throughput" if vals[2].value == 128 + (vals[1].value // 32) * 7 * 4 * vals[3].value else "latency",
     }
