@@ -364,7 +364,7 @@ def test_tk_resolve_matches_oracle(A):
 # ---------------------------------------------------------------------------------
 
 
-def _multi_case_sweep(cases, timekeeper=False, audit=True, repeat=1):
+def _multi_case_sweep(cases, timekeeper=False, audit=True, repeat=1, core_only=False):
     from paper_2601_00397_b200._lib import SIM_CFG_DTYPE
     from paper_2601_00397_b200.predictor import PredictorSet
     from paper_2601_00397_b200.sweep import DeviceSweep
@@ -381,8 +381,11 @@ def _multi_case_sweep(cases, timekeeper=False, audit=True, repeat=1):
         cfgs[i]["workload_id"] = i
     cfgs = np.tile(cfgs, repeat)  # copy k of case i is config k * len(cases) + i
     n = len(cfgs)
-    sw = DeviceSweep(PredictorSet(preds), pack_arrays(arrays), cfgs, per_request=True,
+    pset = PredictorSet(preds)
+    sw = DeviceSweep(pset, pack_arrays(arrays), cfgs, per_request=True,
                      audit=list(range(0, n, max(1, n // len(cases)))) if audit else ())
+    if core_only:  # the caller passes only the blob's core: misses take the scalar LUT path
+        sw.stage_bytes = pset.core_nbytes
     sw.run()
     return sw.fetch()
 
@@ -409,6 +412,17 @@ def test_sim_small_cases_event_for_event():
     cases, ev_all, ev_off = oracle_golden()
     small = [c for c in cases if c["arrivals"] is not None]
     out = _multi_case_sweep(small)
+    for i, case in enumerate(small):
+        lo, hi = out.req_base[i], out.req_base[i + 1]
+        _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], out.events.get(i), ev_all, ev_off)
+
+
+def test_sim_small_cases_core_blob_only():
+    """pset_bytes = core_bytes (no bulk-lookup section): every prediction-cache miss takes
+    the scalar bit-length-LUT path; the event streams must not change."""
+    cases, ev_all, ev_off = oracle_golden()
+    small = [c for c in cases if c["arrivals"] is not None]
+    out = _multi_case_sweep(small, core_only=True)
     for i, case in enumerate(small):
         lo, hi = out.req_base[i], out.req_base[i + 1]
         _check(case, out.results[i], out.first_ns[lo:hi], out.finish_ns[lo:hi], out.events.get(i), ev_all, ev_off)
