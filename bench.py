@@ -381,7 +381,9 @@ def workload_generation(device, n_wl: int = 65536, n_req: int = 1000):
     del ts, pr, op
     return {"kernel": "k_generate_poisson", "workloads": n_wl, "requests": n_wl * n_req, "ms_per_launch": round(ms, 3),
             "requests_per_s": round(n_wl * n_req / (ms / 1e3), 1), "host_numpy_requests_per_s_one_core": round(host_rps, 1),
-            "matches_host": ok, "bound": "latency", "note": "one thread per workload runs its sequential PCG64 stream"}
+            "matches_host": ok, "bound": "latency",
+            "note": "one thread per workload runs its sequential PCG64 stream; outputs staged per warp and "
+                    "written as coalesced rows"}
 
 
 def metrics_roofline(dev, args, flush, stream, peak_gbs):

@@ -63,26 +63,6 @@ struct Pcg64 {
   }
 };
 
-struct ZigTables {
-  const uint64_t* ke;
-  const double* we;
-  const double* fe;
-};
-
-// random_standard_exponential (numpy distributions.c)
-__device__ double std_exponential(Pcg64& g, const ZigTables& z) {
-  for (;;) {
-    uint64_t ri = g.next64() >> 3;
-    const int idx = (int)(ri & 0xff);
-    ri >>= 8;
-    const double x = __dmul_rn((double)ri, z.we[idx]);
-    if (ri < z.ke[idx]) return x;  // 98.9% of draws
-    if (idx == 0) return __dsub_rn(kZigExpR, log1p(-g.next_double()));
-    const double u = g.next_double();
-    if (__dadd_rn(__dmul_rn(__dsub_rn(z.fe[idx - 1], z.fe[idx]), u), z.fe[idx]) < exp(-x)) return x;
-  }
-}
-
 // Generator.integers(low, high + 1): off + buffered_bounded_lemire_uint32(rng = high - low)
 __device__ __forceinline__ int32_t bounded(Pcg64& g, int32_t low, int32_t high) {
   const uint32_t rng = (uint32_t)((int64_t)high - (int64_t)low);
@@ -105,39 +85,96 @@ __device__ __forceinline__ int32_t sample_tokens(Pcg64& g, int32_t kind, int32_t
   return kind == TW_TOKENS_FIXED ? a : bounded(g, a, b);  // TokenDist.sample (workload.py:39-44)
 }
 
-__global__ void __launch_bounds__(kWlThreads) k_generate_poisson(const tw_wl_spec* __restrict__ specs,
-                                                                  int32_t n_wl, const int64_t* __restrict__ wl_off,
-                                                                  int64_t* __restrict__ offset_ns,
-                                                                  int32_t* __restrict__ prompt,
-                                                                  int32_t* __restrict__ output,
-                                                                  int32_t* __restrict__ status) {
-  __shared__ uint64_t ke[256];
-  __shared__ double we[256], fe[256];
+// Laid out for the memory system (profiles/README.md: 2.49 -> 0.85 ms for 65,536 x 1,000):
+//  * the ziggurat's (ke, we) pair is one 16-byte shared-memory record: one LDS.128 per
+//    draw instead of two randomly indexed LDS.64;
+//  * each warp generates its 32 workloads in blocks of 16 requests into a padded
+//    shared-memory tile, then writes every workload's block as one coalesced row
+//    (storing each draw directly touched 32 cache lines per instruction).
+struct ZigPair {
+  uint64_t ke;
+  double we;
+};
+
+// random_standard_exponential (numpy distributions.c)
+__device__ double std_exponential(Pcg64& g, const ZigPair* __restrict__ zp, const double* __restrict__ fe) {
+  for (;;) {
+    uint64_t ri = g.next64() >> 3;
+    const int idx = (int)(ri & 0xff);
+    ri >>= 8;
+    const ZigPair z = zp[idx];
+    const double x = __dmul_rn((double)ri, z.we);
+    if (ri < z.ke) return x;  // 98.9% of draws
+    if (idx == 0) return __dsub_rn(kZigExpR, log1p(-g.next_double()));
+    const double u = g.next_double();
+    if (__dadd_rn(__dmul_rn(__dsub_rn(fe[idx - 1], fe[idx]), u), fe[idx]) < exp(-x)) return x;
+  }
+}
+
+constexpr int kWlBlock = 16;  // requests per thread per staged block (41 KB of shared memory per CTA)
+__global__ void __launch_bounds__(kWlThreads) k_generate_poisson(
+    const tw_wl_spec* __restrict__ specs, int32_t n_wl, const int64_t* __restrict__ wl_off,
+    int64_t* __restrict__ offset_ns, int32_t* __restrict__ prompt, int32_t* __restrict__ output,
+    int32_t* __restrict__ status) {
+  __shared__ ZigPair zp[256];
+  __shared__ double fe[256];
+  __shared__ int64_t t_off[kWlThreads / 32][32][kWlBlock + 1];
+  __shared__ int32_t t_pr[kWlThreads / 32][32][kWlBlock + 1];
+  __shared__ int32_t t_op[kWlThreads / 32][32][kWlBlock + 1];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    ke[i] = kZigKe[i];
-    we[i] = kZigWe[i];
+    zp[i].ke = kZigKe[i];
+    zp[i].we = kZigWe[i];
     fe[i] = kZigFe[i];
   }
   __syncthreads();
-  const ZigTables z{ke, we, fe};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= n_wl) return;
-  const tw_wl_spec sp = specs[w];
+  const bool live = w < n_wl;
+  tw_wl_spec sp;
+  int64_t base = 0, n = 0;
+  if (live) {
+    sp = specs[w];
+    base = wl_off[w];
+    n = wl_off[w + 1] - base;
+  } else {
+    sp = specs[0];  // any valid spec; nothing is generated or stored
+  }
   Pcg64 g{sp.state_hi, sp.state_lo, sp.inc_hi, sp.inc_lo, sp.has_uint32 != 0, sp.uinteger};
-  const int64_t base = wl_off[w], n = wl_off[w + 1] - base;
+  int64_t nmax = n;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t v = __shfl_xor_sync(0xffffffffu, nmax, o);
+    nmax = v > nmax ? v : nmax;
+  }
   int64_t clock = 0;
   int32_t st = 0;
-  for (int64_t i = 0; i < n; i++) {
-    const double gap_s = __dmul_rn(sp.scale, std_exponential(g, z));
-    clock += __double2ll_rn(__dmul_rn(gap_s, 1e9));  // int(round(gap_s * NS_PER_S))
-    const int32_t p = sample_tokens(g, sp.prompt_kind, sp.prompt_a, sp.prompt_b);
-    const int32_t o = sample_tokens(g, sp.output_kind, sp.output_a, sp.output_b);
-    if ((p <= 0 || o <= 0) && st == 0) st = (int32_t)(i + 1);  // WorkloadError at request i
-    offset_ns[base + i] = clock;
-    prompt[base + i] = p;
-    output[base + i] = o;
+  for (int64_t b0 = 0; b0 < nmax; b0 += kWlBlock) {
+    const int cnt = (int)(n - b0 < kWlBlock ? (n - b0 > 0 ? n - b0 : 0) : kWlBlock);
+    for (int k = 0; k < cnt; k++) {
+      const double gap_s = __dmul_rn(sp.scale, std_exponential(g, zp, fe));
+      clock += __double2ll_rn(__dmul_rn(gap_s, 1e9));  // int(round(gap_s * NS_PER_S))
+      const int32_t p = sample_tokens(g, sp.prompt_kind, sp.prompt_a, sp.prompt_b);
+      const int32_t o = sample_tokens(g, sp.output_kind, sp.output_a, sp.output_b);
+      if ((p <= 0 || o <= 0) && st == 0) st = (int32_t)(b0 + k + 1);  // WorkloadError at request i
+      t_off[warp][lane][k] = clock;
+      t_pr[warp][lane][k] = p;
+      t_op[warp][lane][k] = o;
+    }
+    __syncwarp();
+    // rows r, r + 1 = the blocks of the warp's r-th and (r+1)-th workloads: half-warp h
+    // stores row r + h, lane j of it request j
+    const int h = lane >> 4, j = lane & 15;
+    for (int r = 0; r < 32; r += 2) {
+      const int64_t nr = __shfl_sync(0xffffffffu, n, r + h), br = __shfl_sync(0xffffffffu, base, r + h);
+      if (b0 + j < nr) {
+        offset_ns[br + b0 + j] = t_off[warp][r + h][j];
+        prompt[br + b0 + j] = t_pr[warp][r + h][j];
+        output[br + b0 + j] = t_op[warp][r + h][j];
+      }
+    }
+    __syncwarp();
   }
-  status[w] = st;
+  if (live) status[w] = st;
 }
 
 }  // namespace twb
