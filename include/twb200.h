@@ -295,7 +295,8 @@ typedef struct tw_event {
  * ev / ev_off (optional): audited configs get their full event stream in
  * ev[ev_off[c] .. ev_off[c+1]). slot_capacity: per-warp active-list capacity,
  * normally max(max_running) over the configs (configs above it finish with
- * TW_SIM_CAPACITY; at most 4096). scratch: >= 16 bytes of device memory, zeroed by
+ * TW_SIM_CAPACITY; at most 4096; capacities whose slot state does not fit 4 warps
+ * per CTA in shared memory run fewer warps per CTA). scratch: >= 16 bytes of device memory, zeroed by
  * the call (work counter).
  * Two variants of the same kernel, picked by n_cfg: up to 8 configs per SM (every
  * config resident on its own warp: latency-bound), each CTA stages pset_bytes of the

@@ -1007,17 +1007,17 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
 // both variants in one translation unit the shared helpers stop being inlined into the
 // latency variant, whose blob reads then turn from LDS into generic loads (164 -> 173
 // registers, 1-2% slower at 1,024 configs).
-int sim_tput_prepare(size_t smem, int* per_sm) {
+int sim_tput_prepare(int threads, size_t smem, int* per_sm) {
   cudaFuncSetAttribute(k_sim<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true>, kSimThreads, smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true>, threads, smem);
 }
-void sim_tput_launch(int grid, size_t smem, cudaStream_t s, const SimParams& p) {
-  k_sim<true><<<grid, kSimThreads, smem, s>>>(p);
+void sim_tput_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p) {
+  k_sim<true><<<grid, threads, smem, s>>>(p);
 }
 }  // namespace twb
 #else
-int sim_tput_prepare(size_t smem, int* per_sm);  // sim_tput.cu
-void sim_tput_launch(int grid, size_t smem, cudaStream_t s, const SimParams& p);
+int sim_tput_prepare(int threads, size_t smem, int* per_sm);  // sim_tput.cu
+void sim_tput_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
 static thread_local int64_t* g_prof = nullptr;
@@ -1058,20 +1058,25 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   // more configs than 8 per SM: the throughput variant (blob read from global memory)
   const bool tput = (int64_t)n_cfg > (int64_t)kLatencyConfigsPerSm * sms;
   const uint32_t pset_smem = tput ? 0u : (uint32_t)((pset_bytes + 127) & ~127LL);
-  const size_t smem = 128 + pset_smem + (size_t)kSimWarps * 7 * sizeof(int32_t) * cap;
+  // slot state is 7 int32 arrays of cap per warp: large capacities get fewer warps per CTA
+  const size_t per_warp = 7 * sizeof(int32_t) * (size_t)cap;
+  int warps = kSimWarps;
+  while (warps > 1 && 128 + pset_smem + warps * per_warp > (size_t)max_optin) warps--;
+  const int threads = 32 * warps;
+  const size_t smem = 128 + pset_smem + warps * per_warp;
   if ((int)smem > max_optin) {
     set_error("tw_sim_many: %zu B of shared memory needed (slot capacity %d), device allows %d", smem, cap,
               max_optin);
     return TW_ENOSMEM;
   }
   if (tput) {
-    sim_tput_prepare(smem, &per_sm);
+    sim_tput_prepare(threads, smem, &per_sm);
   } else {
     cudaFuncSetAttribute(k_sim<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim<false>, kSimThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim<false>, threads, smem);
   }
   if (per_sm < 1) per_sm = 1;
-  int64_t want = ((int64_t)n_cfg + kSimWarps - 1) / kSimWarps;
+  int64_t want = ((int64_t)n_cfg + warps - 1) / warps;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > want) grid = want;
   cudaMemsetAsync(scratch, 0, sizeof(int32_t), s);
@@ -1095,11 +1100,11 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   p.counter = reinterpret_cast<int32_t*>(scratch);
   p.cap = cap;
   p.prof = g_prof;
-  if (tput) sim_tput_launch((int)grid, smem, s, p);
-  else k_sim<false><<<(int)grid, kSimThreads, smem, s>>>(p);
+  if (tput) sim_tput_launch((int)grid, threads, smem, s, p);
+  else k_sim<false><<<(int)grid, threads, smem, s>>>(p);
   count_launch();
   g_last[0] = (int32_t)grid;
-  g_last[1] = kSimThreads;
+  g_last[1] = threads;
   g_last[2] = (int32_t)smem;
   g_last[3] = cap;
   return check_launch("tw_sim_many");

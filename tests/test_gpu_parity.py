@@ -520,6 +520,52 @@ def test_sim_huge_token_counts_equal_oracle():
         assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
 
 
+def test_sim_large_slot_capacity_equals_oracle():
+    """max_running up to 4096 (the engine limit): thousands of requests active at once
+    run through multi-pass warp loops, and the launch drops to fewer warps per CTA so
+    the slot state fits in shared memory."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.calibration import csv_path
+    from paper_2601_00397_b200.predictor import PredictorSet, TablePredictor
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SchedulingPolicy, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(23)
+    arrays, cfgs = [], []
+    for k, mr in enumerate([4096, 3000, 2048, 1500, 700]):
+        n = int(rng.integers(2500, 4500))
+        ts = np.sort(rng.integers(0, 200_000_000, n)).astype(np.int64)  # bursty: all arrive within 0.2 s
+        pr = rng.integers(16, 600, n).astype(np.int32)
+        op = rng.integers(1, 40, n).astype(np.int32)
+        arrays.append((ts, pr, op))
+        eng = EngineConfig(chunk_size=256, max_batch_tokens=65536, max_running=mr, kv_block_tokens=16,
+                           kv_capacity_blocks=int(rng.choice([40_000, 400_000])),
+                           policy=SchedulingPolicy.MIXED if k % 2 else SchedulingPolicy.PREFILL_PRIORITIZED)
+        cfgs.append(SweepConfig(engine=eng, pred_id=0, workload_id=k, timekeeper=bool(k % 2)))
+    wl = pack_arrays(arrays)
+    ca = config_array(cfgs)
+    pset = PredictorSet([TablePredictor.from_csv(csv_path("8b", 1, 1), allow_extrapolation=True)])
+    dev = DeviceSweep(pset, wl, ca, per_request=True)
+    dev.run()
+    out = dev.fetch()
+    launch = _lib.last_sim_launch()
+    assert launch["slot_capacity"] == 4096 and launch["block"] < 128, launch
+    peak = 0
+    for k in range(len(cfgs)):
+        ts, pr, op = wl.workload(k)
+        res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
+        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+            assert out.results[k][f] == res[f], (k, f)
+        lo, hi = out.req_base[k], out.req_base[k + 1]
+        assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
+        # requests in flight at the busiest moment: admitted before and finished after it
+        order = np.argsort(first)
+        peak = max(peak, int(np.max(np.searchsorted(np.sort(finish), first[order], side="right") * -1
+                                    + np.arange(1, len(first) + 1))))
+    assert peak > 1024, peak  # the large capacities were actually used
+
+
 def test_sweep_1024_equals_oracle_on_every_config():
     """BASELINE config 4 at full size: every record bit-identical to the C oracle."""
     from oracle import oracle as orc
