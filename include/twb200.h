@@ -300,9 +300,9 @@ typedef struct tw_event {
  * the call (work counter).
  * Two variants of the same kernel, picked by n_cfg: up to 8 configs per SM (every
  * config resident on its own warp: latency-bound), each CTA stages pset_bytes of the
- * blob in shared memory; above that (throughput-bound), the blob is read from global
- * memory so that shared memory holds only slot state and 4 CTAs of <= 128 registers
- * fit per SM. Results are identical. */
+ * blob in shared memory; above that (throughput-bound), or when the blob does not fit
+ * in shared memory, the blob is read from global memory so that shared memory holds
+ * only slot state and 4 CTAs of <= 128 registers fit per SM. Results are identical. */
 int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
                 int32_t n_cfg, const int32_t* order, const int64_t* wl_off,
                 const int64_t* req_offset_ns, const int32_t* req_prompt,

@@ -1055,11 +1055,14 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // more configs than 8 per SM: the throughput variant (blob read from global memory)
-  const bool tput = (int64_t)n_cfg > (int64_t)kLatencyConfigsPerSm * sms;
-  const uint32_t pset_smem = tput ? 0u : (uint32_t)((pset_bytes + 127) & ~127LL);
   // slot state is 7 int32 arrays of cap per warp: large capacities get fewer warps per CTA
   const size_t per_warp = 7 * sizeof(int32_t) * (size_t)cap;
+  // more configs than 8 per SM, or a blob too large to stage next to one warp's slot
+  // state: the throughput variant (blob read from global memory)
+  const uint32_t blob_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
+  const bool tput = (int64_t)n_cfg > (int64_t)kLatencyConfigsPerSm * sms ||
+                    128 + (size_t)blob_smem + per_warp > (size_t)max_optin;
+  const uint32_t pset_smem = tput ? 0u : blob_smem;
   int warps = kSimWarps;
   while (warps > 1 && 128 + pset_smem + warps * per_warp > (size_t)max_optin) warps--;
   const int threads = 32 * warps;

@@ -566,6 +566,51 @@ def test_sim_large_slot_capacity_equals_oracle():
     assert peak > 1024, peak  # the large capacities were actually used
 
 
+def test_sim_blob_larger_than_shared_memory_equals_oracle():
+    """A predictor set larger than a CTA's shared memory (48 irregular 24x24 tables with
+    holes, ~460 KB): even a handful of configs take the variant that reads the blob from
+    global memory; results equal the oracle's."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.predictor import PredictorSet, TablePredictor
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SchedulingPolicy, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(29)
+    preds = []
+    for _ in range(48):
+        pax = np.unique(np.concatenate([[0], rng.integers(1, 9000, 23)]))
+        dax = np.unique(np.concatenate([[0], rng.integers(1, 600, 23)]))
+        rows = {(int(p), int(d)): int(800 + 9 * p + 35 * d + rng.integers(0, 50))
+                for p in pax for d in dax if (p, d) != (0, 0) and rng.random() > 0.05}
+        preds.append(TablePredictor(rows, allow_extrapolation=True))
+    pset = PredictorSet(preds)
+    assert pset.nbytes > 232448, pset.nbytes
+    arrays, cfgs = [], []
+    for k in range(6):
+        n = int(rng.integers(100, 400))
+        ts = np.sort(rng.integers(0, 30_000_000_000, n)).astype(np.int64)
+        arrays.append((ts, rng.integers(16, 3000, n).astype(np.int32), rng.integers(1, 200, n).astype(np.int32)))
+        eng = EngineConfig(chunk_size=int(rng.choice([128, 512])), max_batch_tokens=4096, max_running=128,
+                           kv_block_tokens=16, kv_capacity_blocks=200_000,
+                           policy=SchedulingPolicy.MIXED if k % 2 else SchedulingPolicy.PREFILL_PRIORITIZED)
+        cfgs.append(SweepConfig(engine=eng, pred_id=int(rng.integers(0, 48)), workload_id=k, timekeeper=bool(k % 2)))
+    wl = pack_arrays(arrays)
+    ca = config_array(cfgs)
+    dev = DeviceSweep(pset, wl, ca, per_request=True)
+    dev.run()
+    out = dev.fetch()
+    assert _lib.last_sim_launch()["variant"] == "throughput"
+    for k in range(len(cfgs)):
+        ts, pr, op = wl.workload(k)
+        res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
+        assert res["status"] == 0
+        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+            assert out.results[k][f] == res[f], (k, f)
+        lo, hi = out.req_base[k], out.req_base[k + 1]
+        assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
+
+
 def test_sweep_1024_equals_oracle_on_every_config():
     """BASELINE config 4 at full size: every record bit-identical to the C oracle."""
     from oracle import oracle as orc
