@@ -99,6 +99,44 @@ def test_predict_features_random_tables_equals_oracle():
     assert bad.size == 0, [(int(ids[i]), int(P[i]), int(D[i]), int(got[i]), int(want[i])) for i in bad[:5]]
 
 
+def test_bulk_predictors_with_blob_larger_than_shared_memory():
+    """A 367 KB predictor set cannot be staged: both bulk kernels read it through L1 and
+    must still equal the oracle (features) and the staged path's semantics (CSR)."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import PredictorSet, TablePredictor
+
+    rng = np.random.default_rng(29)
+    preds = []
+    for _ in range(48):
+        pax = np.unique(np.concatenate([[0], rng.integers(1, 9000, 23)]))
+        dax = np.unique(np.concatenate([[0], rng.integers(1, 600, 23)]))
+        rows = {(int(p), int(d)): int(800 + 9 * p + 35 * d + rng.integers(0, 50))
+                for p in pax for d in dax if (p, d) != (0, 0) and rng.random() > 0.05}
+        preds.append(TablePredictor(rows, allow_extrapolation=bool(rng.random() < 0.7)))
+    pset = PredictorSet(preds)
+    assert pset.nbytes > 232448
+    n = 200_003
+    P = rng.integers(0, 12000, n).astype(np.int32)
+    D = rng.integers(0, 700, n).astype(np.int32)
+    C = rng.integers(0, 1 << 20, n).astype(np.int64)
+    ids = rng.integers(-1, 49, n).astype(np.int32)
+    got = pset.predict_features(P, D, C, ids)
+    want = orc.predict_many(pset.blob, P, D, C, ids)
+    assert np.array_equal(np.asarray(got), want)
+    # CSR batches through the extraction kernel, against the features path
+    sizes = rng.integers(0, 9, 50_000)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    tok = np.where(rng.random(int(off[-1])) < 0.7, -1, rng.integers(1, 900, int(off[-1]))).astype(np.int32)
+    ctx = rng.integers(0, 4000, int(off[-1])).astype(np.int32)
+    bid = rng.integers(0, 48, len(sizes)).astype(np.int32)
+    out, feat = pset.predict_csr(off, tok, ctx, bid, return_features=True)
+    feat = np.asarray(feat).reshape(-1, 3)
+    assert np.array_equal(feat, np.asarray(orc.extract_features(off, tok, ctx)).reshape(-1, 3))
+    ref = orc.predict_many(pset.blob, feat[:, 0].astype(np.int32), feat[:, 1].astype(np.int32), feat[:, 2], bid)
+    nonempty = sizes > 0
+    assert np.array_equal(np.asarray(out)[nonempty], ref[nonempty])
+
+
 def test_live_single_batch_predict_equals_bulk_and_oracle():
     """predict(batch) (the live engine's per-step call, tw_predict_one_sync) equals the
     bulk kernels and the oracle on random batches of every predictor kind."""
