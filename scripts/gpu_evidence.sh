@@ -16,3 +16,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_pr
 timeout 600 ncu --set full --clock-control none -k regex:k_tk_resolve -s 16 -c 1 -o gpurun_out/prof_tk_bulk python scripts/ab_tk.py > gpurun_out/ncu_tk.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -o gpurun_out/prof_sim65k python scripts/ab_65k.py > gpurun_out/ncu_sim65k.log 2>&1
 timeout 300 python scripts/live_latency.py > gpurun_out/live.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_generate_poisson -s 2 -c 1 -o gpurun_out/prof_wl python scripts/ab_wl.py > gpurun_out/ncu_wl.log 2>&1
