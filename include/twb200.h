@@ -131,7 +131,9 @@ int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batc
  * tw_predict_batches). The call stages them in caller-owned pinned host memory
  * (io_bytes >= 8*n_slots + 8), which a one-warp kernel reads and answers in place
  * (zero-copy under UVA; dev_io is reserved), reading the predictor blob from global
- * memory; then it synchronizes `stream`. *out_ns receives ns or a TW_PRED_* code. */
+ * memory; the call then polls the answer word in the pinned buffer instead of
+ * synchronizing `stream` (which it does only if no answer arrives within 200 ms, to
+ * report the kernel's error). *out_ns receives ns or a TW_PRED_* code. */
 int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const int32_t* host_slots,
                         int32_t n_slots, int32_t desc_id, void* pinned_io, void* dev_io,
                         int64_t io_bytes, int64_t* out_ns, void* stream);

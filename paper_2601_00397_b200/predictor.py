@@ -152,8 +152,8 @@ class _DevicePredictor:
 
         The live engine calls this once per step (engine.py:684): one C call stages the
         slots in pinned memory, which a one-warp kernel reads and answers in place
-        (zero-copy), then synchronizes (~25 us on a B200 box, kernel launch + sync
-        bound). A process that only predicts can use the resident service instead
+        (zero-copy); the call polls the answer word (~22 us on a B200 box through
+        Python, launch-bound). A process that only predicts can use the resident service instead
         (``predictor_set.service()``, ~14 us, no launch on the round trip)."""
         code = self.predictor_set.live().predict_one(batch)
         if code < 0:
