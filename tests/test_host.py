@@ -311,3 +311,40 @@ def test_ziggurat_tables_and_numpy_draw_restatement():
             assert int(rng.integers(lo, hi + 1)) == integers_closed(g, lo, hi)
             n += 1
     assert n == 10_000
+
+
+def test_c_abi_rejects_bad_arguments_before_touching_the_device():
+    """The boundary's error behaviour (twb200.h): invalid pointers, sizes and blobs return
+    TW_EINVAL with a message naming the entry point, before any CUDA call (so this runs
+    without a GPU), and a zero-sized request is a successful no-op."""
+    import ctypes
+
+    from paper_2601_00397_b200 import _lib
+
+    lib = _lib.load()
+    V = ctypes.c_void_p
+    null = V(0)
+    blob = (ctypes.c_uint8 * 64)()  # 16-B aligned enough for the size check, but no valid header
+
+    def err():
+        return lib.tw_last_error().decode()
+
+    cases = [
+        ("tw_sim_many", lambda: lib.tw_sim_many(null, 0, null, 1, null, null, null, null, null, null, null, null,
+                                                 null, null, null, 256, null, null)),
+        ("tw_predict_features", lambda: lib.tw_predict_features(null, 64, null, null, null, null, 10, null, null)),
+        ("tw_predict_batches", lambda: lib.tw_predict_batches(ctypes.cast(blob, V), 64, null, null, null, null, 5,
+                                                               null, null, null)),
+        ("tw_metrics_many", lambda: lib.tw_metrics_many(null, 3, null, null, null, null, null, null, null, null,
+                                                         1000, null, null)),
+        ("tw_generate_poisson", lambda: lib.tw_generate_poisson(null, 4, null, null, null, null, null, null)),
+        ("tw_predict_one_sync", lambda: lib.tw_predict_one_sync(null, 64, null, 3, 0, null, null, 0, null, null)),
+    ]
+    for name, call in cases:
+        rc = call()
+        assert rc == _lib.TW_EINVAL, (name, rc, err())
+        msg = err()
+        assert msg and (name in msg or "pset" in msg), (name, msg)
+    # empty requests are no-ops that never reach the device
+    assert lib.tw_generate_poisson(null, 0, null, null, null, null, null, null) == _lib.TW_OK
+    assert lib.tw_metrics_many(null, 0, null, null, null, null, null, null, null, null, 1000, null, null) == _lib.TW_OK
