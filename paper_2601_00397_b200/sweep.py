@@ -273,7 +273,7 @@ class DeviceSweep:
 
     @property
     def h2d_bytes(self) -> int:
-        n = self.pset.core_nbytes + self.cfgs.nbytes + self.order.nbytes + self.workloads.nbytes
+        n = self.stage_bytes + self.cfgs.nbytes + self.order.nbytes + self.workloads.nbytes
         if self.per_request:
             n += self.req_base.nbytes
         return int(n)
