@@ -1,6 +1,6 @@
 """Run the REFERENCE's own predictor and oracle tests (pkg/tests/test_predictor.py,
 test_oracle.py) with its predictor classes and its event loop replaced by this engine's
-(GPU needed).
+and its Poisson workload generator replaced by the device one (GPU needed).
 
     python scripts/ref_tests_predictor.py --stage   # build container: copy the test file
     python scripts/ref_tests_predictor.py           # GPU box: run it
@@ -22,7 +22,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCRATCH = os.path.join(ROOT, ".reftests")
 REF_TESTS = "/root/reference/pkg/tests"
-FILES = ("test_predictor.py", "test_oracle.py", "_support.py")
+FILES = ("test_predictor.py", "test_oracle.py", "test_workload.py", "_support.py")
 
 CONFTEST = '''
 import os, sys
@@ -41,11 +41,32 @@ from paper_2601_00397_b200 import sweep as _sweep
 _ref_oracle.simulate = _sweep.simulate
 _ref_oracle.OracleStalled = _sweep.OracleStalled
 
+# generate_arrivals: Poisson draws on the GPU (k_generate_poisson); the shim returns the
+# host framework's Arrival objects and raises its WorkloadError, as a drop-in must
+import timewarp.workload as _ref_wl
+from paper_2601_00397_b200 import workload as _wl
+
+_ref_generate = _ref_wl.generate_arrivals
+
+
+def _generate_arrivals(spec):
+    if spec.source != "poisson":
+        return _ref_generate(spec)  # trace files: host parsing, not the device path
+    try:
+        arr = _wl.generate_arrivals_device(spec)
+    except _wl.WorkloadError as exc:
+        raise _ref_wl.WorkloadError(str(exc)) from None
+    return [_ref_wl.Arrival(a.request_id, a.offset_ns, a.prompt_tokens, a.output_tokens) for a in arr]
+
+
+_ref_wl.generate_arrivals = _generate_arrivals
+
 
 def pytest_report_header(config):
     import paper_2601_00397_b200._lib as lib
     return ("timewarp.predictor -> paper_2601_00397_b200.predictor (%s); timewarp.oracle.simulate -> "
-            "paper_2601_00397_b200.sweep.simulate; native: %s" % (", ".join(SWAPPED), lib.load()._name))
+            "paper_2601_00397_b200.sweep.simulate; timewarp.workload.generate_arrivals (poisson) -> "
+            "k_generate_poisson; native: %s" % (", ".join(SWAPPED), lib.load()._name))
 '''
 
 
