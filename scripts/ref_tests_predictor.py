@@ -1,5 +1,5 @@
-"""Run the REFERENCE's own predictor and oracle tests (pkg/tests/test_predictor.py,
-test_oracle.py) with its predictor classes and its event loop replaced by this engine's
+"""Run the REFERENCE's own predictor, oracle, workload and engine tests
+(pkg/tests/test_predictor.py, test_oracle.py, test_workload.py, test_engine.py) with its predictor classes and its event loop replaced by this engine's
 and its Poisson workload generator replaced by the device one (GPU needed).
 
     python scripts/ref_tests_predictor.py --stage   # build container: copy the test file
@@ -22,7 +22,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCRATCH = os.path.join(ROOT, ".reftests")
 REF_TESTS = "/root/reference/pkg/tests"
-FILES = ("test_predictor.py", "test_oracle.py", "test_workload.py", "_support.py")
+FILES = ("test_predictor.py", "test_oracle.py", "test_workload.py", "test_engine.py", "_support.py")
 
 CONFTEST = '''
 import os, sys
