@@ -1,8 +1,9 @@
 """Run the REFERENCE's own predictor, oracle, workload and engine tests
-(pkg/tests/test_predictor.py, test_oracle.py, test_workload.py, test_engine.py) with its predictor classes and its event loop replaced by this engine's
-and its Poisson workload generator replaced by the device one (GPU needed).
+(pkg/tests/test_predictor.py, test_oracle.py, test_workload.py, test_engine.py) with its
+predictor classes, its event loop and its Poisson workload generator replaced by this
+engine's (GPU needed).
 
-    python scripts/ref_tests_predictor.py --stage   # build container: copy the test file
+    python scripts/ref_tests_predictor.py --stage   # build container: copy the test files
     python scripts/ref_tests_predictor.py           # GPU box: run it
 
 --stage copies the reference's test files (and their _support.py) into .reftests/
