@@ -359,8 +359,8 @@ typedef struct tw_run_metrics {
  * of each request in the caller's arrival list, which sets the order of the
  * compensated TPOT sum; NULL = the engine's (stable-sorted) order, which is the
  * caller's order for sorted arrival lists such as generate_arrivals produces.
- * max_requests: an upper bound on any workload's size (sizes shared memory; at most
- * 16384). */
+ * max_requests: an upper bound on any workload's size (sizes shared memory: 8 bytes
+ * per request, so at most ~28,000 requests on a B200; larger gives TW_ENOSMEM). */
 int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off,
                     const int64_t* req_offset_ns, const int32_t* req_output,
                     const int64_t* req_base, const int64_t* req_first_ns,

@@ -27,7 +27,9 @@ namespace twb {
 #endif
 constexpr int kMetThreads = TWB_MET_THREADS;
 constexpr int kMetWarps = kMetThreads / 32;
-constexpr int kMetMaxRequests = 16384;
+// keys (8 B per request) fill the dynamic shared memory: the largest workload a summary
+// takes is (max opt-in shared memory - the kernel's static shared memory) / 8
+constexpr int kMetStaticSmem = 8192;
 
 // total-order key of a non-NaN double (negatives flipped, positives offset)
 __device__ __forceinline__ uint64_t dkey(double v) {
@@ -368,18 +370,23 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
     set_error("tw_metrics_many: bad arguments");
     return TW_EINVAL;
   }
-  if (max_requests < 0 || max_requests > kMetMaxRequests) {
-    set_error("tw_metrics_many: max_requests %d outside [0, %d]", max_requests, kMetMaxRequests);
-    return TW_ENOSMEM;
+  if (max_requests < 0) {
+    set_error("tw_metrics_many: max_requests %d < 0", max_requests);
+    return TW_EINVAL;
   }
   if (n_cfg == 0) return TW_OK;
-  int cap = 1;
-  while (cap < max_requests) cap <<= 1;
-  const size_t smem = (size_t)cap * sizeof(uint64_t);
-  cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per_sm = 1;
+  int dev = 0, sms = 148, per_sm = 1, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int limit = (max_optin - kMetStaticSmem) / (int)sizeof(uint64_t);
+  if (max_requests > limit) {
+    set_error("tw_metrics_many: max_requests %d above the %d requests shared memory holds", max_requests, limit);
+    return TW_ENOSMEM;
+  }
+  const int cap = max_requests > 0 ? max_requests : 1;  // selection needs no power-of-two padding
+  const size_t smem = (size_t)cap * sizeof(uint64_t);
+  cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_metrics, kMetThreads, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;

@@ -750,7 +750,7 @@ def test_device_metrics_match_reference_summaries():
 def test_device_metrics_edge_workloads():
     """Run summaries of degenerate workloads against the oracle: no requests, one
     request, every output a single token (no TPOT values), identical latencies
-    (percentile ties), a 16,384-request workload (largest supported), an epoch offset."""
+    (percentile ties), a 28,000-request workload (near the shared-memory limit), an epoch offset."""
     from oracle import oracle as orc
     from paper_2601_00397_b200.predictor import ConstantPredictor, PredictorSet
     from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SweepConfig, config_array
@@ -763,8 +763,8 @@ def test_device_metrics_edge_workloads():
         (np.sort(rng.integers(0, 10**9, 200)).astype(np.int64), rng.integers(1, 900, 200).astype(np.int32),
          np.ones(200, np.int32)),
         (np.zeros(64, np.int64), np.full(64, 128, np.int32), np.full(64, 3, np.int32)),
-        (np.sort(rng.integers(0, 10**12, 16384)).astype(np.int64), rng.integers(1, 600, 16384).astype(np.int32),
-         rng.integers(1, 40, 16384).astype(np.int32)),
+        (np.sort(rng.integers(0, 10**12, 28000)).astype(np.int64), rng.integers(1, 600, 28000).astype(np.int32),
+         rng.integers(1, 40, 28000).astype(np.int32)),
     ]
     eng = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
                        kv_capacity_blocks=1 << 20)
