@@ -28,6 +28,7 @@ from typing import Iterable, Sequence
 import numpy as np
 
 from . import _lib
+from ._host import host_bases
 from ._lib import (
     PRED_DESC_DTYPE,
     PSET_HEADER_DTYPE,
@@ -48,23 +49,27 @@ log = logging.getLogger(__name__)
 NS_PER_US = 1_000
 
 
-class PredictorError(Exception):
+def _host(name: str) -> tuple:
+    return host_bases("predictor", name)  # predictor.py:27-44
+
+
+class PredictorError(*(_host("PredictorError") or (Exception,))):
     pass
 
 
-class EmptyBatch(PredictorError):
+class EmptyBatch(PredictorError, *_host("EmptyBatch")):
     """Prediction requested for a batch with no work in it."""
 
 
-class NegativeDuration(PredictorError):
+class NegativeDuration(PredictorError, *_host("NegativeDuration")):
     """Model parameters produced a duration below zero."""
 
 
-class TableMiss(PredictorError):
+class TableMiss(PredictorError, *_host("TableMiss")):
     """Lookup key outside the calibrated range with extrapolation disabled."""
 
 
-class TableParseError(PredictorError):
+class TableParseError(PredictorError, *_host("TableParseError")):
     """Calibration file is malformed."""
 
 

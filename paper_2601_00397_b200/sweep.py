@@ -26,6 +26,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
+from ._host import host_bases
 from ._lib import (
     EVENT_DTYPE,
     RUN_METRICS_DTYPE,
@@ -64,7 +65,7 @@ class EngineError(Exception):
     pass
 
 
-class OracleStalled(Exception):
+class OracleStalled(*(host_bases("oracle", "OracleStalled") or (Exception,))):  # oracle.py:26
     """The simulated engine can never make progress again (oracle.py:26-27)."""
 
 

@@ -348,3 +348,27 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
     # empty requests are no-ops that never reach the device
     assert lib.tw_generate_poisson(null, 0, null, null, null, null, null, null) == _lib.TW_OK
     assert lib.tw_metrics_many(null, 0, null, null, null, null, null, null, null, null, 1000, null, null) == _lib.TW_OK
+
+
+def test_exceptions_derive_from_the_host_frameworks_when_present():
+    """With the reference package importable (baseline/_ref), host code that catches
+    timewarp's exception classes catches this engine's (drop-in error behaviour)."""
+    import subprocess
+    import sys
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "timewarp")):
+        pytest.skip("reference not installed under baseline/_ref")
+    code = (
+        "import timewarp.predictor as hp, timewarp.oracle as ho, timewarp.workload as hw\n"
+        "from paper_2601_00397_b200 import predictor as p, sweep as s, workload as w\n"
+        "pairs = [(p.PredictorError, hp.PredictorError), (p.EmptyBatch, hp.EmptyBatch),\n"
+        "         (p.NegativeDuration, hp.NegativeDuration), (p.TableMiss, hp.TableMiss),\n"
+        "         (p.TableParseError, hp.TableParseError), (p.TableMiss, hp.PredictorError),\n"
+        "         (s.OracleStalled, ho.OracleStalled), (w.WorkloadError, hw.WorkloadError),\n"
+        "         (w.TraceParseError, hw.TraceParseError), (w.TraceParseError, hw.WorkloadError)]\n"
+        "assert all(issubclass(a, b) for a, b in pairs)\n"
+        "try:\n    p.TablePredictor({})\nexcept hp.TableParseError:\n    print('ok')\n")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref, ROOT]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr[-2000:]
