@@ -180,9 +180,12 @@ def measured_issue(kernel: str):
     (profiles/traffic.json): issue-slot use and the dominant stall reasons."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh)[kernel].get("issue")
+            entry = json.load(fh)[kernel]
     except (OSError, KeyError, ValueError):
         return None
+    if "issue" in entry:
+        return entry["issue"]
+    return {k: v for k, v in entry.items() if k != "dram_bytes_per_launch"}
 
 
 def predictor_roofline(device, peak_gbs):
@@ -580,12 +583,13 @@ def main():
     achieved = alg_bytes / (ms / 1e3) / 1e9
     launch = _lib.last_sim_launch()
     roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 6), "traffic": measured_traffic("k_sim"),
+            "frac": round(achieved / peak_gbs, 6),
+            "traffic": measured_traffic("k_sim" if launch.get("variant") == "latency" else "k_sim_65536"),
             "algorithmic_bytes_per_launch": int(alg_bytes),
             "note": "serial per-config event loop: latency-bound (one warp per config), not HBM-bound; "
                     "see ns_per_step_per_config and latency_bound", "launch": launch,
             "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2),
-            "latency_bound": measured_issue("k_sim")}
+            "latency_bound": measured_issue("k_sim" if launch.get("variant") == "latency" else "k_sim_65536")}
 
     extra = {}
     if rank == 0:
