@@ -329,12 +329,25 @@ void pred_global_batches(int grid, size_t smem, cudaStream_t s, const void* pset
                          const int64_t* off, const int32_t* tok, const int32_t* ctx, const int32_t* id, int64_t nb,
                          int64_t* feat, int64_t* out);
 
+// One batch's features to ns for the single-batch paths: the bulk-lookup section read
+// through L1 (three dependent loads) when the blob carries it, else the scalar lookup.
+__device__ __forceinline__ int64_t predict_one_global(const char* pset, uint32_t pset_bytes, int32_t desc_id,
+                                                      int64_t Pt, int64_t Dn, int64_t Ct) {
+  const tw_pset_header* h = reinterpret_cast<const tw_pset_header*>(pset);
+  int64_t r;
+  if (h->fast_off > 0 && pset_bytes >= (uint32_t)h->total_bytes && ((Pt | Dn) >> 31) == 0 &&
+      predict_fast<false>(pset, pset_qhdr(pset), pset_ndesc(pset), (int32_t)Pt, (int32_t)Dn, desc_id, r))
+    return r;
+  return predict_scalar(pset, desc_id, Pt, Dn, Ct);
+}
+
 // Single-batch prediction for the live engine's per-step call (engine.py:684): one
 // warp sums the batch's slots (lane-strided, shuffle reduction) and lane 0 predicts
 // straight from the global predictor blob (L2-resident; no shared-memory staging for
 // one query).
 __global__ void __launch_bounds__(32) k_predict_single(const char* __restrict__ pset, const int32_t* __restrict__ io,
-                                                      int32_t n, int32_t desc_id, int64_t* __restrict__ out) {
+                                                      int32_t n, int32_t desc_id, int64_t* __restrict__ out,
+                                                      uint32_t pset_bytes) {
   const int lane = threadIdx.x;
   int64_t Pt = 0, Dn = 0, Ct = 0;
   for (int i = lane; i < n; i += 32) {
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(32) k_predict_single(const char* __restrict__ 
   Dn = warp_sum_i64(Dn);
   Ct = warp_sum_i64(Ct);
   if (lane == 0) {
-    const int64_t r = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(pset, desc_id, Pt, Dn, Ct);
+    const int64_t r = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_one_global(pset, pset_bytes, desc_id, Pt, Dn, Ct);
     // system-scope store: the host polls this word in pinned memory
     asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(out), "l"(r) : "memory");
   }
@@ -499,7 +512,7 @@ extern "C" int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const i
   *ans = INT64_MIN;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   k_predict_single<<<1, 32, 0, s>>>(static_cast<const char*>(pset), reinterpret_cast<const int32_t*>(h), n_slots,
-                                    desc_id, reinterpret_cast<int64_t*>(h + res));
+                                    desc_id, reinterpret_cast<int64_t*>(h + res), (uint32_t)pset_bytes);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) {
@@ -542,7 +555,8 @@ struct tw_service_mailbox {
   volatile int32_t slots[1];  // tok[n] then ctx[n]
 };
 
-__global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__ pset, tw_service_mailbox* mb) {
+__global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__ pset, uint32_t pset_bytes,
+                                                       tw_service_mailbox* mb) {
   const int lane = threadIdx.x;
   uint64_t seen = 0;
   for (;;) {
@@ -567,7 +581,7 @@ __global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__
     Dn = warp_sum_i64(Dn);
     Ct = warp_sum_i64(Ct);
     if (lane == 0) {
-      mb->result = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_scalar(pset, desc, Pt, Dn, Ct);
+      mb->result = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_one_global(pset, pset_bytes, desc, Pt, Dn, Ct);
       __threadfence_system();  // the result lands before the acknowledgement
       mb->ack = w;
     }
@@ -606,7 +620,7 @@ extern "C" int tw_service_start(const void* pset, int64_t pset_bytes, int32_t ma
   sv->seq = 0;
   sv->cap = max_slots;
   cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking);
-  k_predict_service<<<1, 32, 0, sv->stream>>>(static_cast<const char*>(pset), sv->dev);
+  k_predict_service<<<1, 32, 0, sv->stream>>>(static_cast<const char*>(pset), (uint32_t)pset_bytes, sv->dev);
   count_launch();
   const int rc = check_launch("tw_service_start");
   if (rc != TW_OK) {

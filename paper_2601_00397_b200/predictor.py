@@ -157,9 +157,9 @@ class _DevicePredictor:
 
         The live engine calls this once per step (engine.py:684): one C call stages the
         slots in pinned memory, which a one-warp kernel reads and answers in place
-        (zero-copy); the call polls the answer word (~22 us on a B200 box through
+        (zero-copy); the call polls the answer word (~20 us on a B200 box through
         Python, launch-bound). A process that only predicts can use the resident service instead
-        (``predictor_set.service()``, ~14 us, no launch on the round trip)."""
+        (``predictor_set.service()``, ~14.5 us, no launch on the round trip)."""
         code = self.predictor_set.live().predict_one(batch)
         if code < 0:
             raise_for_code(code, _describe(batch))
