@@ -684,7 +684,8 @@ class _LiveChannel:
     def _alloc(self, cap: int) -> None:
         self.cap = cap
         self.h = self._torch.empty(8 * cap + 16, dtype=self._torch.uint8, pin_memory=True)
-        self.buf = np.zeros(2 * cap, np.int32)
+        self.buf = (ctypes.c_int32 * (2 * cap))()  # tok[n] | ctx[n], filled by slice assignment
+        self.buf_addr = ctypes.addressof(self.buf)
 
     def predict_one(self, batch) -> int:
         from ._device import stream_handle
@@ -694,17 +695,11 @@ class _LiveChannel:
         if n > self.cap:
             self._alloc(max(2 * self.cap, n))
         buf = self.buf
-        i = 0
-        for c in chunks:
-            buf[i] = c.chunk_tokens
-            buf[n + i] = c.context_len_before
-            i += 1
-        for dslot in decodes:
-            buf[i] = -1
-            buf[n + i] = dslot.context_len
-            i += 1
+        # PrefillChunk -> its tokens, DecodeSlot -> -1; then the contexts (predictor.py:69-84)
+        buf[0:n] = [c.chunk_tokens for c in chunks] + [-1] * len(decodes)
+        buf[n : 2 * n] = [c.context_len_before for c in chunks] + [d.context_len for d in decodes]
         hp = self.h.data_ptr()
-        rc = self._fn(self.blob_ptr, self.pset.nbytes, buf.ctypes.data, n, 0, hp, hp, 8 * self.cap + 16,
+        rc = self._fn(self.blob_ptr, self.pset.nbytes, self.buf_addr, n, 0, hp, hp, 8 * self.cap + 16,
                       self._out_ref, stream_handle())
         _lib.check(rc, "tw_predict_one_sync")
         return int(self._out.value)
