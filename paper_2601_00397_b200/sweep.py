@@ -440,15 +440,23 @@ class HostSweep(DeviceSweep):
     """A sweep driven from HOST buffers: every ``run_from_host()`` copies the inputs
     from pinned host memory to HBM and runs the event-loop kernel, all stream-ordered.
     The result records and per-request stamps land in pinned host memory: with
-    ``zero_copy`` (default) the kernel stores them there directly over PCIe as it
-    produces them (host memory is device-addressable under UVA), so no copy follows
-    the kernel; otherwise they are copied back after it. This is the end-to-end path a
+    ``zero_copy`` (the default up to 256 MB of outputs) the kernel stores them there
+    directly over PCIe as it produces them (host memory is device-addressable under
+    UVA), so no copy follows the kernel; otherwise they are copied back after it. This is the end-to-end path a
     host caller pays for (bench.py ``e2e``)."""
 
-    def __init__(self, *args, zero_copy: bool = True, **kwargs) -> None:
+    # Zero-copy wins for small outputs (config 4, 16 MB of stamps: 7.98 vs 8.3 ms per step);
+    # for 1 GB of stamps (config 5) the kernel's scattered PCIe stores cost more than one
+    # bulk copy after it (316 vs 308-315 ms; scripts/ab_e2e65.py).
+    ZERO_COPY_MAX_BYTES = 256 << 20
+
+    def __init__(self, *args, zero_copy: bool | None = None, **kwargs) -> None:
         import torch
 
         super().__init__(*args, **kwargs)
+        if zero_copy is None:
+            out_bytes = self.d_res.numel() + (16 * int(self.req_base[-1]) if self.per_request else 0)
+            zero_copy = out_bytes <= self.ZERO_COPY_MAX_BYTES
         self.zero_copy = zero_copy
         self._pairs_in = []
         staged = self.d_pset[: self.stage_bytes]  # what the event loop reads of the blob
