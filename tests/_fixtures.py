@@ -46,10 +46,18 @@ def predictor_from_spec(s):
 
 
 @functools.lru_cache(maxsize=None)
-def barrier_golden():
-    z = _npz("barrier.npz")
+def barrier_golden(name: str = "barrier.npz"):
+    """barrier.npz: 1-5 actors (run_random_schedule); barrier_wide.npz: 6-32 clients."""
+    z = _npz(name)
     ops = z["ops"].view(TK_OP_DTYPE)
     return {k: z[k] for k in z.files if k != "ops"} | {"ops": ops}
+
+
+@functools.lru_cache(maxsize=None)
+def resolve_golden():
+    """Single resolve rounds at A = 9, 17, 32 computed by the reference BarrierCore._resolve."""
+    z = _npz("resolve_wide.npz")
+    return {A: {k: z[f"{k}{A}"] for k in ("pending", "elig", "in", "out", "flag")} for A in (9, 17, 32)}
 
 
 @functools.lru_cache(maxsize=None)

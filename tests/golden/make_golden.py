@@ -291,6 +291,35 @@ def scripted():
     return h, r
 
 
+def save_streams(streams, name):
+    """Pack recorded (harness, recorder, cooldown, suppress) streams into a barrier-format npz."""
+    ops, op_off, acks, ev, ev_off, fin, wall0, cool, sup = [], [0], [], [], [0], [], [], [], []
+    for h, r, c, s in streams:
+        ops.extend(r.ops)
+        acks.extend(r.acks)
+        op_off.append(len(ops))
+        evs = harness_events(h)
+        gids = iter(release_groups(r, h))
+        evs = [(k, next(gids) if k == 1 else a, b, w) for (k, a, b, w) in evs]
+        ev.extend(evs)
+        ev_off.append(len(ev))
+        fin.append((h.core.offset_ns, h.core.seq, h.clock.now_ns))
+        wall0.append(1_000_000_000)
+        cool.append(c)
+        sup.append(int(s))
+    op_arr = np.zeros(len(ops), TK_OP_DTYPE)
+    for i, (arg, t, cl, g) in enumerate(ops):
+        op_arr[i] = (arg, t, cl, g)
+    np.savez_compressed(
+        os.path.join(HERE, name),
+        ops=op_arr.view(np.uint8), op_off=np.asarray(op_off, np.int64), acks=np.asarray(acks, np.int32),
+        events=np.asarray(ev, np.int64).reshape(-1, 4), ev_off=np.asarray(ev_off, np.int64),
+        final=np.asarray(fin, np.int64), wall0=np.asarray(wall0, np.int64), cooldown=np.asarray(cool, np.int64),
+        suppress=np.asarray(sup, np.uint8),
+    )
+    return len(ops), len(ev)
+
+
 def make_barrier_golden():
     streams = []  # (h, rec, cooldown, suppress)
     orig_build = _support.CoreHarness.build
@@ -315,31 +344,228 @@ def make_barrier_golden():
     for h, r in scenario_streams():
         streams.append((h, r, h.core.cooldown_ns, h.core.suppress_broadcasts))
 
-    ops, op_off, acks, ev, ev_off, fin, wall0, cool, sup = [], [0], [], [], [0], [], [], [], []
-    for h, r, c, s in streams:
-        ops.extend(r.ops)
-        acks.extend(r.acks)
-        op_off.append(len(ops))
-        evs = harness_events(h)
-        gids = iter(release_groups(r, h))
-        evs = [(k, next(gids) if k == 1 else a, b, w) for (k, a, b, w) in evs]
-        ev.extend(evs)
-        ev_off.append(len(ev))
-        fin.append((h.core.offset_ns, h.core.seq, h.clock.now_ns))
-        wall0.append(1_000_000_000)
-        cool.append(c)
-        sup.append(int(s))
-    op_arr = np.zeros(len(ops), TK_OP_DTYPE)
-    for i, (arg, t, cl, g) in enumerate(ops):
-        op_arr[i] = (arg, t, cl, g)
-    np.savez_compressed(
-        os.path.join(HERE, "barrier.npz"),
-        ops=op_arr.view(np.uint8), op_off=np.asarray(op_off, np.int64), acks=np.asarray(acks, np.int32),
-        events=np.asarray(ev, np.int64).reshape(-1, 4), ev_off=np.asarray(ev_off, np.int64),
-        final=np.asarray(fin, np.int64), wall0=np.asarray(wall0, np.int64), cooldown=np.asarray(cool, np.int64),
-        suppress=np.asarray(sup, np.uint8),
-    )
-    print("barrier:", len(streams), "streams,", len(ops), "ops,", len(ev), "events")
+    n_ops, n_ev = save_streams(streams, "barrier.npz")
+    print("barrier:", len(streams), "streams,", n_ops, "ops,", n_ev, "events")
+
+
+# ------------------------------------------------------------------------------
+# BarrierCore at the actor counts the sweep configs use (6-32 clients)
+# ------------------------------------------------------------------------------
+
+WIDE_ACTORS = (6, 7, 8, 9, 9, 9, 12, 16, 17, 17, 17, 24, 31, 32, 32)
+WIDE_COOLDOWNS = (0, 1, 500_000, 500_000, 2_000_000, 123_000_000)
+
+
+def wide_schedule(seed, transcript=None):
+    """One CoreHarness-driven schedule with 6-32 clients (A up to 17 and beyond).
+
+    Unlike run_random_schedule (pkg/tests/_support.py:99, 1-5 actors), collectives here
+    are sized up to every live actor ("all-hands" groups that make the whole actor set
+    exempt one by one), actors jump while inside a group (exemption dropped,
+    timekeeper.py:213), deregister inside an open group (timekeeper.py:294-314), and the
+    error paths (observer jumps, non-positive targets, unknown ids, bad expected) are
+    interleaved with real traffic. Every message goes through the reference BarrierCore.
+    """
+    rng = random.Random(seed)
+    n_act = rng.choice(WIDE_ACTORS)
+    n_obs = 0 if n_act >= 32 else rng.randint(0, min(2, 32 - n_act))
+    cooldown = rng.choice(WIDE_COOLDOWNS)
+    suppress = rng.random() < 0.15
+    h = _support.CoreHarness.build(cooldown_ns=cooldown, suppress=suppress)
+    rec = Recorder(h)
+    if transcript is not None:
+        transcript(h, cooldown, suppress)
+    roles = ["A"] * n_act + ["O"] * n_obs
+    rng.shuffle(roles)
+    actors, observers = [], []
+    for r in roles:
+        (actors if r == "A" else observers).append(h.register_actor() if r == "A" else h.register_observer())
+    h.seal()
+    alive = list(actors)
+    targets = {}
+    groups = {}  # name -> expected size of the open round (None when closed)
+    members = {}  # name -> set of arrived ids
+
+    def fresh(cid):
+        targets[cid] = h.virtual_now() + rng.randint(1, rng.choice((50_000, 5_000_000, 50_000_000)))
+
+    def jump(cid):
+        if h.virtual_now() >= targets[cid]:
+            fresh(cid)
+        h.jump(cid, targets[cid])
+
+    def enter(cid, g, size):
+        ack = h.enter(cid, g, size)
+        if ack.error is None:
+            members.setdefault(g, set()).add(cid)
+            if len(members[g]) == size:
+                members[g] = set()
+                groups[g] = None
+        return ack
+
+    for cid in actors:
+        fresh(cid)
+    busy = lambda c: any(c in m for m in members.values())  # noqa: E731
+    for _ in range(rng.randint(10, 25) * n_act):
+        if not alive:
+            break
+        cid = rng.choice(alive)
+        roll = rng.random()
+        if roll < 0.50:
+            if not busy(cid) or rng.random() < 0.1:  # a jump from inside a group drops exemption
+                jump(cid)
+        elif roll < 0.58:
+            h.clock.advance(rng.choice((0, 1, rng.randint(1, 2_000_000))))
+        elif roll < 0.70:
+            g = f"g{rng.randint(0, 3)}"
+            if groups.get(g) is None:
+                groups[g] = rng.choice((len(alive), rng.randint(1, len(alive))))
+            size = groups[g] if rng.random() > 0.04 else groups[g] + 1  # occasional ExpectedMismatch
+            enter(cid, g, size)
+        elif roll < 0.73:
+            # all-hands collective: every live actor enters one by one, the rest keep jumping
+            g = "all"
+            if groups.get(g) is None and not members.get(g):
+                groups[g] = len(alive)
+                order = list(alive)
+                rng.shuffle(order)
+                for c in order:
+                    enter(c, g, groups[g])
+                    for o in rng.sample(alive, min(len(alive), 3)):
+                        if not busy(o):
+                            jump(o)
+        elif roll < 0.77 and len(alive) > 1:
+            h.deregister(cid)
+            alive.remove(cid)
+            targets.pop(cid, None)
+            for m in members.values():
+                m.discard(cid)
+        elif roll < 0.80:
+            pick = rng.randrange(6)
+            if pick == 0 and observers:
+                h.jump(rng.choice(observers), targets.get(cid, 5))
+            elif pick == 1:
+                h.jump(cid, rng.choice((0, -5)))
+            elif pick == 2:
+                h.jump(f"actor{40 + rng.randrange(9)}", 5)
+            elif pick == 3:
+                h.enter(cid, "bad", 0)
+            elif pick == 4 and len(actors) > len(alive):
+                h.jump(rng.choice([a for a in actors if a not in alive]), 5)
+            else:
+                h.deregister(rng.choice([a for a in actors if a not in alive] or [f"actor{50}"]))
+        else:
+            jump(cid)
+    for _ in range(12):  # drain: everyone outside a group jumps to its target
+        any_ = False
+        for cid in alive:
+            if not busy(cid) and h.virtual_now() < targets[cid]:
+                h.jump(cid, targets[cid])
+                any_ = True
+        if not any_:
+            break
+    return h, rec, cooldown, suppress
+
+
+def resolve_rounds(A, C, rng):
+    """Single resolve rounds for C Timekeepers of A actor slots, each computed by the
+    reference BarrierCore._try_resolve/_resolve (timekeeper.py:318-366) on a FakeClock.
+
+    Returns the bulk-resolve inputs (pending [C*A] with INT64_MAX = none, eligible
+    bitmasks, offset, seq, wall, last broadcast with INT64_MIN = None) and the reference's
+    outputs (broadcast flag 1 / silent 0 / unresolved -1, and the post-round state)."""
+    I64MAX, I64MIN = np.iinfo(np.int64).max, np.iinfo(np.int64).min
+    pend = np.full(C * A, I64MAX, np.int64)
+    elig = np.zeros(C, np.uint32)
+    st_in = np.zeros((C, 4), np.int64)
+    st_out = np.zeros((C, 4), np.int64)
+    flag = np.zeros(C, np.int8)
+    cool = 500_000
+    for c in range(C):
+        h = _support.CoreHarness.build(cooldown_ns=cool)
+        core = h.core
+        ids = [h.register_actor() for _ in range(A)]
+        core.sealed = True
+        mask = rng.getrandbits(A) if rng.random() < 0.6 else (1 << A) - 1
+        if mask == 0:
+            mask = 1 << rng.randrange(A)
+        kind = rng.random()
+        p_below = rng.choice((0.0, 0.0, 0.02, 0.2))
+        wall = 10**9 + rng.randint(0, 10**12)
+        h.clock.now_ns = wall
+        core.offset_ns = rng.choice((0, rng.randint(0, 10**9)))
+        core.seq = rng.randint(0, 1000)
+        core.last_broadcast_wall_ns = None if rng.random() < 0.3 else wall - rng.choice((0, 1, rng.randint(0, 10**6)))
+        for a, cid in enumerate(ids):
+            if not (mask >> a) & 1:
+                core.exempt.add(cid) if rng.random() < 0.5 else setattr(core.clients[cid], "active", False)
+                continue
+            if kind < 0.15 and rng.random() < 0.2:
+                continue  # round still open: unresolved
+            lo = wall - 10**6 if rng.random() < p_below else wall + 1
+            core.pending[cid] = rng.randint(max(1, lo), wall + rng.choice((1000, 10**6, 10**9)))
+        for a, cid in enumerate(ids):
+            if cid in core.pending:
+                pend[c * A + a] = core.pending[cid]
+        elig[c] = mask
+        last = core.last_broadcast_wall_ns
+        st_in[c] = (core.offset_ns, core.seq, wall, I64MIN if last is None else last)
+        seq0 = core.seq
+        n_pend = len(core.pending)
+        core._try_resolve()
+        resolved = n_pend and not core.pending
+        flag[c] = -1 if not resolved else (1 if core.seq > seq0 else 0)
+        last = core.last_broadcast_wall_ns
+        st_out[c] = (core.offset_ns, core.seq, h.clock.now_ns, I64MIN if last is None else last)
+    return pend, elig, st_in, st_out, flag
+
+
+def make_wide_golden():
+    streams, transcripts = [], []
+    for seed in range(360):
+        tr_hook = None
+        if seed < 120:
+            def tr_hook(h, cooldown, suppress):
+                tr = {"cooldown": cooldown, "suppress": suppress, "steps": []}
+                orig = h.core.handle
+
+                def handle(msg, reply=None):
+                    ack = orig(msg, reply)
+                    tr["steps"].append({"msg": msg_doc(msg), "ack": msg_doc(ack)})
+                    return ack
+
+                h.core.handle = handle
+                orig_adv = h.clock.advance
+
+                def advance(ns):
+                    orig_adv(ns)
+                    tr["steps"].append({"advance": int(ns)})
+
+                h.clock.advance = advance
+                transcripts.append((h, tr))
+        streams.append(wide_schedule(7_000 + seed, tr_hook))
+    n_ops, n_ev = save_streams(streams, "barrier_wide.npz")
+    acts = sorted({sum(1 for o in r.ops if o[1] == 0) for _, r, _, _ in streams})
+    print("barrier_wide:", len(streams), "streams,", n_ops, "ops,", n_ev, "events; actor counts", acts)
+    out = []
+    for h, tr in transcripts:
+        tr["records"] = h.records
+        tr["emitted"] = [msg_doc(m) for m in h.broadcasts]
+        tr["final"] = [h.core.offset_ns, h.core.seq, h.clock.now_ns]
+        out.append(tr)
+    import gzip
+
+    with open(os.path.join(HERE, "core_log_wide.json.gz"), "wb") as raw, \
+            gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as fh:  # mtime=0: byte-reproducible
+        fh.write(json.dumps(out, separators=(",", ":")).encode())
+    print("core_log_wide:", len(out), "transcripts,", sum(len(t["steps"]) for t in out), "messages")
+    rng = random.Random(20260217)
+    arrs = {}
+    for A in (9, 17, 32):
+        pend, elig, st_in, st_out, flag = resolve_rounds(A, 1500, rng)
+        arrs |= {f"pending{A}": pend, f"elig{A}": elig, f"in{A}": st_in, f"out{A}": st_out, f"flag{A}": flag}
+        print(f"resolve A={A}:", {k: int((flag == k).sum()) for k in (-1, 0, 1)})
+    np.savez_compressed(os.path.join(HERE, "resolve_wide.npz"), **arrs)
 
 
 # ------------------------------------------------------------------------------
@@ -786,8 +1012,9 @@ def make_core_golden():
         out.append(tr)
     import gzip
 
-    with gzip.open(os.path.join(HERE, "core_log.json.gz"), "wt") as fh:
-        json.dump(out, fh, separators=(",", ":"))
+    with open(os.path.join(HERE, "core_log.json.gz"), "wb") as raw, \
+            gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as fh:  # mtime=0: byte-reproducible
+        fh.write(json.dumps(out, separators=(",", ":")).encode())
     print("core_log:", len(out), "transcripts,", sum(len(t["steps"]) for t in out), "messages")
 
 
@@ -831,7 +1058,7 @@ def make_metrics_golden():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics", "core"}
+    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics", "core", "wide"}
     rng = np.random.default_rng(20260100397)
     if "predictor" in which:
         make_predictor_golden(rng)
@@ -847,3 +1074,5 @@ if __name__ == "__main__":
         make_metrics_golden()
     if "core" in which:
         make_core_golden()
+    if "wide" in which:
+        make_wide_golden()

@@ -39,8 +39,8 @@ def doc(m) -> dict:
     return d
 
 
-def transcripts():
-    with gzip.open(GOLDEN, "rt") as fh:
+def transcripts(path=GOLDEN):
+    with gzip.open(path, "rt") as fh:
         return json.load(fh)
 
 
@@ -79,6 +79,18 @@ def test_native_core_reproduces_reference_transcripts():
         assert [core.offset_ns, core.seq, clock.now_ns] == tr["final"], i
         n_msgs += len(tr["steps"])
     assert n_msgs > 10_000
+
+
+def test_native_core_reproduces_reference_transcripts_6_to_32_clients():
+    """120 wide schedules (make_golden.wide_schedule): 6-32 clients, all-hands collectives,
+    jumps from inside groups, deregisters in open groups, error paths."""
+    trs = transcripts(GOLDEN.replace("core_log", "core_log_wide"))
+    assert len(trs) == 120
+    for i, tr in enumerate(trs):
+        core, clock, records, emitted = replay(tr)
+        assert records == tr["records"], i
+        assert [doc(e) for e in emitted] == tr["emitted"], i
+        assert [core.offset_ns, core.seq, clock.now_ns] == tr["final"], i
 
 
 def test_native_core_state_views_and_stall_diagnostics():

@@ -13,6 +13,7 @@ import pytest
 
 from _fixtures import (
     barrier_golden,
+    resolve_golden,
     case_events,
     case_inputs,
     oracle_golden,
@@ -334,10 +335,11 @@ def test_reference_known_answers_through_drop_in_predict():
 # ---------------------------------------------------------------------------------
 
 
-def test_tk_replay_matches_reference_barriercore():
+@pytest.mark.parametrize("name", ["barrier.npz", "barrier_wide.npz"])
+def test_tk_replay_matches_reference_barriercore(name):
     from paper_2601_00397_b200.timekeeper import replay_arrays
 
-    g = barrier_golden()
+    g = barrier_golden(name)
     r = replay_arrays(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"])
     assert np.array_equal(r.acks, g["acks"])
     for s in range(len(g["op_off"]) - 1):
@@ -364,6 +366,25 @@ def test_tk_opstream_api_reproduces_two_round_example():
     r = replay_many([h])
     assert r.broadcast_sequence(0) == [(30 * MS, 1), (79_500_000, 2)]
     assert int(r.final[0]["wall_ns"]) == WALL0 + 20 * MS + 500_000
+
+
+@pytest.mark.parametrize("A", [9, 17, 32])
+def test_tk_resolve_matches_reference_resolve(A):
+    """k_tk_resolve_rows against rounds computed by the reference BarrierCore._resolve
+    (timekeeper.py:318-366) at the actor counts of configs 3-5 (TP4xPP2, TP8xPP2) and the limit."""
+    import torch
+
+    from paper_2601_00397_b200.timekeeper import resolve_round
+
+    g = resolve_golden()[A]
+    dv = [torch.from_numpy(g["pending"].copy()).cuda()] + [torch.from_numpy(g["in"][:, k].copy()).cuda()
+                                                           for k in range(4)]
+    flag = resolve_round(dv[0], torch.from_numpy(g["elig"].view(np.int32)).cuda(), A, 500_000, *dv[1:])
+    assert np.array_equal(flag.cpu().numpy(), g["flag"])
+    assert np.array_equal(np.stack([d.cpu().numpy() for d in dv[1:]], axis=1), g["out"])
+    pend = dv[0].cpu().numpy()
+    assert (pend[np.repeat(g["flag"] >= 0, A)] == np.iinfo(np.int64).max).all()
+    assert np.array_equal(pend[np.repeat(g["flag"] < 0, A)], g["pending"][np.repeat(g["flag"] < 0, A)])
 
 
 @pytest.mark.parametrize("A", [1, 2, 5, 9, 17, 32])

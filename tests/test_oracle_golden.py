@@ -18,6 +18,7 @@ import pytest
 from _fixtures import (
     GOLDEN,
     barrier_golden,
+    resolve_golden,
     case_events,
     case_inputs,
     oracle_golden,
@@ -47,8 +48,9 @@ def test_oracle_predictor_empty_batch_code():
     assert out.tolist() == [-1, -1]
 
 
-def test_oracle_barrier_replay_matches_reference():
-    g = barrier_golden()
+@pytest.mark.parametrize("name", ["barrier.npz", "barrier_wide.npz"])
+def test_oracle_barrier_replay_matches_reference(name):
+    g = barrier_golden(name)
     ack, events, fin = orc.tk_replay(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"])
     assert np.array_equal(ack, g["acks"])
     n = len(g["op_off"]) - 1
@@ -59,6 +61,16 @@ def test_oracle_barrier_replay_matches_reference():
         got4 = np.stack([got["kind"], got["offset_ns"], got["seq"], got["wall_ns"]], axis=1) if len(got) else np.zeros((0, 4))
         assert np.array_equal(got4, want), s
     assert np.array_equal(np.stack([fin["offset_ns"], fin["seq"], fin["wall_ns"]], axis=1), g["final"])
+
+
+@pytest.mark.parametrize("A", [9, 17, 32])
+def test_oracle_resolve_rounds_match_reference_resolve(A):
+    g = resolve_golden()[A]
+    st = [g["pending"].copy()] + [g["in"][:, k].copy() for k in range(4)]
+    flag = orc.tk_resolve(st[0], g["elig"], A, 500_000, st[1], st[2], st[3], st[4])
+    assert np.array_equal(flag, g["flag"])
+    assert np.array_equal(np.stack(st[1:], axis=1), g["out"])
+    assert (st[0][np.repeat(g["flag"] >= 0, A)] == np.iinfo(np.int64).max).all()
 
 
 def _check_case(case, res, first, finish, events, ev_all, ev_off):
