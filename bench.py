@@ -4,18 +4,22 @@
 Metric (BASELINE.json): "emulated virtual-sec/wall-sec over config sweep; batch
 predictions/sec @1/2/4/8 GPU". One step = one pass of the hot path over one batch
 of synthetic input = the full event loop (oracle.simulate semantics + Timekeeper
-actor grid) of every config in the sweep, in one persistent tw_sim_many launch.
+actor grid) of every config in the sweep, in one persistent tw_sim_many launch per GPU.
 
-Workload per rank (weak scaling): BASELINE config 4 — the 1,024-config grid
-(max_batch_tokens x chunk x max_running x (TP,PP) x policy) on Llama-3-8B tables,
-1,000 Poisson requests (qps 8); rank r uses workload seed 1 + r. `--sweep 65536`
-runs config 5 instead (65,536 configs sharded over the ranks, strong scaling).
+Workload (the same at every N, strong scaling): BASELINE config 5, the 65,536-config
+sweep (the config-4 grid x {Llama-3-8B, 70B} tables x 32 Poisson workload seeds),
+sharded over the N ranks by a cost-model LPT partition; at N > 1 the records of all
+ranks are merged with one NCCL all-gather inside the e2e window. At N = 1 the line also
+carries BASELINE config 4 (the 1,024-config sweep on one B200) as `config4`, and the
+projected N = 2/4/8 step times (each rank's shard timed alone on this GPU).
+`--sweep 1024` makes config 4 the headline instead (weak scaling, seed 1 + rank).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-value  = sum over all ranks' configs of virtual span / max-over-ranks device time
+value  = sum over all configs of virtual span / max-over-ranks device time per step
 e2e    = the same through the public host API (pinned host inputs -> H2D -> kernel ->
-         D2H of result records and per-request stamps), timed with CUDA events
+         result records and per-request stamps in pinned host memory -> at N > 1 the
+         NCCL gather + merge of all records), timed with CUDA events, max over ranks
 roofline / predictor_roofline / cpu_baseline: see DESIGN.md §Measurement.
 """
 
@@ -44,9 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--sweep", choices=("1024", "65536"), default="1024")
+    ap.add_argument("--sweep", choices=("1024", "65536"), default="65536")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-projection", action="store_true", help="skip the per-shard strong-scaling projection")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 block at N = 1")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--share-device", action="store_true",
                     help="all ranks on cuda:0 with gloo collectives: a one-GPU dry run of the multi-rank path")
@@ -83,7 +89,10 @@ def build_workload(args, world, rank):
     sw.n_global = len(full)
     config = {"workload": "BASELINE config 5: 65,536-config sweep sharded over GPUs (strong scaling)",
               "model": "Llama-3-8B/70B calibration tables (synthetic)", "configs_total": len(full),
-              "configs_this_rank": len(sw), "parallelism": f"configs sharded, dp{world}",
+              "configs_rank0": len(sw), "requests_per_config": 1000, "qps": 8, "workload_seeds": "1..32",
+              "grid": "mbt{1024..8192} x chunk{128..1024} x max_running{32..256} x (TP,PP) x 8 x policy x 2",
+              "timekeeper": "dispatcher + TP*PP workers, cooldown 500us",
+              "parallelism": f"configs sharded by cost-model LPT, dp{world}",
               "l2": "flushed (512 MiB write) between timed iterations"}
     return sw, config, "strong"
 
@@ -472,42 +481,164 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def init_dist(args, world):
+    """One process per GPU under torchrun (also at WORLD_SIZE 1, so a 1-rank NCCL run
+    exercises the same collective path); `--share-device` puts every rank on cuda:0 with
+    gloo collectives on host tensors (a one-GPU dry run of the multi-rank path)."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    on = "WORLD_SIZE" in os.environ
+    if not on:
+        return False, torch.device("cuda", 0), torch.device("cuda", 0)
+    if args.share_device:
+        dist.init_process_group("gloo")
+        return True, torch.device("cuda", 0), torch.device("cpu")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    return True, dev, dev
+
+
+def all_reduce(vals, op, cdev):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=op)
+    return [float(x) for x in t.cpu().tolist()]
+
+
+def ksim_profile(sw, device):
+    """Per-config cycles and loop iterations of one extra (untimed) launch with
+    tw_sim_set_profile: cycles per event-loop iteration, and the heaviest config."""
     import torch
 
     from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    d = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+    prof = torch.zeros(16 * len(sw), dtype=torch.int64, device=device)
+    _lib.load().tw_sim_set_profile(prof.data_ptr())
+    try:
+        d.run()
+        torch.cuda.synchronize(device)
+    finally:
+        _lib.load().tw_sim_set_profile(None)
+    pr = prof.view(-1, 16).cpu().numpy()
+    cyc, iters = pr[:, 0].astype(np.float64), (pr[:, 1] + pr[:, 2]).astype(np.float64)
+    del d
+    return cyc, iters
+
+
+def time_alone(sw, device, reps=3):
+    """Mean CUDA-event time of one sweep launched alone (L2 flushed between launches)."""
+    import torch
+
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    d = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    durs = time_kernel_steps(d.run, reps, 1, flush, torch.cuda.current_stream(device))
+    del d, flush
+    return sum(durs) / len(durs)
+
+
+def issue_roofline(kernel_key, ms, sm_mhz, sms, extra):
+    """Issue-slot roofline of the event loop: warp instructions per launch (ncu count of this
+    code version, profiles/traffic.json) / live launch time, against 4 schedulers x 1 issue
+    per cycle x SMs x the SM clock sampled during the timed region."""
+    issue = measured_issue(kernel_key) or {}
+    inst = issue.get("inst_executed")
+    clock = (sm_mhz or 1965.0) * 1e6
+    peak = sms * 4 * clock
+    out = {"bound": "issue", "unit": "warp-inst/s", "peak": round(peak, 1),
+           "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-inst/cycle x {clock / 1e6:.0f} MHz (sampled)"}
+    if inst:
+        ach = inst / (ms / 1e3)
+        out |= {"achieved": round(ach, 1), "frac": round(ach / peak, 4), "inst_per_launch": int(inst)}
+    out |= {k: v for k, v in issue.items() if k not in ("inst_executed",)}
+    return out | extra
+
+
+def ksim_roofline(sw, dev, ms, device, peak_gbs, sm_mhz, key, heavy_alone=True):
+    """The dominant kernel's line: the issue-slot roofline it is bound by, its HBM numbers
+    (tiny: the loop is not bandwidth-bound), cycles per loop iteration and the critical
+    chain (the heaviest config alone vs the whole sweep)."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+
+    launch = _lib.last_sim_launch()
+    n_req = int(dev.req_base[-1])
+    alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req + 16 * n_req
+                 + dev.stage_bytes * (launch["grid"] if launch["variant"] == "latency" else 1))
+    ach = alg_bytes / (ms / 1e3) / 1e9
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    cyc, iters = ksim_profile(sw, device)
+    heavy = int(np.argmax(cyc))
+    chain = {"heaviest_config": heavy, "heaviest_label": sw.configs[heavy].label,
+             "heaviest_cycles_in_sweep": int(cyc[heavy]), "sweep_ms": round(ms, 4)}
+    if heavy_alone:
+        chain["heaviest_alone_ms"] = round(time_alone(sw.subset([heavy]), device), 4)
+    extra = {
+        "kernel": "k_sim", "launch": launch, "traffic": measured_traffic(key),
+        "cycles_per_iteration": round(float(cyc.sum() / max(iters.sum(), 1)), 1),
+        "iterations_per_config_mean": round(float(iters.mean()), 1),
+        "critical_chain": chain,
+        "hbm": {"achieved": round(ach, 3), "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 6),
+                "algorithmic_bytes_per_launch": int(alg_bytes),
+                "note": "not the bound: configs are serial event loops whose state stays in registers, "
+                        "shared memory and L2"},
+    }
+    return issue_roofline(key, ms, sm_mhz, sms, extra)
+
+
+def scaling_projection(full, vsec, device, worlds=(2, 4, 8)):
+    """Strong scaling of config 5 projected from this GPU: every LPT shard rank r of N would
+    run (the same partition bench.py uses under torchrun), each timed ALONE here. Ranks
+    share nothing until the final records gather, so the N-GPU step time is the slowest
+    shard (plus the gather, measured at N > 1 in e2e)."""
+    from paper_2601_00397_b200.distributed import partition
+    from paper_2601_00397_b200.sweep import estimate_cost
+
+    cost = estimate_cost(full.pset, full.cfgs, full.workloads)
+    out = {"method": "each LPT shard of N timed alone on this B200 (CUDA events, mean of 3 after 1 warm-up)"}
+    for N in worlds:
+        shards = partition(cost, N)
+        ms = [time_alone(full.subset(s), device) for s in shards]
+        c = [float(cost[s].sum()) for s in shards]
+        out[f"N{N}"] = {"shard_ms": [round(x, 3) for x in ms], "ms_per_step": round(max(ms), 3),
+                        "value": round(vsec / (max(ms) / 1e3), 1),
+                        "predicted_cost_imbalance": round(max(c) / (sum(c) / N) - 1, 5),
+                        "measured_shard_imbalance": round(max(ms) / (sum(ms) / N) - 1, 4)}
+    return out
+
+
+def measure_sweep(sw, args, world, rank, device, cdev, dist_on, label):
+    """The timed step of one sweep: device-resident value (kernel only, CUDA events, L2
+    flushed) and e2e through the host API (H2D of inputs, kernel, outputs to pinned host
+    memory, and at N > 1 the NCCL all-gather + merge of every rank's records)."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.distributed import gather_records_device
     from paper_2601_00397_b200.sweep import DeviceSweep, HostSweep
 
-    world, rank, local = dist_env()
-    if world > 1:
+    MAX, SUM = None, None
+    if dist_on:
         import torch.distributed as dist
 
-        if args.share_device:
-            local = 0
-            dist.init_process_group("gloo")
-        else:
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(device)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "fallback": True}
-    peak_gbs = float(peaks["hbm_gbs"])
-
-    sw, config, scaling = build_workload(args, world, rank)
+        MAX, SUM = dist.ReduceOp.MAX, dist.ReduceOp.SUM
     dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
     stream = torch.cuda.current_stream(device)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
 
     def barrier():
-        if world > 1:
+        if dist_on:
             torch.distributed.barrier()
 
-    # ---- device-resident timed region
     barrier()
     torch.cuda.synchronize(device)
     launches0 = _lib.launch_count()
@@ -519,104 +650,113 @@ def main():
     ms = sum(durs) / len(durs)
     out = dev.fetch()
     if not (out.results["status"] == 0).all():
-        raise SystemExit(f"rank {rank}: {int((out.results['status'] != 0).sum())} configs did not finish OK")
-    vsec_local = out.virtual_seconds(sw.cfgs["epoch_ns"])
-    steps_local = out.predictions
+        raise SystemExit(f"rank {rank}: {int((out.results['status'] != 0).sum())} configs of {label} did not finish OK")
+    vsec, steps = out.virtual_seconds(sw.cfgs["epoch_ns"]), float(out.predictions)
     ms_max = ms
-    vsec, steps_total = vsec_local, steps_local
-    if world > 1:
-        import torch.distributed as dist
+    max_local = len(sw)
+    if dist_on:
+        ms_max, = all_reduce([ms], MAX, cdev)
+        vsec, steps = all_reduce([vsec, steps], SUM, cdev)
+        max_local = int(all_reduce([len(sw)], MAX, cdev)[0])
+    res = {"dev": dev, "out": out, "ms": ms, "ms_max": ms_max, "vsec": vsec, "steps": steps, "launches": launches,
+           "clocks": clk.summary(), "flush": flush}
+    if args.no_e2e:
+        res["e2e"] = None
+        return res
+    host = HostSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+    ids_dev = torch.from_numpy(np.asarray(sw.global_ids, np.int64)).to(cdev)
+    merged_host = torch.empty((sw.n_global, 8), dtype=torch.int64, pin_memory=True) if dist_on else None
+    e_durs = []
+    for i in range(args.warmup + args.steps):
+        flush_l2(flush)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        host.run_from_host()
+        if dist_on:  # the sweep's one collective: records of every rank, merged by config id
+            recs = host.d_res if cdev.type == "cuda" else host.d_res.cpu()
+            merged, _ = gather_records_device(ids_dev, recs, sw.n_global, max_local, cdev)
+            merged_host.copy_(merged, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        if i >= args.warmup:
+            e_durs.append(a.elapsed_time(b))
+    e_ms = sum(e_durs) / len(e_durs)
+    hr = host.host_results()
+    if not (hr == out.results).all() or not np.array_equal(host._pairs_out[2][1].numpy()[: n_req_e2e(host)],
+                                                              out.finish_ns):
+        raise SystemExit(f"rank {rank}: e2e host results differ from the device run")
+    d2h = host.d2h_bytes
+    if dist_on:
+        from paper_2601_00397_b200._lib import SIM_RESULT_DTYPE
 
-        cdev = "cpu" if args.share_device else device  # gloo collectives on host tensors
-        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-        s = torch.tensor([vsec_local, float(steps_local)], dtype=torch.float64, device=cdev)
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        vsec, steps_total = float(s[0].item()), float(s[1].item())
-        # merge the per-config records on every rank (the sweep's only collective)
-        from paper_2601_00397_b200.distributed import gather_results
+        m = merged_host.numpy().view(np.uint8).reshape(-1).view(SIM_RESULT_DTYPE)
+        if int((m["status"] == 0).sum()) != sw.n_global or int((m["steps"] > 0).sum()) != sw.n_global:
+            raise SystemExit(f"rank {rank}: merged records incomplete")
+        if not (m[sw.global_ids] == out.results).all():
+            raise SystemExit(f"rank {rank}: merged records differ from this rank's")
+        e_ms, = all_reduce([e_ms], MAX, cdev)
+        d2h += merged_host.numel() * 8
+        res["merged"] = m
+    res["e2e"] = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
+                  "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": int(d2h),
+                  "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps / (e_ms / 1e3), 1),
+                  "outputs": ("zero-copy: the kernel stores records and stamps into pinned host memory"
+                              if host.zero_copy else "records and stamps copied to pinned host memory after the kernel")
+                  + ("; then the NCCL all-gather of every rank's records and the merge by config id, on device, "
+                     "copied to host" if dist_on else "")}
+    del host
+    return res
 
-        n_local = torch.tensor([len(sw)], device=cdev)
-        dist.all_reduce(n_local, op=dist.ReduceOp.MAX)
-        # every rank ends with all records ordered by global config id
-        merged = gather_results(sw.global_ids, out.results, sw.n_global, int(n_local.item()), cdev)
-        assert int((merged["status"] == 0).sum()) == sw.n_global
 
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    world, rank, local = dist_env()
+    dist_on, device, cdev = init_dist(args, world)
+    torch.cuda.set_device(device)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "fallback": True}
+    peak_gbs = float(peaks["hbm_gbs"])
+
+    sw, config, scaling = build_workload(args, world, rank)
+    head = measure_sweep(sw, args, world, rank, device, cdev, dist_on, config["workload"])
+    ms_max, vsec, steps_total = head["ms_max"], head["vsec"], head["steps"]
     value = vsec / (ms_max / 1e3)
-    preds_per_s = steps_total / (ms_max / 1e3)
-
-    # ---- e2e through the public API with host buffers
-    e2e = None
-    if not args.no_e2e:
-        host = HostSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
-        e_durs = []
-        for i in range(args.warmup + args.steps):
-            flush_l2(flush)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            host.run_from_host()
-            b.record(stream)
-            b.synchronize()
-            if i >= args.warmup:
-                e_durs.append(a.elapsed_time(b))
-        e_ms = sum(e_durs) / len(e_durs)
-        # the records and stamps the kernel wrote into pinned host memory are the device run's
-        hr = host.host_results()
-        if not (hr == out.results).all() or not np.array_equal(host._pairs_out[2][1].numpy()[: n_req_e2e(host)],
-                                                                  out.finish_ns):
-            raise SystemExit(f"rank {rank}: e2e host results differ from the device run")
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device="cpu" if args.share_device else device)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
-               "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": host.d2h_bytes,
-               "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps_total / (e_ms / 1e3), 1),
-               "outputs": "zero-copy: the kernel stores records and stamps into pinned host memory"
-                          if host.zero_copy else "copied back after the kernel"}
-
-    # ---- roofline of the dominant kernel (k_sim): algorithmic bytes / device time
-    n_req = int(dev.req_base[-1])
-    alg_bytes = (sw.cfgs.nbytes + 64 * len(sw) + 16 * n_req  # configs in, records out, stamps out
-                 + 16 * n_req  # each config reads its workload (ts 8 + prompt 4 + output 4 B/request)
-                 + dev.stage_bytes * (_lib.last_sim_launch()["grid"]
-                                      if _lib.last_sim_launch()["variant"] == "latency" else 1))
-    achieved = alg_bytes / (ms / 1e3) / 1e9
-    launch = _lib.last_sim_launch()
-    roof = {"kernel": "k_sim", "bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 6),
-            "traffic": measured_traffic("k_sim" if launch.get("variant") == "latency" else "k_sim_65536"),
-            "algorithmic_bytes_per_launch": int(alg_bytes),
-            "note": "serial per-config event loop: latency-bound (one warp per config), not HBM-bound; "
-                    "see ns_per_step_per_config and latency_bound", "launch": launch,
-            "ns_per_step_per_config": round(ms * 1e6 / max(1.0, steps_local / len(sw)), 2),
-            "latency_bound": measured_issue("k_sim" if launch.get("variant") == "latency" else "k_sim_65536")}
+    key = "k_sim" if args.sweep == "1024" else "k_sim_65536"
+    roof = ksim_roofline(sw, head["dev"], head["ms"], device, peak_gbs, head["clocks"].get("sm_mhz"), key,
+                         heavy_alone=(rank == 0))
 
     extra = {}
+    solo = rank == 0 and world == 1
     if rank == 0:
+        flush = head["flush"]
+        stream = torch.cuda.current_stream(device)
+        for name, fn in (("predictor_roofline", lambda: predictor_roofline(device, peak_gbs)),
+                         ("extraction_roofline", lambda: extraction_roofline(device, peak_gbs)),
+                         ("timekeeper_roofline", lambda: timekeeper_roofline(device, peak_gbs)),
+                         ("workload_generation", lambda: workload_generation(device)),
+                         ("metrics_reduction", lambda: metrics_roofline(head["dev"], args, flush, stream, peak_gbs))):
+            try:
+                extra[name] = fn()
+            except Exception as exc:  # report, never hide
+                extra[name] = {"error": repr(exc)}
+    if solo and args.sweep == "65536" and not args.no_projection:
         try:
-            extra["predictor_roofline"] = predictor_roofline(device, peak_gbs)
-        except Exception as exc:  # report, never hide
-            extra["predictor_roofline"] = {"error": repr(exc)}
-        try:
-            extra["extraction_roofline"] = extraction_roofline(device, peak_gbs)
+            extra["scaling_projection"] = scaling_projection(sw, vsec, device)
         except Exception as exc:
-            extra["extraction_roofline"] = {"error": repr(exc)}
+            extra["scaling_projection"] = {"error": repr(exc)}
+    if solo and args.sweep == "65536" and not args.no_config4:
         try:
-            extra["timekeeper_roofline"] = timekeeper_roofline(device, peak_gbs)
+            extra["config4"] = config4_block(args, device, cdev, peak_gbs)
         except Exception as exc:
-            extra["timekeeper_roofline"] = {"error": repr(exc)}
-        try:
-            extra["workload_generation"] = workload_generation(device)
-        except Exception as exc:
-            extra["workload_generation"] = {"error": repr(exc)}
-        try:
-            extra["metrics_reduction"] = metrics_roofline(dev, args, flush, stream, peak_gbs)
-        except Exception as exc:
-            extra["metrics_reduction"] = {"error": repr(exc)}
+            extra["config4"] = {"error": repr(exc)}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if solo and not args.no_cpu_baseline:
         cpu = cpu_baseline(sw, args.cpu_budget_s, os.cpu_count() or 1)
 
     if rank == 0:
@@ -625,13 +765,29 @@ def main():
             "unit": "virtual-s/wall-s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "int64+f64", "data": "synthetic", "config": config,
-            "predictions_per_s": round(preds_per_s, 1), "predictions_per_step": int(steps_total),
-            "virtual_s_per_step": round(vsec, 3), "gpu_launches": int(launches), "clocks": clk.summary(),
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, **extra,
+            "steps_per_s": round(steps_total / (ms_max / 1e3), 1), "emulated_steps_per_step": int(steps_total),
+            "virtual_s_per_step": round(vsec, 3), "gpu_launches": int(head["launches"]), "clocks": head["clocks"],
+            "e2e": head["e2e"], "roofline": roof, "cpu_baseline": cpu, **extra,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         torch.distributed.destroy_process_group()
+
+
+def config4_block(args, device, cdev, peak_gbs):
+    """BASELINE config 4 (the 1,024-config sweep on one B200): the same measurements as
+    the headline at N = 1, reported beside it."""
+    from paper_2601_00397_b200 import presets
+
+    sw = presets.sweep_1024(model="8b", seed=1)
+    sw.global_ids = np.arange(len(sw), dtype=np.int64)
+    sw.n_global = len(sw)
+    r = measure_sweep(sw, args, 1, 0, device, cdev, False, "config 4")
+    roof = ksim_roofline(sw, r["dev"], r["ms"], device, peak_gbs, r["clocks"].get("sm_mhz"), "k_sim")
+    return {"workload": "BASELINE config 4: 1,024 configs (Llama-3-8B tables, 1,000 requests, qps 8, seed 1)",
+            "value": round(r["vsec"] / (r["ms_max"] / 1e3), 1), "unit": "virtual-s/wall-s",
+            "ms_per_step": round(r["ms_max"], 4), "steps_per_s": round(r["steps"] / (r["ms_max"] / 1e3), 1),
+            "e2e": r["e2e"], "roofline": roof, "clocks": r["clocks"]}
 
 
 if __name__ == "__main__":

@@ -500,8 +500,19 @@ int64_t tw_launch_count(void);
 
 /* ---- the event digest, shared by the CUDA path and the oracle ------------- */
 /* digest = sum over events k (0-based, emission order) of tw_event_hash(k, ...)
- * mod 2^64: position-bound, so any reordering, timestamp, step or kind change of
- * any event changes it (w.h.p.). req = index in the stable-sorted arrivals. */
+ * mod 2^64, with tw_event_hash = M(req, kind) * L(k, ts, step):
+ *   M = tw_mix64(req*C1 + kind*C2 + C3) | 1   (odd: a pseudo-random multiplier per
+ *       request and event kind; req = index in the stable-sorted arrivals)
+ *   L = k*A + ts*B + step*G + 1               (A, B, G odd)
+ * Position-bound (k), and every field change of one event changes the digest
+ * (M and the coefficients are odd, so M*coef*delta != 0 mod 2^64 for any
+ * delta != 0 mod 2^64); reorderings cancel only with probability ~2^-60.
+ * L is linear in (k, ts, step), so the OUTPUT_TOKEN events of a run of identical
+ * decode steps sum in closed form per request (tw_event_run_sum). */
+#define TW_DIGEST_VERSION 2
+#define TW_DIG_A 0x9E3779B97F4A7C15ULL
+#define TW_DIG_B 0xD6E8FEB86659FD93ULL
+#define TW_DIG_G 0xFF51AFD7ED558CCDULL
 #if defined(__CUDACC__)
 #define TW_HD __host__ __device__ __forceinline__
 #else
@@ -515,11 +526,23 @@ TW_HD uint64_t tw_mix64(uint64_t x) {
   x ^= x >> 31;
   return x;
 }
-TW_HD uint64_t tw_event_hash(uint64_t k, uint64_t req, uint64_t kind, int64_t ts,
-                             int64_t step) {
-  uint64_t a = k * 0x9E3779B97F4A7C15ULL + req * 0xC2B2AE3D27D4EB4FULL + kind;
-  uint64_t b = tw_mix64(a ^ (uint64_t)ts);
-  return tw_mix64(b + (uint64_t)step);
+TW_HD uint64_t tw_event_mult(uint64_t req, uint64_t kind) {
+  return tw_mix64(req * 0xC2B2AE3D27D4EB4FULL + kind * 0x165667B19E3779F9ULL + 0x27D4EB2F165667C5ULL) | 1ULL;
+}
+/* the step-uniform part of L: ts*B + step*G + 1 */
+TW_HD uint64_t tw_event_u(int64_t ts, int64_t step) {
+  return (uint64_t)ts * TW_DIG_B + (uint64_t)step * TW_DIG_G + 1ULL;
+}
+TW_HD uint64_t tw_event_hash(uint64_t k, uint64_t req, uint64_t kind, int64_t ts, int64_t step) {
+  return tw_event_mult(req, kind) * (k * TW_DIG_A + tw_event_u(ts, step));
+}
+/* sum of L over the m events k = k0 + (j-1)*stride, ts = ts0 + j*d, step = step0 + j
+ * (j = 1..m): one request's OUTPUT_TOKENs over m identical steps of duration d */
+TW_HD uint64_t tw_event_run_sum(uint64_t m, uint64_t k0, uint64_t stride, int64_t ts0, int64_t d, int64_t step0) {
+  const uint64_t t1 = (m & 1ULL) ? m * ((m + 1ULL) >> 1) : (m >> 1) * (m + 1ULL); /* sum j     */
+  const uint64_t t0 = t1 - m;                                                      /* sum j - 1 */
+  return m * (k0 * TW_DIG_A + tw_event_u(ts0, step0)) + TW_DIG_A * stride * t0 +
+         ((uint64_t)d * TW_DIG_B + TW_DIG_G) * t1;
 }
 
 #endif /* TWB200_H */

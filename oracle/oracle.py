@@ -190,10 +190,14 @@ def mix64(x: int) -> int:
     return x
 
 
+def event_mult(req: int, kind: int) -> int:
+    return mix64(req * 0xC2B2AE3D27D4EB4F + kind * 0x165667B19E3779F9 + 0x27D4EB2F165667C5) | 1
+
+
 def event_hash(k: int, req: int, kind: int, ts: int, step: int) -> int:
-    a = (k * 0x9E3779B97F4A7C15 + req * 0xC2B2AE3D27D4EB4F + kind) & M64
-    b = mix64(a ^ (ts & M64))
-    return mix64(b + (step & M64))
+    """twb200.h tw_event_hash (digest v2): M(req, kind) * (k*A + ts*B + step*G + 1) mod 2^64."""
+    L = k * 0x9E3779B97F4A7C15 + (ts & M64) * 0xD6E8FEB86659FD93 + (step & M64) * 0xFF51AFD7ED558CCD + 1
+    return (event_mult(req, kind) * L) & M64
 
 
 KIND_CODE = {"FIRST_TOKEN": 0, "OUTPUT_TOKEN": 1, "FINISHED": 2}

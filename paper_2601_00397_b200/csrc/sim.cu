@@ -23,7 +23,8 @@
 //    duration, so the run length is closed-form (min remaining outputs, first
 //    arrival crossing) and the run's K*D token events are hashed in parallel across
 //    the lanes instead of K serial plan/apply passes ("macro steps");
-//  * every token event is hashed into a position-bound digest (tw_event_hash) and
+//  * every token event is hashed into a position-bound digest (tw_event_hash, linear in
+//    position/time/step per request, so a run's body sums in closed form) and
 //    FIRST_TOKEN / FINISHED stamps are stored per request; full event dumps only
 //    for audited configs.
 #include "common.cuh"
@@ -505,6 +506,11 @@ struct Emitter {
     dig += tw_event_hash((uint64_t)pos, (uint64_t)rq, (uint64_t)kind, ts, step);
     if (evp && pos < ev_cap) cold_dump_event(evp, pos, rq, kind, ts, step);
   }
+  // u = tw_event_u(ts, step), the step-uniform part of the hash, computed once per step
+  __device__ __forceinline__ void event_u(int64_t pos, int32_t rq, int kind, uint64_t u, int64_t ts, int64_t step) {
+    dig += tw_event_mult((uint64_t)rq, (uint64_t)kind) * ((uint64_t)pos * TW_DIG_A + u);
+    if (evp && pos < ev_cap) cold_dump_event(evp, pos, rq, kind, ts, step);
+  }
 };
 
 // kTput: the throughput variant (predictor blob read from global memory, see k_sim)
@@ -824,15 +830,27 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int64_t body = (K - 1) * (int64_t)n_dec;
     if (body > 0) {
       const int D = n_dec;
-      const int q32 = 32 / D, r32 = 32 % D;
-      int64_t j = lane / D;
-      int i = lane - (int)j * D;
+      if (em.evp == nullptr) {
+        // digest v2 is linear in (position, ts, step) per request: decoder i's K-1 body
+        // events sum to M_i * (U + (K-1)*A*i) (twb200.h tw_event_run_sum), one term per
+        // decoder instead of one hash per event
+        const uint64_t m = (uint64_t)(K - 1);
+        const uint64_t U = tw_event_run_sum(m, (uint64_t)n_events, (uint64_t)D, now0, d, step0);
+        const uint64_t mA = m * TW_DIG_A;
+#pragma unroll 1
+        for (int i = lane; i < D; i += 32)
+          em.dig += tw_event_mult((uint64_t)sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN) * (U + mA * (uint64_t)i);
+      } else {  // audited config: every event is also dumped
+        const int q32 = 32 / D, r32 = 32 % D;
+        int64_t j = lane / D;
+        int i = lane - (int)j * D;
 #pragma unroll 1  // one copy of the event hash in the loop
-      for (int64_t e = lane; e < body; e += 32) {
-        em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
-        i += r32;
-        j += q32;
-        if (i >= D) { i -= D; j++; }
+        for (int64_t e = lane; e < body; e += 32) {
+          em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
+          i += r32;
+          j += q32;
+          if (i >= D) { i -= D; j++; }
+        }
       }
     }
     if (K >= 2) {
@@ -851,6 +869,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int chunk_ev_total = __reduce_add_sync(kFull, (unsigned)chunk_ev);
     int64_t pos_c = n_events + body, pos_d = pos_c + chunk_ev_total;
     int kept = 0;
+    const uint64_t u_now = tw_event_u(now, step);
 #pragma unroll 1
     for (int b = 0; b < n_tot; b += 32) {
       const int i = b + lane;
@@ -889,7 +908,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         const int64_t ps0 = is_chunk ? pos_c + __popc(c1 & lt) + __popc(c2 & lt)
                                      : pos_d + __popc(d1 & lt) + __popc(d2 & lt);
 #pragma unroll 1
-        for (int t = 0; t < nev; t++) em.event(ps0 + t, rq, t ? TW_EV_FINISHED : k0, now, step);
+        for (int t = 0; t < nev; t++) em.event_u(ps0 + t, rq, t ? TW_EV_FINISHED : k0, u_now, now, step);
         if (k0 == TW_EV_FIRST_TOKEN && em.first) em.first[rq] = now;
         if (nev == 2 && em.finish) em.finish[rq] = now;
       }

@@ -45,6 +45,30 @@ def records_to_tensor(ids: np.ndarray, results: np.ndarray, max_local: int, devi
     return torch.from_numpy(rows).to(device)
 
 
+def gather_records_device(ids_dev, records, n_total: int, max_local: int, device, group=None):
+    """The sweep's merge step, device-resident: all-gather every rank's (config id, 64-byte
+    record) rows with one collective (NCCL over NVLink between GPUs), then scatter them
+    into an [n_total, 8] int64 table ordered by config id on `device`. `records` is the
+    rank's raw record bytes (a device tensor, or pinned host memory when the kernel wrote
+    them zero-copy); stream-ordered, no host synchronisation. Returns (merged, rows)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = ids_dev.numel()
+    local = torch.full((max_local, 9), -1, dtype=torch.int64, device=device)
+    local[:n, 0] = ids_dev
+    rec = records[: n * SIM_RESULT_DTYPE.itemsize].view(torch.int64).view(n, 8)
+    local[:n, 1:].copy_(rec, non_blocking=True)
+    rows = torch.empty((world * max_local, 9), dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(rows, local, group=group)
+    # padding rows (id -1) land in a spare row n_total: no host sync for a boolean mask
+    idx = torch.where(rows[:, 0] >= 0, rows[:, 0], torch.full_like(rows[:, 0], n_total))
+    merged = torch.zeros((n_total + 1, 8), dtype=torch.int64, device=device)
+    merged.index_copy_(0, idx, rows[:, 1:])
+    return merged[:n_total], rows
+
+
 def gather_results(ids: np.ndarray, results: np.ndarray, n_total: int, max_local: int, device, group=None) -> np.ndarray:
     """All-gather every rank's records; returns the merged SIM_RESULT_DTYPE[n_total] on every rank."""
     import torch

@@ -20,6 +20,8 @@ pkg/src/timewarp/engine.py:46-133):
 from __future__ import annotations
 
 import enum
+import json
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -163,12 +165,17 @@ def as_device_predictor(p):
     raise TypeError(f"cannot run predictor {type(p).__name__} on the B200 engine")
 
 
-def estimate_cost(pset: PredictorSet, cfgs: np.ndarray, wl: PackedWorkloads) -> np.ndarray:
-    """Rough relative cost (~ steps) per config, for largest-first scheduling."""
-    tokens = np.zeros(wl.n_workloads, np.float64)
+COST_MODEL_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cost_model.json")
+
+
+def cost_features(pset: PredictorSet, cfgs: np.ndarray, wl: PackedWorkloads):
+    """Numeric per-config features of the event loop's cost (log scale where multiplicative)."""
+    out_tok = np.ones(wl.n_workloads, np.float64)
+    prm_tok = np.ones(wl.n_workloads, np.float64)
     for w in range(wl.n_workloads):
         lo, hi = int(wl.wl_off[w]), int(wl.wl_off[w + 1])
-        tokens[w] = float(wl.output[lo:hi].sum()) + 1.0
+        out_tok[w] = float(wl.output[lo:hi].astype(np.int64).sum()) + 1.0
+        prm_tok[w] = float(wl.prompt[lo:hi].astype(np.int64).sum()) + 1.0
     step_us = np.ones(len(pset.predictors))
     for i, p in enumerate(pset.predictors):
         if isinstance(p, ConstantPredictor):
@@ -176,10 +183,50 @@ def estimate_cost(pset: PredictorSet, cfgs: np.ndarray, wl: PackedWorkloads) -> 
         elif isinstance(p, LinearPredictor):
             step_us[i] = max(abs(p.base_us) + abs(p.per_decode_us), 1.0)
         else:
-            vals = list(p._rows.values())
-            step_us[i] = max(min(vals), 1)
+            step_us[i] = max(min(p._rows.values()), 1)
     pid = np.clip(cfgs["pred_id"], 0, len(step_us) - 1)
-    return tokens[cfgs["workload_id"]] / np.sqrt(step_us[pid])
+    wid = cfgs["workload_id"]
+    names = ["chunk", "mbt", "max_running", "tp", "pp", "policy", "step_us", "out_tokens", "prompt_tokens"]
+    F = np.stack([
+        np.log2(np.maximum(cfgs["chunk_size"], 1)), np.log2(np.maximum(cfgs["max_batch_tokens"], 1)),
+        np.log2(np.maximum(cfgs["max_running"], 1)), np.log2(np.maximum(cfgs["workers_per_replica"], 1)),
+        cfgs["pp_stages"].astype(np.float64), cfgs["policy"].astype(np.float64), np.log(step_us[pid]),
+        np.log(out_tok[wid]), np.log(prm_tok[wid]),
+    ], 1)
+    return names, F
+
+
+def cost_design(names, F):
+    """Design matrix of the cost model: 1, the features, and their pairwise products."""
+    cols, terms = [np.ones(len(F))], ["1"]
+    for i, a in enumerate(names):
+        cols.append(F[:, i])
+        terms.append(a)
+    for i in range(len(names)):
+        for j in range(i, len(names)):
+            cols.append(F[:, i] * F[:, j])
+            terms.append(f"{names[i]}*{names[j]}")
+    return np.stack(cols, 1), terms
+
+
+_COST_MODEL = None
+
+
+def estimate_cost(pset: PredictorSet, cfgs: np.ndarray, wl: PackedWorkloads) -> np.ndarray:
+    """Relative cost per config (~ device cycles), for the LPT shard partition and the
+    largest-first pull order: a log-linear model with pairwise terms fitted to measured
+    per-config cycles of config 5 (cost_model.json, refit by scripts/fit_cost.py)."""
+    global _COST_MODEL
+    if len(cfgs) == 0:
+        return np.zeros(0)
+    if _COST_MODEL is None:
+        with open(COST_MODEL_PATH) as fh:
+            _COST_MODEL = json.load(fh)
+    names, F = cost_features(pset, cfgs, wl)
+    if names != _COST_MODEL["features"]:
+        raise EngineError("cost_model.json was fitted on other features; rerun scripts/fit_cost.py")
+    X, _ = cost_design(names, F)
+    return np.exp(np.clip(X @ np.asarray(_COST_MODEL["coef"]), -700, 700))
 
 
 @dataclass
