@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-projection", action="store_true", help="skip the per-shard strong-scaling projection")
     ap.add_argument("--no-config4", action="store_true", help="skip the config-4 block at N = 1")
+    ap.add_argument("--no-configs13", action="store_true", help="skip the BASELINE configs 1-3 block at N = 1")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--share-device", action="store_true",
                     help="all ranks on cuda:0 with gloo collectives: a one-GPU dry run of the multi-rank path")
@@ -443,6 +444,124 @@ def cpu_baseline(sw, budget_s: float, n_threads: int):
     }
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _ref_simulate_one(job):
+    """One config through the UNMODIFIED reference (baseline/_ref: timewarp.oracle.simulate
+    with TablePredictor.from_csv, pkg/src/timewarp/oracle.py:49-114): virtual span, steps
+    (= predict calls) and the final timestamp, for the Python CPU baseline."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from timewarp import oracle as ref_oracle
+    from timewarp.engine import EngineConfig as RefEngineConfig
+    from timewarp.engine import SchedulingPolicy as RefPolicy
+    from timewarp.predictor import TablePredictor as RefTable
+    from timewarp.workload import Arrival as RefArrival
+
+    ts, prompt, output, eng, csv, epoch = job
+    arrivals = [RefArrival(f"r{i}", int(t), int(p), int(o)) for i, (t, p, o) in enumerate(zip(ts, prompt, output))]
+    cfg = RefEngineConfig(chunk_size=eng[0], policy=RefPolicy("mixed" if eng[7] == 0 else "prefill_prioritized"),
+                          max_batch_tokens=eng[1], max_running=eng[2], kv_block_tokens=eng[3],
+                          kv_capacity_blocks=eng[4], workers_per_replica=eng[5], pp_stages=eng[6])
+    pred = RefTable.from_csv(csv, allow_extrapolation=True)
+    calls = [0]
+    inner = pred.predict
+
+    def counting(batch, hw=None):
+        calls[0] += 1
+        return inner(batch, hw)
+
+    pred.predict = counting
+    events = ref_oracle.simulate(arrivals, cfg, pred, epoch_ns=epoch)
+    last = max(e["virtual_ts_ns"] for e in events if e["kind"] == "FINISHED")
+    return last - epoch, calls[0], last
+
+
+def _ref_jobs(sw, ids):
+    from paper_2601_00397_b200 import calibration
+
+    grid = [(m, tp, pp) for m in calibration.MODELS for tp, pp in calibration.TP_PP_GRID]
+    wl = sw.workloads
+    jobs = []
+    for c in ids:
+        cf = sw.cfgs[c]
+        lo, hi = int(wl.wl_off[cf["workload_id"]]), int(wl.wl_off[cf["workload_id"] + 1])
+        eng = tuple(int(cf[k]) for k in ("chunk_size", "max_batch_tokens", "max_running", "kv_block_tokens",
+                                           "kv_capacity_blocks", "workers_per_replica", "pp_stages", "policy"))
+        jobs.append((wl.offset_ns[lo:hi].tolist(), wl.prompt[lo:hi].tolist(), wl.output[lo:hi].tolist(), eng,
+                     calibration.csv_path(*grid[int(cf["pred_id"])]), int(cf["epoch_ns"])))
+    return jobs
+
+
+def cpu_baseline_python(sw, device_results, n_sample: int = 0):
+    """SURVEY §8d's CPU path: multiprocessing.Pool(os.cpu_count()) over the unmodified
+    reference's oracle.simulate (baseline/_ref) on an evenly spaced sample of the sweep
+    (both models), wall-clock timed; each config's span and step count are also checked
+    against this engine's device records."""
+    import multiprocessing as mp
+
+    if not os.path.isdir(os.path.join(REF_DIR, "timewarp")):
+        return {"unavailable": "baseline/_ref has no timewarp package"}
+    n = len(sw)
+    procs = os.cpu_count() or 1
+    ids = np.linspace(0, n - 1, min(n, n_sample or max(64, 8 * procs))).astype(np.int64)
+    jobs = _ref_jobs(sw, ids)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        out = pool.map(_ref_simulate_one, jobs, chunksize=1)
+    dt = time.perf_counter() - t0
+    span = np.array([o[0] for o in out], np.float64)
+    steps = np.array([o[1] for o in out], np.int64)
+    agree = bool(np.array_equal(steps, device_results["steps"][ids]) and
+                 np.array_equal(np.array([o[2] for o in out], np.int64), device_results["final_now_ns"][ids]))
+    return {"value": round(float(span.sum()) / 1e9 / dt, 2), "unit": "virtual-s/wall-s", "cores": procs,
+            "kind": "reference",
+            "sample": f"{len(ids)} of {n} configs (evenly spaced, both models), unmodified reference "
+                      f"timewarp.oracle.simulate + TablePredictor.from_csv (baseline/_ref), Pool({procs})",
+            "steps_per_s": round(float(steps.sum()) / dt, 1), "seconds": round(dt, 3),
+            "matches_device_records": agree}
+
+
+def configs_1_3(device):
+    """BASELINE configs 1-3 (single configurations) on the GPU (one tw_sim_many
+    launch each, CUDA events), beside the C port on one host thread and the unmodified
+    Python reference (one process)."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    out = {}
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    for name, mk in (("config1", presets.config1), ("config2", presets.config2), ("config3", presets.config3)):
+        sw = mk()
+        d = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+        durs = time_kernel_steps(d.run, 5, 2, flush, torch.cuda.current_stream(device))
+        ms = sum(durs) / len(durs)
+        r = d.fetch().results
+        vs = float(r["final_now_ns"][0] - sw.cfgs["epoch_ns"][0]) / 1e9
+        t0 = time.perf_counter()
+        cres, *_ = orc.sim_many(sw.pset.blob, sw.cfgs, sw.workloads.wl_off, sw.workloads.offset_ns,
+                                sw.workloads.prompt, sw.workloads.output, n_threads=1)
+        c_s = time.perf_counter() - t0
+        rec = {"label": sw.configs[0].label, "requests": int(sw.workloads.sizes()[0]), "steps": int(r["steps"][0]),
+               "virtual_s": round(vs, 3), "gpu_ms": round(ms, 4), "gpu_virtual_s_per_wall_s": round(vs / (ms / 1e3), 1),
+               "c_port_one_thread_ms": round(c_s * 1e3, 2), "c_port_matches": bool((cres == r).all())}
+        if os.path.isdir(os.path.join(REF_DIR, "timewarp")):
+            t0 = time.perf_counter()
+            span, calls, last = _ref_simulate_one(_ref_jobs(sw, [0])[0])
+            py_s = time.perf_counter() - t0
+            rec |= {"python_reference_ms": round(py_s * 1e3, 1),
+                    "python_reference_virtual_s_per_wall_s": round(span / 1e9 / py_s, 1),
+                    "python_reference_matches": bool(calls == int(r["steps"][0]) and last == int(r["final_now_ns"][0]))}
+        out[name] = rec
+        del d
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU implementation (C oracle port; the reference is pure Python
     and has no compiled path) on this box's host cores, same metric/config."""
@@ -755,9 +874,18 @@ def main():
             extra["config4"] = config4_block(args, device, cdev, peak_gbs)
         except Exception as exc:
             extra["config4"] = {"error": repr(exc)}
+    if solo and not args.no_configs13:
+        try:
+            extra["configs_1_3"] = configs_1_3(device)
+        except Exception as exc:
+            extra["configs_1_3"] = {"error": repr(exc)}
     cpu = None
     if solo and not args.no_cpu_baseline:
         cpu = cpu_baseline(sw, args.cpu_budget_s, os.cpu_count() or 1)
+        try:
+            cpu["python"] = cpu_baseline_python(sw, head["out"].results)
+        except Exception as exc:
+            cpu["python"] = {"error": repr(exc)}
 
     if rank == 0:
         line = {

@@ -30,19 +30,24 @@
 extern "C" {
 #endif
 
-#define TWB200_ABI_VERSION 1
+#define TWB200_ABI_VERSION 2 /* 2: tw_predict_one_sync lost dev_io; tw_core_abort / set_suppress; TW_PRED_NAN / OVERFLOW */
 
 /* ---- call status codes ---------------------------------------------------- */
 #define TW_OK 0
 #define TW_EINVAL 1    /* bad argument (null pointer, size, malformed blob) */
 #define TW_ECUDA 2     /* CUDA launch/runtime error */
 #define TW_ENOSMEM 3   /* predictor blob or per-warp state exceeds shared memory */
+#define TW_ECALLBACK 4 /* a host callback of the native BarrierCore failed (tw_core_abort) */
 
 /* ---- per-element prediction codes (negative int64 in out_ns) -------------- */
 #define TW_PRED_EMPTY_BATCH (-1)      /* predictor.py:95-97   EmptyBatch       */
 #define TW_PRED_NEGATIVE (-2)         /* predictor.py:143-145 NegativeDuration */
 #define TW_PRED_TABLE_MISS (-3)       /* predictor.py:240-242 TableMiss        */
 #define TW_PRED_BAD_DESC (-4)         /* desc_id out of range (host bug)       */
+#define TW_PRED_NAN (-5)              /* predictor.py:142 round(nan): ValueError */
+#define TW_PRED_OVERFLOW (-6)         /* round(+-inf): OverflowError; or a duration
+                                         beyond int64 ns (the reference returns a
+                                         Python int there: engine limit)          */
 
 /* ---- predictor set ("pset") blob ------------------------------------------ */
 /* One contiguous, 16-byte aligned byte blob holding every predictor a sweep uses:
@@ -130,13 +135,13 @@ int tw_predict_batches(const void* pset, int64_t pset_bytes, const int64_t* batc
  * host_slots holds int32 tok[n_slots] then int32 ctx[n_slots] (slot encoding as in
  * tw_predict_batches). The call stages them in caller-owned pinned host memory
  * (io_bytes >= 8*n_slots + 8), which a one-warp kernel reads and answers in place
- * (zero-copy under UVA; dev_io is reserved), reading the predictor blob from global
+ * (zero-copy under UVA), reading the predictor blob from global
  * memory; the call then polls the answer word in the pinned buffer instead of
  * synchronizing `stream` (which it does only if no answer arrives within 200 ms, to
  * report the kernel's error). *out_ns receives ns or a TW_PRED_* code. */
 int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const int32_t* host_slots,
-                        int32_t n_slots, int32_t desc_id, void* pinned_io, void* dev_io,
-                        int64_t io_bytes, int64_t* out_ns, void* stream);
+                        int32_t n_slots, int32_t desc_id, void* pinned_io, int64_t io_bytes,
+                        int64_t* out_ns, void* stream);
 
 /* Resident predictor service (the live engine's per-step predict(), engine.py:684):
  * tw_service_start launches one persistent warp on its own non-blocking stream that
@@ -455,6 +460,13 @@ int tw_core_free(tw_core* core);
  * are ack.error, not call failures); TW_EINVAL = MalformedBody. */
 int tw_core_handle(tw_core* core, const tw_core_msg* msg, tw_core_ack* ack);
 int tw_core_try_resolve(tw_core* core);
+/* From inside a clock / sleep / emit / log callback: the callback failed. The core
+ * unwinds as soon as the callback returns and the call in progress returns TW_ECALLBACK,
+ * keeping the state changed so far (as the reference core does when a callback raises). */
+int tw_core_abort(tw_core* core);
+/* BarrierCore.suppress_broadcasts is a plain attribute the reference re-reads on every
+ * resolve (timekeeper.py:351-363): this updates it on a live core. */
+int tw_core_set_suppress(tw_core* core, int32_t suppress_broadcasts);
 int tw_core_state(const tw_core* core, tw_core_state_t* st);
 /* flags: 1 active, 2 exempt, 4 has a pending target (pending_target) */
 int tw_core_client(const tw_core* core, int32_t idx, int32_t* role, int32_t* flags,

@@ -53,6 +53,13 @@ def ptr(t) -> int | None:
     return t.data_ptr()
 
 
+def on_stream(stream=None):
+    """Context that makes `stream` current (a no-op for None)."""
+    import contextlib
+
+    return contextlib.nullcontext() if stream is None else torch.cuda.stream(stream)
+
+
 def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream

@@ -16,11 +16,12 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libtwb200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # ---- status / code constants (twb200.h) ------------------------------------------
-TW_OK, TW_EINVAL, TW_ECUDA, TW_ENOSMEM = 0, 1, 2, 3
+TW_OK, TW_EINVAL, TW_ECUDA, TW_ENOSMEM, TW_ECALLBACK = 0, 1, 2, 3, 4
 TW_PRED_EMPTY_BATCH, TW_PRED_NEGATIVE, TW_PRED_TABLE_MISS, TW_PRED_BAD_DESC = -1, -2, -3, -4
+TW_PRED_NAN, TW_PRED_OVERFLOW = -5, -6
 TW_PSET_MAGIC = 0x54534550
 TW_PRED_CONSTANT, TW_PRED_LINEAR, TW_PRED_TABLE = 0, 1, 2
 TW_TABLE_HOLE = -1
@@ -185,6 +186,8 @@ EXPORTED_SYMBOLS = (
     "tw_core_free",
     "tw_core_handle",
     "tw_core_try_resolve",
+    "tw_core_abort",
+    "tw_core_set_suppress",
     "tw_core_state",
     "tw_core_client",
     "tw_core_group",
@@ -209,7 +212,7 @@ _I64 = ctypes.c_int64
 _SIGNATURES = {
     "tw_predict_features": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P]),
     "tw_predict_batches": (_I32, [_P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
-    "tw_predict_one_sync": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P, _I64, _P, _P]),
+    "tw_predict_one_sync": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _P]),
     "tw_service_start": (_I32, [_P, _I64, _I32, _P]),
     "tw_service_predict": (_I32, [_P, _P, _I32, _I32, _P]),
     "tw_service_stop": (_I32, [_P]),
@@ -239,7 +242,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or os.environ.get("TWB200_LIB") or LIB_PATH  # override for A/B builds
+        # TWB200_LIB swaps in an A/B build of the library (scripts/); honoured only with
+        # TWB200_ALLOW_LIB_OVERRIDE=1 so a stray variable cannot replace the product library
+        override = os.environ.get("TWB200_LIB") if os.environ.get("TWB200_ALLOW_LIB_OVERRIDE") == "1" else None
+        p = path or override or LIB_PATH
         if not os.path.exists(p):
             raise NativeLibraryMissing(
                 f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -154,8 +154,10 @@ def _bind(lib):
                                   ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
                                   ctypes.POINTER(ctypes.c_int32)]
+    lib.tw_core_abort.argtypes = [P]
+    lib.tw_core_set_suppress.argtypes = [P, ctypes.c_int32]
     for name in ("tw_core_new", "tw_core_free", "tw_core_handle", "tw_core_try_resolve", "tw_core_state",
-                 "tw_core_client", "tw_core_group"):
+                 "tw_core_client", "tw_core_group", "tw_core_abort", "tw_core_set_suppress"):
         getattr(lib, name).restype = ctypes.c_int32
     lib._tw_core_bound = True
     return lib
@@ -183,7 +185,9 @@ class NativeBarrierCore:
         if cooldown_ns < 0:
             raise ValueError(f"cooldown must be >= 0, got {cooldown_ns}")
         self.cooldown_ns = cooldown_ns
-        self.suppress_broadcasts = suppress_broadcasts
+        self._suppress = bool(suppress_broadcasts)
+        self._h = None
+        self._cb_exc = None  # exception raised by a host callback, re-raised after the native call
         self._emit = emit or (lambda msg: None)
         self._log = log_record
         self._clock = clock
@@ -203,10 +207,10 @@ class NativeBarrierCore:
         if sleep is None:
             self._sleep = time.sleep
         self._cb = (
-            _CLOCK() if native_clock else _CLOCK(lambda _u: int(self._clock())),  # NULL: native realtime
-            _SLEEP() if native_sleep else _SLEEP(lambda _u, s: self._sleep(s)),
-            _EMIT(self._on_emit),
-            _LOG(self._on_log) if log_record is not None else _LOG(),  # NULL: no records
+            _CLOCK() if native_clock else _CLOCK(self._guard(lambda _u: int(self._clock()), 0)),  # NULL: realtime
+            _SLEEP() if native_sleep else _SLEEP(self._guard(lambda _u, s: self._sleep(s), None)),
+            _EMIT(self._guard(self._on_emit, None)),
+            _LOG(self._guard(self._on_log, None)) if log_record is not None else _LOG(),  # NULL: no records
         )
         self._codes: dict = {}
         self._mbuf, self._abuf = _Msg(), _Ack()
@@ -224,6 +228,43 @@ class NativeBarrierCore:
             self._h = None
 
     # -- callbacks -----------------------------------------------------------
+    def _guard(self, fn, default):
+        """ctypes cannot propagate a Python exception through C: a failing callback stores
+        it and asks the core to unwind (tw_core_abort); the native call then returns
+        TW_ECALLBACK and _raise_callback re-raises it, as the reference core would."""
+
+        def tramp(*args):
+            try:
+                return fn(*args)
+            except BaseException as exc:  # noqa: BLE001 - re-raised after the native call
+                self._cb_exc = exc
+                self._lib.tw_core_abort(self._h)
+                return default
+
+        return tramp
+
+    def _raise_callback(self, rc: int) -> None:
+        # a registration the failing callback interrupted still created its client (the
+        # reference adds it before logging): adopt any client ids the core holds
+        n = int(self._state().n_clients)
+        for i in range(len(self._ids), n):
+            self._id_for(i, self._client_flags(i)[0])
+        exc, self._cb_exc = self._cb_exc, None
+        if exc is not None:
+            raise exc
+        _lib.check(rc, "tw_core callback")
+
+    @property
+    def suppress_broadcasts(self) -> bool:
+        return self._suppress
+
+    @suppress_broadcasts.setter
+    def suppress_broadcasts(self, value: bool) -> None:
+        """Re-read at every resolve by the reference (timekeeper.py:351-363): pushed to the core."""
+        self._suppress = bool(value)
+        if self._h is not None:
+            self._lib.tw_core_set_suppress(self._h, int(self._suppress))
+
     def _mk(self, name: str, **kw):
         return self._msg_cls(type=getattr(self._type_cls, name), **kw)
 
@@ -298,6 +339,8 @@ class NativeBarrierCore:
         a = self._abuf
         rc = self._handle_fn(self._h, self._mref, self._aref)
         if rc:
+            if rc == _lib.TW_ECALLBACK:
+                self._raise_callback(rc)
             if rc == _lib.TW_EINVAL:
                 if code == 0:
                     raise MalformedBody(f"unknown role {msg.role!r}")
@@ -323,7 +366,9 @@ class NativeBarrierCore:
         if reply is not None:
             reply(ack)
         if a.resolve:
-            self._resolve_fn(self._h)
+            rc = self._resolve_fn(self._h)
+            if rc:
+                self._raise_callback(rc)
         return ack
 
     def _learn_type(self, msg) -> int:

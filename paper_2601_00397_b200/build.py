@@ -3,9 +3,12 @@
 from __future__ import annotations
 
 import glob
+import hashlib
+import json
 import os
 import shutil
 import subprocess
+import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -55,6 +58,13 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, OUT)
     with open(os.path.join(HERE, "lib", "ptxas.log"), "w") as fh:
         fh.write(proc.stderr)
+    with open(OUT, "rb") as fh:
+        digest = hashlib.sha256(fh.read()).hexdigest()
+    info = {"library": os.path.relpath(OUT, os.path.dirname(HERE)), "sha256": digest,
+            "built_at_unix": int(time.time()), "nvcc": [os.path.basename(cmd[0]), *NVCC_FLAGS],
+            "sources": [os.path.relpath(x, os.path.dirname(HERE)) for x in sources()]}
+    with open(os.path.join(HERE, "lib", "build_info.json"), "w") as fh:
+        json.dump(info, fh, indent=1)
     return OUT
 
 

@@ -75,8 +75,24 @@ struct tw_core {
 
   // NULL clock / sleep: the host realtime clock and nanosleep, i.e. the reference's
   // defaults wall_now() (time_core.py:27-35) and time.sleep, without a callback
+  // A host callback that failed calls tw_core_abort: the core unwinds right after that
+  // callback returns (state changed so far stays, as when a Python callback raises inside
+  // the reference core) and tw_core_handle / tw_core_try_resolve return TW_ECALLBACK.
+  bool aborted = false;
+  struct Abort {};
+  void check_abort() {
+    if (aborted) {
+      aborted = false;
+      throw Abort{};
+    }
+  }
+
   int64_t now() {
-    if (clock) return clock(user);
+    if (clock) {
+      const int64_t t = clock(user);
+      check_abort();
+      return t;
+    }
     timespec ts;
     clock_gettime(CLOCK_REALTIME, &ts);
     return (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
@@ -84,6 +100,7 @@ struct tw_core {
   void do_sleep(double seconds) {
     if (sleep) {
       sleep(user, seconds);
+      check_abort();
       return;
     }
     const double ns = seconds * 1e9;
@@ -97,7 +114,10 @@ struct tw_core {
   int32_t eligible() const { return n_active_actors - n_exempt; }
 
   void record(tw_core_record& r) {
-    if (log) log(user, &r);
+    if (log) {
+      log(user, &r);
+      check_abort();
+    }
   }
   static tw_core_record blank(int32_t kind) {
     tw_core_record r;
@@ -184,6 +204,7 @@ struct tw_core {
         ev.offset_ns = offset_ns;
         ev.seq = seq;
         emit(user, &ev);
+        check_abort();
       }
       has_last_bcast = true;
       last_bcast = stamp;
@@ -349,6 +370,8 @@ struct tw_core {
             ev.group = m.group;
             ev.generation = generation;
             emit(user, &ev);
+            check_abort();
+        check_abort();
           }
           g.generation++;
           g.arrived.clear();
@@ -415,12 +438,32 @@ extern "C" int tw_core_free(tw_core* core) {
 
 extern "C" int tw_core_handle(tw_core* core, const tw_core_msg* msg, tw_core_ack* ack) {
   if (!core || !msg || !ack) return TW_EINVAL;
-  return core->handle(*msg, *ack);
+  try {
+    return core->handle(*msg, *ack);
+  } catch (const tw_core::Abort&) {
+    return TW_ECALLBACK;
+  }
 }
 
 extern "C" int tw_core_try_resolve(tw_core* core) {
   if (!core) return TW_EINVAL;
-  core->try_resolve();
+  try {
+    core->try_resolve();
+  } catch (const tw_core::Abort&) {
+    return TW_ECALLBACK;
+  }
+  return TW_OK;
+}
+
+extern "C" int tw_core_abort(tw_core* core) {
+  if (!core) return TW_EINVAL;
+  core->aborted = true;
+  return TW_OK;
+}
+
+extern "C" int tw_core_set_suppress(tw_core* core, int32_t suppress_broadcasts) {
+  if (!core) return TW_EINVAL;
+  core->suppress = suppress_broadcasts ? 1 : 0;
   return TW_OK;
 }
 

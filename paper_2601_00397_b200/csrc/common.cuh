@@ -114,6 +114,19 @@ __device__ __forceinline__ TableView table_view(const char* pset, const tw_pred_
 // Python round(float) -> int (half to even), then us -> ns.
 __device__ __forceinline__ int64_t us_to_ns_rn(double us) { return __double2ll_rn(us) * 1000; }
 
+// LinearPredictor.predict's quantisation (predictor.py:142-146): int(round(us)), a
+// negative result raises NegativeDuration, then * 1000. round() itself raises for NaN
+// (ValueError) and +-inf (OverflowError); a finite result beyond int64 ns is the engine's
+// limit (TW_PRED_OVERFLOW) instead of the reference's unbounded Python int.
+__device__ __forceinline__ int64_t linear_us_to_ns(double us) {
+  if (us != us) return TW_PRED_NAN;
+  if (__dadd_rn(us, -us) != 0.0) return TW_PRED_OVERFLOW;  // +-inf (inf - inf = nan)
+  if (us < -0.5) return TW_PRED_NEGATIVE;                  // round(us) < 0 (half-even: -0.5 -> 0)
+  if (us >= 9223372036854775807.0) return TW_PRED_OVERFLOW;
+  const int64_t q = __double2ll_rn(us);
+  return q > INT64_MAX / 1000 ? (int64_t)TW_PRED_OVERFLOW : q * 1000;
+}
+
 // Correctly rounded a / b for an integer-valued b > 0 given rb = RN(1/b): a first
 // quotient RN(a*rb) within 2 ulps, then two FMA residual corrections (Markstein: with a
 // correctly rounded reciprocal, q + (a - b q) rb rounded once is RN(a/b) once q is
@@ -425,8 +438,7 @@ __device__ __forceinline__ int64_t predict_scalar(const char* pset, int id, int6
     double us = __dadd_rn(d->base_us, __dmul_rn(d->per_prefill_token_us, __ll2double_rn(P)));
     us = __dadd_rn(us, __dmul_rn(d->per_decode_us, __ll2double_rn(D)));
     us = __dadd_rn(us, __dmul_rn(d->per_context_token_us, __ll2double_rn(C)));
-    const int64_t q = __double2ll_rn(us);
-    return q < 0 ? (int64_t)TW_PRED_NEGATIVE : q * 1000;
+    return linear_us_to_ns(us);
   }
   if (d->kind != TW_PRED_TABLE) return TW_PRED_BAD_DESC;
   const TableView t = table_view(pset, d);

@@ -491,9 +491,9 @@ extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const in
 }
 
 extern "C" int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const int32_t* host_slots, int32_t n_slots,
-                                   int32_t desc_id, void* pinned_io, void* dev_io, int64_t io_bytes,
-                                   int64_t* out_ns, void* stream) {
-  if (!pset || !pinned_io || !dev_io || !out_ns || n_slots < 0 || (n_slots > 0 && !host_slots) ||
+                                   int32_t desc_id, void* pinned_io, int64_t io_bytes, int64_t* out_ns,
+                                   void* stream) {
+  if (!pset || !pinned_io || !out_ns || n_slots < 0 || (n_slots > 0 && !host_slots) ||
       io_bytes < 8 * (int64_t)n_slots + 8 || pset_bytes < (int64_t)sizeof(tw_pset_header)) {
     set_error("tw_predict_one_sync: bad arguments");
     return TW_EINVAL;
@@ -505,7 +505,6 @@ extern "C" int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const i
   char* h = static_cast<char*>(pinned_io);
   const size_t slots = 8 * (size_t)n_slots, res = (slots + 7) & ~(size_t)7;
   if (n_slots) memcpy(h, host_slots, slots);
-  (void)dev_io;
   // the answer word starts as a value no answer takes (ns >= 0, TW_PRED_* codes are small
   // negatives); the host polls it instead of synchronizing the stream (~10 us less)
   volatile int64_t* ans = reinterpret_cast<volatile int64_t*>(h + res);

@@ -830,23 +830,23 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int64_t body = (K - 1) * (int64_t)n_dec;
     if (body > 0) {
       const int D = n_dec;
-      if (em.evp == nullptr) {
-        // digest v2 is linear in (position, ts, step) per request: decoder i's K-1 body
-        // events sum to M_i * (U + (K-1)*A*i) (twb200.h tw_event_run_sum), one term per
-        // decoder instead of one hash per event
-        const uint64_t m = (uint64_t)(K - 1);
-        const uint64_t U = tw_event_run_sum(m, (uint64_t)n_events, (uint64_t)D, now0, d, step0);
-        const uint64_t mA = m * TW_DIG_A;
+      // digest v2 is linear in (position, ts, step) per request: decoder i's K-1 body
+      // events sum to M_i * (U + (K-1)*A*i) (twb200.h tw_event_run_sum), one term per
+      // decoder instead of one hash per event
+      const uint64_t m = (uint64_t)(K - 1);
+      const uint64_t U = tw_event_run_sum(m, (uint64_t)n_events, (uint64_t)D, now0, d, step0);
+      const uint64_t mA = m * TW_DIG_A;
 #pragma unroll 1
-        for (int i = lane; i < D; i += 32)
-          em.dig += tw_event_mult((uint64_t)sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN) * (U + mA * (uint64_t)i);
-      } else {  // audited config: every event is also dumped
+      for (int i = lane; i < D; i += 32)
+        em.dig += tw_event_mult((uint64_t)sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN) * (U + mA * (uint64_t)i);
+      if (em.evp) {  // audited config: the body's events themselves, flattened over the lanes
         const int q32 = 32 / D, r32 = 32 % D;
         int64_t j = lane / D;
         int i = lane - (int)j * D;
-#pragma unroll 1  // one copy of the event hash in the loop
-        for (int64_t e = lane; e < body; e += 32) {
-          em.event(n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d, step0 + j + 1);
+#pragma unroll 1
+        for (int64_t e = lane; e < body && n_events + e < em.ev_cap; e += 32) {
+          cold_dump_event(em.evp, n_events + e, sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN, now0 + (j + 1) * d,
+                          step0 + j + 1);
           i += r32;
           j += q32;
           if (i >= D) { i -= D; j++; }

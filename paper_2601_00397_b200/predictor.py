@@ -33,6 +33,8 @@ from ._lib import (
     PRED_DESC_DTYPE,
     PSET_HEADER_DTYPE,
     TW_PRED_BAD_DESC,
+    TW_PRED_NAN,
+    TW_PRED_OVERFLOW,
     TW_PRED_CONSTANT,
     TW_PRED_EMPTY_BATCH,
     TW_PRED_LINEAR,
@@ -127,6 +129,10 @@ def raise_for_code(code: int, context: str = "") -> None:
         raise TableMiss(f"no calibration for {context or 'this batch'} and extrapolation is disabled")
     if code == TW_PRED_BAD_DESC:
         raise PredictorError("predictor descriptor out of range")
+    if code == TW_PRED_NAN:  # the reference's int(round(nan)) (predictor.py:142)
+        raise ValueError("cannot convert float NaN to integer")
+    if code == TW_PRED_OVERFLOW:  # round(+-inf), or a duration past int64 ns (engine limit)
+        raise OverflowError(f"predicted duration does not fit int64 nanoseconds{context}")
     raise PredictorError(f"unknown prediction code {code}")
 
 
@@ -496,8 +502,16 @@ class PredictorSet:
         """out[i] = ns for features (P, D, C) with descriptor desc_id (torch or numpy in).
 
         Empty batches are encoded as P == D == 0 and C < 0 (twb200.h). Returns a CUDA
-        int64 tensor when given CUDA tensors, else a numpy array.
+        int64 tensor when given CUDA tensors, else a numpy array. With an explicit
+        `stream`, the input copies, the output allocation, the kernel and the read-back all
+        run on it (no cross-stream race).
         """
+        from ._device import on_stream
+
+        with on_stream(stream):
+            return self._predict_features(P, D, C, desc_id, device)
+
+    def _predict_features(self, P, D, C, desc_id, device=None, stream=None):
         import torch
 
         from ._device import require_cuda, stream_handle
@@ -542,6 +556,14 @@ class PredictorSet:
 
     # -- CSR batches -> features -> ns ------------------------------------------------
     def predict_csr(self, off, tok, ctx, desc_id, device=None, return_features=False, stream=None):
+        """CSR batches -> ns (see _predict_csr); with an explicit `stream` every copy, the
+        kernel and the read-back run on that stream."""
+        from ._device import on_stream
+
+        with on_stream(stream):
+            return self._predict_csr(off, tok, ctx, desc_id, device, return_features)
+
+    def _predict_csr(self, off, tok, ctx, desc_id, device=None, return_features=False, stream=None):
         """Fused extraction + prediction over CSR batches given as arrays (torch or numpy).
 
         off: int64 [nb + 1]; tok / ctx: int32 per slot (tok -1 = DecodeSlot), padded to
@@ -699,7 +721,7 @@ class _LiveChannel:
         buf[0:n] = [c.chunk_tokens for c in chunks] + [-1] * len(decodes)
         buf[n : 2 * n] = [c.context_len_before for c in chunks] + [d.context_len for d in decodes]
         hp = self.h.data_ptr()
-        rc = self._fn(self.blob_ptr, self.pset.nbytes, self.buf_addr, n, 0, hp, hp, 8 * self.cap + 16,
+        rc = self._fn(self.blob_ptr, self.pset.nbytes, self.buf_addr, n, 0, hp, 8 * self.cap + 16,
                       self._out_ref, stream_handle())
         _lib.check(rc, "tw_predict_one_sync")
         return int(self._out.value)

@@ -310,7 +310,10 @@ class DeviceSweep:
             caps = np.zeros(self.n_cfg, np.int64)
             for c in self.audit:
                 lo, hi = workloads.wl_off[self.cfgs[c]["workload_id"]], workloads.wl_off[self.cfgs[c]["workload_id"] + 1]
-                caps[c] = int(workloads.output[lo:hi].astype(np.int64).sum() + (hi - lo))  # output+1 per request
+                # at most max(output, 1) + 1 events per request: FIRST_TOKEN, output - 1
+                # OUTPUT_TOKENs, FINISHED; a request with output <= 0 still emits
+                # FIRST_TOKEN + FINISHED (oracle.py:93-100)
+                caps[c] = int(np.maximum(workloads.output[lo:hi].astype(np.int64), 1).sum() + (hi - lo))
             self.ev_off = np.zeros(self.n_cfg + 1, np.int64)
             np.cumsum(caps, out=self.ev_off[1:])
             self.d_ev_off = to_device(self.ev_off, dev)
@@ -379,6 +382,8 @@ class DeviceSweep:
         if self.audit:
             evs = to_numpy_struct(self.d_ev, EVENT_DTYPE, int(self.ev_off[-1]))
             for c in self.audit:
+                if int(res[c]["status"]) & TW_SIM_OVERFLOW_BIT:
+                    raise EngineError(f"config {c}: event dump overflowed its buffer ({int(res[c]['events'])} events)")
                 k = min(int(res[c]["events"]), int(self.ev_off[c + 1] - self.ev_off[c]))
                 out.events[c] = evs[self.ev_off[c] : self.ev_off[c] + k]
         return out
@@ -442,7 +447,9 @@ def summary_doc(rec, mode: str = "oracle", workload_fingerprint: str = "", wall_
     return doc
 
 
-def _raise_status(res, what: str = "") -> None:
+def _raise_status(res, what: str = "", audited: bool = False) -> None:
+    if audited and int(res["status"]) & TW_SIM_OVERFLOW_BIT:
+        raise EngineError(f"{what}event dump overflowed its buffer: {int(res['events'])} events")
     st = int(res["status"]) & ~TW_SIM_OVERFLOW_BIT
     if st == TW_SIM_OK:
         return
@@ -479,7 +486,7 @@ def simulate(arrivals, cfg, predictor, epoch_ns: int = 0) -> list[dict]:
     wl = pack_arrivals([arrivals])
     sc = SweepConfig(engine=cfg, pred_id=0, workload_id=0, epoch_ns=epoch_ns, timekeeper=False)
     out = simulate_many(wl, [sc], [predictor], audit=[0], per_request=False)
-    _raise_status(out.results[0])
+    _raise_status(out.results[0], audited=True)
     return events_to_docs(out.events[0], wl.request_ids[0])
 
 

@@ -63,26 +63,40 @@ class OpStream:
     ops: list = field(default_factory=list)
     _n_clients: int = 0
     _groups: dict = field(default_factory=dict)
+    _ids: dict = field(default_factory=dict)  # client id -> registration index, as the core issued them
+    _live_actors: set = field(default_factory=set)
+    _sealed: bool = False
 
     def _op(self, t, arg=0, client=0, group=0):
         self.ops.append((int(arg), t, int(client), int(group)))
 
-    def register_actor(self) -> str:
-        self._op(TW_OP_REGISTER_ACTOR)
+    def _register(self, t, role: str):
+        self._op(t)
+        if self._sealed:  # RegistrationSealed: no client is created (timekeeper.py:155-157)
+            return None
         self._n_clients += 1
-        return f"actor{self._n_clients}"
+        cid = f"{role}{self._n_clients}"
+        self._ids[cid] = self._n_clients - 1
+        if role == "actor":
+            self._live_actors.add(cid)
+        return cid
 
-    def register_observer(self) -> str:
-        self._op(TW_OP_REGISTER_OBSERVER)
-        self._n_clients += 1
-        return f"observer{self._n_clients}"
+    def register_actor(self) -> str | None:
+        return self._register(TW_OP_REGISTER_ACTOR, "actor")
+
+    def register_observer(self) -> str | None:
+        return self._register(TW_OP_REGISTER_OBSERVER, "observer")
 
     def seal(self) -> None:
         self._op(TW_OP_SEAL)
+        if self._live_actors:  # sealing with no active actor fails with NoActors (timekeeper.py:176-178)
+            self._sealed = True
 
     def _client(self, client_id: str):
-        c = client_index(client_id or "")
-        return (c, True) if c >= 0 else (0, False)
+        """Only ids the core issued map to a client (the reference raises UnknownClient for
+        anything else, e.g. 'actor01' or an observer's index under the actor prefix)."""
+        c = self._ids.get(client_id or "")
+        return (c, True) if c is not None else (0, False)
 
     def jump(self, client_id: str, target_ns: int) -> None:
         c, ok = self._client(client_id)
@@ -98,6 +112,7 @@ class OpStream:
     def deregister(self, client_id: str) -> None:
         c, ok = self._client(client_id)
         self._op(TW_OP_DEREGISTER if ok else TW_OP_BAD_CLIENT, 0, c)
+        self._live_actors.discard(client_id)
 
     def advance(self, ns: int) -> None:
         """FakeClock.advance (pkg/tests/_support.py:36-37)."""

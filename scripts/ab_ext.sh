@@ -1,4 +1,4 @@
 mkdir -p gpurun_out; rm -f gpurun_out/ab_ext.log
 for i in 1 2; do for v in $AB_VARIANTS; do
-  TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_$v.so timeout 300 python scripts/ab_ext.py 2>/dev/null | sed "s/^/$v: /" >> gpurun_out/ab_ext.log
+  TWB200_ALLOW_LIB_OVERRIDE=1 TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_$v.so timeout 300 python scripts/ab_ext.py 2>/dev/null | sed "s/^/$v: /" >> gpurun_out/ab_ext.log
 done; done

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out; rm -f gpurun_out/ab_pred2.log
 for i in 1 2; do for v in $AB_VARIANTS; do
-  TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_$v.so timeout 300 python scripts/ab_pred.py 2>/dev/null | sed "s/^/$v: /" >> gpurun_out/ab_pred2.log
+  TWB200_ALLOW_LIB_OVERRIDE=1 TWB200_LIB=paper_2601_00397_b200/lib/libtwb200_$v.so timeout 300 python scripts/ab_pred.py 2>/dev/null | sed "s/^/$v: /" >> gpurun_out/ab_pred2.log
 done; done
 cat gpurun_out/ab_pred2.log

@@ -114,3 +114,84 @@ def test_native_core_state_views_and_stall_diagnostics():
     assert core.stalled(now_ns=clock.now_ns)["collectives"]["tp0"]["arrived"] == ["actor2"]
     core.handle(Message(MessageType.DEREGISTER, client_id=b))
     assert core.clients["actor2"].active is False and core.groups["tp0"].arrived == set()
+
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def _ref_core_cls():
+    import sys
+
+    if not os.path.isdir(os.path.join(REF, "timewarp")):
+        pytest.skip("reference not installed under baseline/_ref")
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    from timewarp.timekeeper import BarrierCore
+    from timewarp.wire import Message as RefMessage
+    from timewarp.wire import MessageType as RefType
+
+    return BarrierCore, RefMessage, RefType
+
+
+class _Boom(RuntimeError):
+    pass
+
+
+def _drive(core_cls, fail_clock_at, fail_emit, Message=Message, MessageType=MessageType):
+    """Two actors, jumps that resolve; the clock raises on its n-th read (or emit raises)."""
+    clock = FakeClock()
+    n = [0]
+
+    def clk():
+        n[0] += 1
+        if n[0] == fail_clock_at:
+            raise _Boom("clock")
+        return clock.clock()
+
+    def emit(_m):
+        if fail_emit:
+            raise _Boom("emit")
+
+    # with a log sink both cores read the clock for every record (without one, the native
+    # core skips the reads that only stamp records)
+    core = core_cls(cooldown_ns=500_000, emit=emit, clock=clk, sleep=clock.sleep, log_record=lambda r: None)
+    trace = []
+    msgs = [Message(MessageType.REGISTER, role="ACTOR"), Message(MessageType.REGISTER, role="ACTOR"),
+            Message(MessageType.SEAL), Message(MessageType.JUMP_REQUEST, client_id="actor1", target=2_000_000_000),
+            Message(MessageType.JUMP_REQUEST, client_id="actor2", target=3_000_000_000),
+            Message(MessageType.JUMP_REQUEST, client_id="actor1", target=4_000_000_000),
+            Message(MessageType.JUMP_REQUEST, client_id="actor2", target=4_000_000_000)]
+    for m in msgs:
+        try:
+            core.handle(m)
+            trace.append("ok")
+        except _Boom as exc:
+            trace.append(str(exc))
+        trace.append((core.offset_ns, core.seq, core.last_broadcast_wall_ns, sorted(core.pending.items())))
+    return trace
+
+
+@pytest.mark.parametrize("fail_clock_at,fail_emit", [(k, False) for k in range(1, 14)] + [(0, True)])
+def test_native_core_propagates_callback_exceptions_like_the_reference(fail_clock_at, fail_emit):
+    """A clock or emit callback that raises: the exception reaches the caller of handle()
+    and the core keeps the state changed up to that point, as the reference core does
+    (ctypes trampolines store it, tw_core_abort unwinds the native call)."""
+    ref_core, ref_msg, ref_type = _ref_core_cls()
+    want = _drive(ref_core, fail_clock_at, fail_emit, ref_msg, ref_type)
+    got = _drive(NativeBarrierCore, fail_clock_at, fail_emit)
+    assert got == want
+
+
+def test_native_core_suppress_broadcasts_is_live():
+    """suppress_broadcasts set after construction takes effect at the next resolve."""
+    clock = FakeClock()
+    emitted = []
+    core = NativeBarrierCore(cooldown_ns=0, emit=emitted.append, clock=clock.clock, sleep=clock.sleep)
+    a = core.handle(Message(MessageType.REGISTER, role="ACTOR")).client_id
+    core.handle(Message(MessageType.SEAL))
+    core.handle(Message(MessageType.JUMP_REQUEST, client_id=a, target=2_000_000_000))
+    core.suppress_broadcasts = True
+    core.handle(Message(MessageType.JUMP_REQUEST, client_id=a, target=3_000_000_000))
+    core.suppress_broadcasts = False
+    core.handle(Message(MessageType.JUMP_REQUEST, client_id=a, target=4_000_000_000))
+    assert [m.seq for m in emitted] == [1, 3] and core.seq == 3

@@ -843,6 +843,43 @@ def test_drop_in_simulate_matches_reference_timeline():
                  ConstantPredictor(10_000))
 
 
+def test_drop_in_simulate_with_zero_and_negative_outputs():
+    """Requests with output_tokens <= 0 emit FIRST_TOKEN + FINISHED (2 events) in the
+    reference (oracle.py:93-100): the event buffer must hold them (no silent truncation).
+    Expected list produced by the reference's oracle.simulate on this input."""
+    from paper_2601_00397_b200.predictor import ConstantPredictor
+    from paper_2601_00397_b200.sweep import EngineConfig, simulate
+    from paper_2601_00397_b200.workload import Arrival
+
+    arr = [Arrival("a", 0, 10, 0), Arrival("b", 5, 20, -3), Arrival("c", 7, 5, 1), Arrival("d", 9, 12, 3)]
+    ev = simulate(arr, EngineConfig(chunk_size=8, max_batch_tokens=16), ConstantPredictor(10))
+    want = [("a", "FIRST_TOKEN", 20000, 2), ("a", "FINISHED", 20000, 2), ("c", "FIRST_TOKEN", 20000, 2),
+            ("c", "FINISHED", 20000, 2), ("b", "FIRST_TOKEN", 40000, 4), ("b", "FINISHED", 40000, 4),
+            ("d", "FIRST_TOKEN", 40000, 4), ("d", "OUTPUT_TOKEN", 50000, 5), ("d", "OUTPUT_TOKEN", 60000, 6),
+            ("d", "FINISHED", 60000, 6)]
+    assert [(e["request_id"], e["kind"], e["virtual_ts_ns"], e["step"]) for e in ev] == want
+
+
+def test_linear_quantisation_extremes_raise_like_the_reference():
+    """NaN / inf / overflowing Linear durations through the bulk kernel (codes equal the
+    oracle's) and through the drop-in predict(), raising the reference's exception types
+    (round(nan): ValueError, round(inf): OverflowError; predictor.py:142)."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import BatchComposition, DecodeSlot, LinearPredictor, NegativeDuration, PredictorSet
+
+    bases = [float("nan"), float("inf"), float("-inf"), 1e16, 9.2e15, -0.5, -0.51, -1e300, 2.5]
+    pset = PredictorSet([LinearPredictor(b) for b in bases])
+    n = len(bases)
+    args = (np.zeros(n, np.int32), np.ones(n, np.int32), np.zeros(n, np.int64), np.arange(n, dtype=np.int32))
+    assert np.array_equal(pset.predict_features(*args), orc.predict_many(pset.blob, *args))
+    batch = BatchComposition(decodes=(DecodeSlot("x", 1),))
+    for b, exc in ((float("nan"), ValueError), (float("inf"), OverflowError), (-0.51, NegativeDuration)):
+        with pytest.raises(exc):
+            LinearPredictor(b).predict(batch)
+    assert LinearPredictor(9.2e15).predict(batch) == 9_200_000_000_000_000_000
+    assert LinearPredictor(-0.5).predict(batch) == 0
+
+
 def test_native_library_is_the_in_tree_build():
     import os
 

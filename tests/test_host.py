@@ -166,11 +166,34 @@ def test_opstream_encoding():
     h.jump("bogus", 3)
     h.deregister(o)
     ops, off, wall0, cool, sup = pack_streams([h])
-    assert ops["type"].tolist() == [0, 1, 2, 3, 4, 4, 3, 7, 5]
+    assert ops["type"].tolist() == [0, 1, 2, 3, 4, 4, 7, 7, 5]  # never-issued ids are unknown clients
     assert ops["group"].tolist()[4:6] == [0, 1]
-    assert ops["client"].tolist()[6] == 98
+    assert ops["client"].tolist()[8] == 1
     assert client_index("observer2") == 1 and client_index("nope") == -1
     assert off.tolist() == [0, 9]
+
+
+def test_opstream_only_maps_ids_the_core_issued():
+    """'actor01', an observer's index under the actor prefix and registrations after the
+    seal are unknown clients, as in the reference core (UnknownClient, timekeeper.py:122-128),
+    checked through the C oracle's replay (ack 3 = UnknownClient, 5 = RoleViolation,
+    1 = RegistrationSealed)."""
+    from oracle import oracle as orc
+
+    h = OpStream(cooldown_ns=0)
+    a = h.register_actor()
+    o = h.register_observer()
+    h.seal()
+    late = h.register_actor()
+    assert (a, o, late) == ("actor1", "observer2", None)
+    h.jump("actor01", 5)
+    h.jump("actor2", 5)
+    h.jump(o, 5)
+    h.jump(a, 7)
+    ops, off, wall0, cool, sup = pack_streams([h])
+    assert ops["type"].tolist() == [0, 1, 2, 0, 7, 7, 3, 3]
+    ack, events, fin = orc.tk_replay(ops, off, wall0, cool, sup)
+    assert ack.tolist()[:8] == [0, 0, 0, 1, 3, 3, 5, 0]
 
 
 def test_partition_balances_and_covers():
@@ -338,7 +361,7 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
         ("tw_metrics_many", lambda: lib.tw_metrics_many(null, 3, null, null, null, null, null, null, null, null,
                                                          1000, null, null)),
         ("tw_generate_poisson", lambda: lib.tw_generate_poisson(null, 4, null, null, null, null, null, null)),
-        ("tw_predict_one_sync", lambda: lib.tw_predict_one_sync(null, 64, null, 3, 0, null, null, 0, null, null)),
+        ("tw_predict_one_sync", lambda: lib.tw_predict_one_sync(null, 64, null, 3, 0, null, 0, null, null)),
     ]
     for name, call in cases:
         rc = call()

@@ -202,3 +202,20 @@ def test_oracle_metrics_full_size_cases():
     for rec, case in metrics_golden():
         if case["arrivals"] is None:
             assert_summary_equal(_oracle_metrics_case(rec, case), rec["summary"], rec["name"])
+
+
+def test_oracle_linear_quantisation_extremes():
+    """int(round(us)) * 1000 at the edges (predictor.py:137-146): NaN -> ValueError code,
+    +-inf -> OverflowError code, finite beyond int64 ns -> engine-limit overflow code,
+    -0.5 rounds to 0 (half-even), below that NegativeDuration."""
+    from paper_2601_00397_b200.predictor import LinearPredictor
+
+    cases = [(float("nan"), -5), (float("inf"), -6), (float("-inf"), -6), (1e16, -6), (9.3e15, -6),
+             (9.2e15, 9_200_000_000_000_000_000), (-0.5, 0), (-0.51, -2), (-1e300, -2), (2.5, 2000), (3.5, 4000)]
+    preds = [LinearPredictor(b) for b, _ in cases]
+    blob = PredictorSet(preds).blob
+    n = len(cases)
+    got = orc.predict_many(blob, np.zeros(n, np.int32), np.ones(n, np.int32), np.zeros(n, np.int64),
+                           np.arange(n, dtype=np.int32))
+    assert got.tolist() == [w for _, w in cases]
+
