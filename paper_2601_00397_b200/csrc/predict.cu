@@ -250,7 +250,21 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
         const uint32_t tbase = smem_u32(slots + (size_t)(2 * s) * cap), cbase = tbase + 4u * (uint32_t)cap;
         const uint32_t q1 = 4u * (uint32_t)(s1[j] - a0);
         int32_t dn = 0;
-        for (uint32_t q = 4u * (uint32_t)(s0[j] - a0); q < q1; q += 4u) {
+        uint32_t q = 4u * (uint32_t)(s0[j] - a0);
+#ifdef TWB_EXT_PAIR
+        // two slots per iteration: four independent shared loads in flight, half the loop overhead
+        for (; q + 4u < q1; q += 8u) {
+          int32_t x0, c0, x1, c1;
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x0) : "r"(tbase + q));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x1) : "r"(tbase + q + 4u));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(c0) : "r"(cbase + q));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(c1) : "r"(cbase + q + 4u));
+          Pt[j] += (int64_t)(x0 > 0 ? x0 : 0) + (int64_t)(x1 > 0 ? x1 : 0);
+          dn += (x0 < 0) + (x1 < 0);
+          Ct[j] += (int64_t)c0 + (int64_t)c1;
+        }
+#endif
+        for (; q < q1; q += 4u) {
           int32_t x, c;
           asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x) : "r"(tbase + q));
           asm volatile("ld.shared.b32 %0, [%1];" : "=r"(c) : "r"(cbase + q));
@@ -278,6 +292,14 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
           feat[3 * b + 2] = Ct[j];
         }
         int64_t r;
+#ifdef TWB_EXT_NOPRED  // A/B only: extraction without the predictor (not the product)
+        r = Pt[j] * 3 + Dn[j] * 5 + Ct[j] + ib[j];
+        __stcs(out + b, r);
+        s0[j] = n0[j];
+        s1[j] = n1[j];
+        ib[j] = nid[j];
+        continue;
+#endif
         if (s1[j] == s0[j]) r = TW_PRED_EMPTY_BATCH;
         else if (((Pt[j] | Dn[j]) >> 31) == 0 && Ct[j] >= 0)
           r = predict_one<kShared>(ps, qh, n_desc, (int32_t)Pt[j], (int32_t)Dn[j], Ct[j], ib[j]);

@@ -384,7 +384,12 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
   }
 }
 
-TWB_TK_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
+#ifdef TWB_SIM_OUTLINE_IDLE
+#define TWB_IDLE_FN static __device__ __noinline__
+#else
+#define TWB_IDLE_FN TWB_TK_FN
+#endif
+TWB_IDLE_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                         int64_t end) {
   // idle jump: only the dispatcher drives time (its target is <= end while V < end)
   for (;;) {
@@ -447,6 +452,7 @@ int64_t cold_predict_warp(const char* ps, int id, int64_t P, int64_t D, int64_t 
 
 struct PredCache {
   int64_t misses;      // profiling only
+  int64_t miss_cyc;    // profiling only
   int64_t key, val;    // this lane's entry
   int64_t P, D, C, d;  // single entry (uses_c)
   bool uses_c;
@@ -469,9 +475,13 @@ __device__ __forceinline__ int64_t predict_cached(PredCache& pc, const char* ps,
   const int64_t key = (P << 32) | D;
   const unsigned hit = __ballot_sync(kFull, pc.key == key);
   if (hit) return __shfl_sync(kFull, pc.val, __ffs(hit) - 1);
+#ifdef TWB_PROFILE_PHASES
+  const long long m0 = clock64();
+#endif
   const int64_t d = predict_miss<kTput>(ps, qh, id, P, D, C);
 #ifdef TWB_PROFILE_PHASES
   pc.misses++;
+  pc.miss_cyc += clock64() - m0;
 #endif
   if (lane == pc.victim) {
     pc.key = key;
@@ -513,6 +523,45 @@ struct Emitter {
   }
 };
 
+// Plan passes over more than 32 active slots (pass 1a: decode candidates and whether any
+// request is mid-prefill; the KV blocks held, oracle.py:43-46, 122). Out of line in the
+// throughput variant (TWB_SIM_OUTLINE_WIDE): the hot loop's code footprint is what bounds
+// it there (instruction-fetch stalls), and most steps have <= 32 active requests.
+#ifdef TWB_SIM_OUTLINE_WIDE
+#define TWB_WIDE_FN static __device__ __noinline__
+#else
+#define TWB_WIDE_FN static __device__ __forceinline__
+#endif
+TWB_WIDE_FN int wide_pass1a(Slots sl, int n_act) {
+  const int lane = threadIdx.x & 31;
+  int total_dec = 0;
+  bool any_mid = false;
+#pragma unroll 1
+  for (int b = 0; b < n_act; b += 32) {
+    const int i = b + lane;
+    const bool v = i < n_act;
+    const int32_t pr = v ? sl.prompt[i] : 0, dn = v ? sl.done[i] : 0;
+    const int32_t e = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
+    const bool mid = v && dn < pr;
+    total_dec += __popc(__ballot_sync(kFull, v && !mid && e < op));
+    any_mid |= __any_sync(kFull, mid);
+  }
+  return (total_dec << 1) | (any_mid ? 1 : 0);
+}
+TWB_WIDE_FN int64_t wide_held(Slots sl, int n_act, Blocks blk) {
+  const int lane = threadIdx.x & 31;
+  int64_t held_l = 0;
+#pragma unroll 1
+  for (int b = 0; b < n_act; b += 32) {
+    const int i = b + lane;
+    if (i < n_act) {
+      const int32_t h0 = blk.ceil_div(sl.prompt[i]), h1 = blk.ceil_div(sl.done[i] + sl.emit[i]);
+      held_l += h0 > h1 ? h0 : h1;  // _held (oracle.py:43-46)
+    }
+  }
+  return warp_sum_i64_redux(held_l);
+}
+
 // kTput: the throughput variant (predictor blob read from global memory, see k_sim)
 template <bool kTput>
 __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
@@ -521,6 +570,11 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const long long t_start = clock64();  // per-config cycles (always on: 2 reads)
   int64_t n_normal = 0, n_runs = 0, n_run_steps = 0, tk_cyc = 0, ev_cyc = 0;
   int64_t plan_cyc = 0, pred_cyc = 0, apply_cyc = 0, arr_cyc = 0, adm_cyc = 0;
+#ifdef TWB_PROFILE_PHASES
+  // TWB_PROFILE_PHASES builds write 32 int64 per config (tw_sim_set_profile stride 32)
+  int64_t x_walk_cyc = 0, x_fast_cyc = 0, x_it_adm = 0, x_it_wait = 0, x_it_wide = 0, x_body_cyc = 0;
+  int64_t x_it_chunk = 0, x_it_k1 = 0, x_it_idle = 0, x_idle_cyc = 0;
+#endif
   const tw_sim_cfg cfg = p.cfgs[c];
   tw_sim_result r;
   r.final_now_ns = cfg.epoch_ns;
@@ -573,6 +627,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const tw_pred_desc* pd = pset_desc(ps, cfg.pred_id < pset_ndesc(ps) ? cfg.pred_id : 0);
   PredCache pc;
   pc.misses = 0;
+  pc.miss_cyc = 0;
   pc.key = -1;
   pc.val = 0;
   pc.victim = 0;
@@ -630,32 +685,14 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     int total_dec = 0;
     bool any_mid = false;
     if (n_act > 32) {
-#pragma unroll 1
-      for (int b = 0; b < n_act; b += 32) {
-        const int i = b + lane;
-        const bool v = i < n_act;
-        const int32_t pr = v ? sl.prompt[i] : 0, dn = v ? sl.done[i] : 0;
-        const int32_t e = v ? sl.emit[i] : 0, op = v ? sl.output[i] : 0;
-        const bool mid = v && dn < pr;
-        total_dec += __popc(__ballot_sync(kFull, v && !mid && e < op));
-        any_mid |= __any_sync(kFull, mid);
-      }
+      const int v = wide_pass1a(sl, n_act);
+      total_dec = v >> 1;
+      any_mid = v & 1;
     }
     // KV: free = cap - sum(_held) (oracle.py:122), only needed when a queue head is probed
     int64_t free0 = 0;
     const bool need_free = waiting && n_act > 32;  // <= 32 active: summed in pass 1b below
-    if (need_free) {
-      int64_t held_l = 0;
-#pragma unroll 1
-      for (int b = 0; b < n_act; b += 32) {
-        const int i = b + lane;
-        if (i < n_act) {
-          const int32_t h0 = blk.ceil_div(sl.prompt[i]), h1 = blk.ceil_div(sl.done[i] + sl.emit[i]);
-          held_l += h0 > h1 ? h0 : h1;  // _held (oracle.py:43-46)
-        }
-      }
-      free0 = (int64_t)cfg.kv_capacity_blocks - warp_sum_i64_redux(held_l);
-    }
+    if (need_free) free0 = (int64_t)cfg.kv_capacity_blocks - wide_held(sl, n_act, blk);
 
     // ---- pass 1b: decode cutoff, chunk takes, features
     bool do_dec = true, do_chunks = true;
@@ -781,7 +818,14 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         break;
       }
       now = next_arr;  // idle until the next arrival (oracle.py:81-83)
+#ifdef TWB_PROFILE_PHASES
+      const long long i0 = clock64();
+      x_it_idle++;
+#endif
       if (tk_on) tk_idle(g, ts, n, epoch, now);
+#ifdef TWB_PROFILE_PHASES
+      x_idle_cyc += clock64() - i0;
+#endif
       continue;
     }
 
@@ -821,13 +865,30 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     const int64_t now0 = now;
     const int32_t step0 = step;
     {
+#ifdef TWB_PROFILE_PHASES
+      const int64_t prof_fast0 = g.prof_fast;
+      x_it_adm += n_adm > 0;
+      x_it_wait += waiting;
+      x_it_wide += n_act > 32;
+      x_it_chunk += n_chunk > 0;
+      x_it_k1 += K == 1;
+#endif
       const long long c0 = TWB_CLK();
       if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);  // WorkerGrid stage deadlines
       tk_cyc += TWB_CLK() - c0;
+#ifdef TWB_PROFILE_PHASES
+      if (tk_on) {
+        if (g.prof_fast != prof_fast0) x_fast_cyc += TWB_CLK() - c0;
+        else x_walk_cyc += TWB_CLK() - c0;
+      }
+#endif
     }
     const long long q4 = TWB_CLK();
     // events of steps 1..K-1 (decodes only), flattened over the lanes: e -> (step j, rank i)
     const int64_t body = (K - 1) * (int64_t)n_dec;
+#ifdef TWB_PROFILE_PHASES
+    const long long b0 = clock64();
+#endif
     if (body > 0) {
       const int D = n_dec;
       // digest v2 is linear in (position, ts, step) per request: decoder i's K-1 body
@@ -853,6 +914,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         }
       }
     }
+#ifdef TWB_PROFILE_PHASES
+    x_body_cyc += clock64() - b0;
+#endif
     if (K >= 2) {
       n_runs++;
       n_run_steps += K;
@@ -958,7 +1022,22 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   if (lane == 0) {
     p.res[c] = r;
     if (p.prof) {
+#ifdef TWB_PROFILE_PHASES
+      int64_t* q = p.prof + 32 * c;
+      q[16] = x_walk_cyc;
+      q[17] = x_fast_cyc;
+      q[18] = pc.miss_cyc;
+      q[19] = x_it_adm;
+      q[20] = x_it_wait;
+      q[21] = x_it_wide;
+      q[22] = x_body_cyc;
+      q[23] = x_it_chunk;
+      q[24] = x_it_k1;
+      q[25] = x_it_idle;
+      q[26] = x_idle_cyc;
+#else
       int64_t* q = p.prof + 16 * c;
+#endif
       q[0] = clock64() - t_start;
       q[1] = n_normal;
       q[2] = n_runs;

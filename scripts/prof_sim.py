@@ -11,7 +11,9 @@ from paper_2601_00397_b200.sweep import DeviceSweep  # noqa: E402
 
 sw = presets.sweep_1024()
 dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
-prof = torch.zeros(16 * len(sw), dtype=torch.int64, device="cuda")
+import os  # noqa: E402
+STRIDE = int(os.environ.get("TWB_PROF_STRIDE", "16"))  # 32 for TWB_PROFILE_PHASES builds
+prof = torch.zeros(STRIDE * len(sw), dtype=torch.int64, device="cuda")
 _lib.load().tw_sim_set_profile(prof.data_ptr())
 for _ in range(3):
     dev.run()
@@ -20,7 +22,7 @@ s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 s.record(); dev.run(); e.record(); e.synchronize()
 ms = s.elapsed_time(e)
 _lib.load().tw_sim_set_profile(None)
-pr = prof.view(-1, 16).cpu().numpy()
+pr = prof.view(-1, STRIDE).cpu().numpy()
 res = dev.fetch().results
 cyc, normal, runs, run_steps, tkc, evc, rounds, arc, plc, adc, prc, apc, misses, tcalls, tfast, tloops = pr.T[:16]
 order = np.argsort(-cyc)
@@ -37,5 +39,13 @@ for c in order[:12]:
 A = np.stack([normal, runs, run_steps], 1).astype(float)
 coef, *_ = np.linalg.lstsq(A, cyc.astype(float), rcond=None)
 print("fit cycles/normal step, /run, /run step:", coef.round(1))
+if STRIDE == 32:
+    names = ["walk_cyc", "fast_cyc", "miss_cyc", "it_adm", "it_wait", "it_wide", "body_cyc", "it_chunk", "it_k1",
+             "it_idle", "idle_cyc"]
+    for c in order[:3]:
+        it = normal[c] + runs[c]
+        print(c, "iters", it, {k: int(v) for k, v in zip(names, pr[c, 16:27])},
+              f"walk {100*pr[c,16]/cyc[c]:.1f}% fast {100*pr[c,17]/cyc[c]:.1f}% miss {100*pr[c,18]/cyc[c]:.1f}% "
+              f"body {100*pr[c,22]/cyc[c]:.1f}% idle {100*pr[c,26]/cyc[c]:.1f}% cyc/iter {cyc[c]/it:.0f}")
 json.dump({"ms": ms, "cyc": cyc.tolist(), "normal": normal.tolist(), "runs": runs.tolist(), "run_steps": run_steps.tolist()},
           open("gpurun_out/prof_sim.json", "w"))
