@@ -1,0 +1,19 @@
+# round-2 evidence for profiles/: tests, smoke, bench (config 5 headline + config 4 + projections + CPU
+# baselines), reference arm, launch list, ncu --set full of k_sim (both variants) and the HBM kernels
+mkdir -p gpurun_out
+nproc > gpurun_out/box.txt; nvidia-smi -L >> gpurun_out/box.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-projection --no-configs13 > gpurun_out/ncu_launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -f -o gpurun_out/prof_sim65k python scripts/ab_c5.py model 1 > gpurun_out/ncu_sim65k.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -f -o gpurun_out/prof_sim python scripts/ab_c5.py model1k 1 > gpurun_out/ncu_sim.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_features -s 2 -c 1 -f -o gpurun_out/prof_pred python scripts/ab_pred.py > gpurun_out/ncu_pred.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_batches -s 3 -c 1 -f -o gpurun_out/prof_ext python scripts/ab_ext.py > gpurun_out/ncu_ext.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:k_tk_resolve -s 16 -c 1 -f -o gpurun_out/prof_tk_bulk python scripts/ab_tk.py > gpurun_out/ncu_tk.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_metrics -s 1 -c 1 -f -o gpurun_out/prof_metrics python scripts/ab_metrics.py > gpurun_out/ncu_metrics.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_generate_poisson -s 2 -c 1 -f -o gpurun_out/prof_wl python scripts/ab_wl.py > gpurun_out/ncu_wl.log 2>&1
+timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim.log 2>&1
+timeout 300 python scripts/live_latency.py > gpurun_out/live.log 2>&1
+tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -c 400 gpurun_out/bench.log

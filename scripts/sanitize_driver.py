@@ -141,3 +141,14 @@ if "service" in which:
     print("k_predict_service ok")
 torch.cuda.synchronize()
 print(f"sanitize driver done: {_lib.launch_count()} launches")
+# hand torch's cached device and pinned blocks back so --leak-check reports only what the
+# engine itself would leak
+import gc  # noqa: E402
+
+for name in list(globals()):
+    if not name.startswith("_") and name not in ("gc", "torch", "which", "sys"):
+        globals().pop(name, None)
+gc.collect()
+torch.cuda.empty_cache()
+if hasattr(torch._C, "_host_emptyCache"):
+    torch._C._host_emptyCache()
