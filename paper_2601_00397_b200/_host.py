@@ -18,3 +18,11 @@ def host_bases(module: str, name: str) -> tuple:
         return ()
     cls = getattr(mod, name, None)
     return (cls,) if isinstance(cls, type) and issubclass(cls, Exception) else ()
+
+
+def host_module(module: str):
+    """timewarp.<module> when the host framework is importable, else None."""
+    try:
+        return importlib.import_module(f"timewarp.{module}")
+    except Exception:
+        return None

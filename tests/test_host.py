@@ -395,3 +395,52 @@ def test_exceptions_derive_from_the_host_frameworks_when_present():
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref, ROOT]))
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr[-2000:]
+
+
+def test_standalone_workload_schema_equals_the_reference(tmp_path):
+    """Without the host framework importable, workload.py declares the schema itself: it must
+    parse, render, fingerprint, draw and load traces exactly like timewarp.workload
+    (baseline/_ref), including the error texts."""
+    import importlib
+    import sys
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "timewarp")):
+        pytest.skip("reference not installed under baseline/_ref")
+    from paper_2601_00397_b200 import workload as ours
+
+    assert ours._HOST is None  # standalone in the test process
+    sys.path.insert(0, ref_dir)
+    try:
+        ref = importlib.import_module("timewarp.workload")
+    finally:
+        sys.path.remove(ref_dir)
+    docs = [{"source": "poisson", "qps": 8, "seed": 3, "num_requests": 50,
+             "prompt_tokens": {"kind": "uniform", "low": 64, "high": 2048}, "output_tokens": 17},
+            {"qps": 2.5, "seed": 9, "num_requests": 20, "prompt_tokens": {"value": 300},
+             "output_tokens": {"kind": "uniform", "low": 1, "high": 4}}, {}]
+    for doc in docs:
+        a, b = ours.WorkloadSpec.from_doc(doc), ref.WorkloadSpec.from_doc(doc)
+        assert a.to_doc() == b.to_doc() and a.fingerprint() == b.fingerprint()
+        if a.num_requests:
+            assert [tuple(vars(x).values()) for x in ours.generate_arrivals(a)] == \
+                   [tuple(vars(x).values()) for x in ref.generate_arrivals(b)]
+    for bad in ({"kind": "zipf"},):
+        with pytest.raises(Exception) as e1:
+            ours.TokenDist.from_doc(bad)
+        with pytest.raises(Exception) as e2:
+            ref.TokenDist.from_doc(bad)
+        assert str(e1.value) == str(e2.value)
+    good = tmp_path / "t.csv"
+    good.write_text("prompt_tokens,arrival_ms,output_tokens,extra\n10,5.5,3,x\n20,1.25,4,y\n7,5.5,1,z\n")
+    assert [tuple(vars(x).values()) for x in ours.load_trace(str(good))] == \
+           [tuple(vars(x).values()) for x in ref.load_trace(str(good))]
+    for text in ("arrival_ms,prompt_tokens\n1,2\n", "arrival_ms,prompt_tokens,output_tokens\n1,x,2\n",
+                 "arrival_ms,prompt_tokens,output_tokens\n-1,2,2\n"):
+        bad = tmp_path / "b.csv"
+        bad.write_text(text)
+        with pytest.raises(Exception) as e1:
+            ours.load_trace(str(bad))
+        with pytest.raises(Exception) as e2:
+            ref.load_trace(str(bad))
+        assert str(e1.value) == str(e2.value) and type(e1.value).__name__ == type(e2.value).__name__
