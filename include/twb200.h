@@ -364,14 +364,19 @@ typedef struct tw_run_metrics {
  * of each request in the caller's arrival list, which sets the order of the
  * compensated TPOT sum; NULL = the engine's (stable-sorted) order, which is the
  * caller's order for sorted arrival lists such as generate_arrivals produces.
- * max_requests: an upper bound on any workload's size (sizes shared memory: 8 bytes
- * per request, so at most ~28,000 requests on a B200; larger gives TW_ENOSMEM). */
+ * max_requests: an upper bound on any workload's size. Up to ~28,000 requests the
+ * per-request keys (8 B each) live in shared memory and scratch may be NULL; above
+ * that they live in the caller's global scratch (scratch_bytes >=
+ * tw_metrics_scratch_bytes(n_cfg, max_requests); less, down to one slice of
+ * 8*max_requests bytes, runs fewer CTAs; none gives TW_ENOSMEM). */
 int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off,
                     const int64_t* req_offset_ns, const int32_t* req_output,
                     const int64_t* req_base, const int64_t* req_first_ns,
                     const int64_t* req_finish_ns, const tw_sim_result* sim,
-                    const int32_t* sum_order, int32_t max_requests, tw_run_metrics* out,
-                    void* stream);
+                    const int32_t* sum_order, int32_t max_requests, void* scratch,
+                    int64_t scratch_bytes, tw_run_metrics* out, void* stream);
+/* bytes of global scratch tw_metrics_many wants for these sizes (0: shared memory suffices) */
+int64_t tw_metrics_scratch_bytes(int32_t n_cfg, int32_t max_requests);
 
 /* ---- native BarrierCore for the live Timekeeper --------- */
 /* Host C++ (no GPU): the reference's single-threaded protocol state machine

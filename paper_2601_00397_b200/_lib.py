@@ -181,6 +181,7 @@ EXPORTED_SYMBOLS = (
     "tw_sim_last_launch",
     "tw_sim_set_profile",
     "tw_metrics_many",
+    "tw_metrics_scratch_bytes",
     "tw_generate_poisson",
     "tw_core_new",
     "tw_core_free",
@@ -225,7 +226,8 @@ _SIGNATURES = {
     ),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
     "tw_sim_set_profile": (_I32, [_P]),
-    "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P]),
+    "tw_metrics_scratch_bytes": (_I64, [_I32, _I32]),
     "tw_generate_poisson": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "tw_abi_version": (_I32, []),
     "tw_last_error": (ctypes.c_char_p, []),

@@ -78,6 +78,7 @@ struct MetParams {
   const tw_sim_result* sim;
   const int32_t* sum_order;
   int32_t cap;  // keys capacity
+  uint64_t* gkeys;  // global-memory keys (cap per CTA) for workloads shared memory cannot hold
   tw_run_metrics* out;
 };
 
@@ -230,8 +231,12 @@ __device__ void stats_from_keys(const uint64_t* keys, int n, int count, double m
   __syncthreads();
 }
 
+// kGlobal: the keys live in a caller-provided global scratch (cap per CTA) instead of
+// dynamic shared memory: workloads above ~28,000 requests (metrics.py has no limit)
+template <bool kGlobal>
 __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
-  extern __shared__ __align__(16) uint64_t keys[];
+  extern __shared__ __align__(16) uint64_t skeys[];
+  uint64_t* keys = kGlobal ? p.gkeys + (size_t)blockIdx.x * (size_t)p.cap : skeys;
   __shared__ int64_t red[6][kMetWarps];
   __shared__ tw_run_metrics res;
   __shared__ double sh_mean;
@@ -363,8 +368,8 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
                                const int64_t* req_offset_ns, const int32_t* req_output,
                                const int64_t* req_base, const int64_t* req_first_ns,
                                const int64_t* req_finish_ns, const tw_sim_result* sim,
-                               const int32_t* sum_order, int32_t max_requests, tw_run_metrics* out,
-                               void* stream) {
+                               const int32_t* sum_order, int32_t max_requests, void* scratch,
+                               int64_t scratch_bytes, tw_run_metrics* out, void* stream) {
   if (n_cfg < 0 || (n_cfg > 0 && (!cfgs || !wl_off || !req_offset_ns || !req_output || !req_base ||
                                   !req_first_ns || !req_finish_ns || !out))) {
     set_error("tw_metrics_many: bad arguments");
@@ -380,16 +385,28 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int limit = (max_optin - kMetStaticSmem) / (int)sizeof(uint64_t);
-  if (max_requests > limit) {
-    set_error("tw_metrics_many: max_requests %d above the %d requests shared memory holds", max_requests, limit);
-    return TW_ENOSMEM;
-  }
   const int cap = max_requests > 0 ? max_requests : 1;  // selection needs no power-of-two padding
-  const size_t smem = (size_t)cap * sizeof(uint64_t);
-  cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_metrics, kMetThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  int64_t grid = (int64_t)sms * per_sm;
+  const bool global = max_requests > limit;
+  int64_t grid;
+  size_t smem = 0;
+  if (!global) {
+    smem = (size_t)cap * sizeof(uint64_t);
+    cudaFuncSetAttribute(k_metrics<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_metrics<false>, kMetThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    grid = (int64_t)sms * per_sm;
+  } else {
+    // keys in global scratch: one cap-sized slice per CTA, as many CTAs as the scratch holds
+    const int64_t slices = scratch ? scratch_bytes / ((int64_t)cap * (int64_t)sizeof(uint64_t)) : 0;
+    if (slices < 1) {
+      set_error("tw_metrics_many: max_requests %d above the %d requests shared memory holds and no scratch "
+                "(%lld bytes; tw_metrics_scratch_bytes gives the size)", max_requests, limit,
+                (long long)scratch_bytes);
+      return TW_ENOSMEM;
+    }
+    grid = (int64_t)sms * 4;
+    if (grid > slices) grid = slices;
+  }
   if (grid > n_cfg) grid = n_cfg;
   MetParams p;
   p.cfgs = cfgs;
@@ -403,8 +420,20 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
   p.sim = sim;
   p.sum_order = sum_order;
   p.cap = cap;
+  p.gkeys = static_cast<uint64_t*>(scratch);
   p.out = out;
-  k_metrics<<<(int)grid, kMetThreads, smem, (cudaStream_t)stream>>>(p);
+  if (global) k_metrics<true><<<(int)grid, kMetThreads, 0, (cudaStream_t)stream>>>(p);
+  else k_metrics<false><<<(int)grid, kMetThreads, smem, (cudaStream_t)stream>>>(p);
   count_launch();
   return check_launch("tw_metrics_many");
+}
+
+extern "C" int64_t tw_metrics_scratch_bytes(int32_t n_cfg, int32_t max_requests) {
+  int dev = 0, sms = 148, max_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (max_requests <= (max_optin - kMetStaticSmem) / (int)sizeof(uint64_t) || n_cfg <= 0) return 0;
+  const int64_t ctas = n_cfg < 4 * sms ? n_cfg : 4 * sms;
+  return ctas * (int64_t)max_requests * (int64_t)sizeof(uint64_t);
 }

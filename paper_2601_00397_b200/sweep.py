@@ -356,11 +356,16 @@ class DeviceSweep:
             ci = self.workloads.caller_index
             self.d_sum_order = to_device(ci, self.device) if ci is not None and len(ci) else None
             self.max_requests = int(self.workloads.sizes().max()) if self.workloads.n_workloads else 0
+            # workloads above what shared memory holds keep their keys in global scratch
+            nbytes = int(_lib.load().tw_metrics_scratch_bytes(self.n_cfg, self.max_requests))
+            self.d_met_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device) if nbytes else None
+        sc = self.d_met_scratch
         rc = _lib.load().tw_metrics_many(
             self.d_cfgs.data_ptr(), self.n_cfg, self.d_wl_off.data_ptr(), self.d_ts.data_ptr(),
             self.d_output.data_ptr(), self.d_req_base.data_ptr(), self.d_first.data_ptr(),
             self.d_finish.data_ptr(), self.d_res.data_ptr(),
             self.d_sum_order.data_ptr() if self.d_sum_order is not None else None, self.max_requests,
+            sc.data_ptr() if sc is not None else None, sc.numel() if sc is not None else 0,
             self.d_metrics.data_ptr(), stream_handle(stream),
         )
         _lib.check(rc, "tw_metrics_many")

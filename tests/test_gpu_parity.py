@@ -804,6 +804,36 @@ def test_device_metrics_edge_workloads():
     assert int(got[2]["tpot"]["count"]) == 0 and int(got[0]["num_requests"]) == 0
 
 
+def test_device_metrics_beyond_shared_memory_equal_oracle():
+    """Workloads of 40,000 and 65,000 requests (above the ~28,000 whose keys fit shared
+    memory): the summary keys spill to global scratch (tw_metrics_scratch_bytes) and the
+    records still equal the oracle's, next to a small workload in the same launch."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.predictor import ConstantPredictor, PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(41)
+    arrays = [(np.sort(rng.integers(0, 10**12, n)).astype(np.int64), rng.integers(1, 600, n).astype(np.int32),
+               rng.integers(1, 40, n).astype(np.int32)) for n in (40_000, 300, 65_000)]
+    eng = EngineConfig(chunk_size=512, max_batch_tokens=4096, max_running=256, kv_block_tokens=16,
+                       kv_capacity_blocks=1 << 22)
+    cfgs = config_array([SweepConfig(engine=eng, pred_id=0, workload_id=w, epoch_ns=11 * w) for w in range(3)])
+    dev = DeviceSweep(PredictorSet([ConstantPredictor(700)]), pack_arrays(arrays), cfgs, per_request=True)
+    assert _lib.load().tw_metrics_scratch_bytes(3, 65_000) > 0
+    dev.run()
+    dev.run_metrics()
+    got = dev.fetch_metrics()
+    out = dev.fetch()
+    assert dev.d_met_scratch is not None
+    for w, (ts, pr, op) in enumerate(arrays):
+        rb = int(out.req_base[w])
+        want = orc.metrics(ts, op, out.first_ns[rb : rb + len(ts)], out.finish_ns[rb : rb + len(ts)],
+                           int(cfgs[w]["epoch_ns"]))
+        assert int(got[w]["status"]) == 0 and got[w].tobytes() == want.tobytes(), w
+
+
 def test_device_metrics_equal_oracle_on_sweep_1024():
     from oracle import oracle as orc
     from paper_2601_00397_b200 import presets

@@ -359,7 +359,7 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
         ("tw_predict_batches", lambda: lib.tw_predict_batches(ctypes.cast(blob, V), 64, null, null, null, null, 5,
                                                                null, null, null)),
         ("tw_metrics_many", lambda: lib.tw_metrics_many(null, 3, null, null, null, null, null, null, null, null,
-                                                         1000, null, null)),
+                                                         1000, null, 0, null, null)),
         ("tw_generate_poisson", lambda: lib.tw_generate_poisson(null, 4, null, null, null, null, null, null)),
         ("tw_predict_one_sync", lambda: lib.tw_predict_one_sync(null, 64, null, 3, 0, null, 0, null, null)),
     ]
@@ -370,7 +370,8 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
         assert msg and (name in msg or "pset" in msg), (name, msg)
     # empty requests are no-ops that never reach the device
     assert lib.tw_generate_poisson(null, 0, null, null, null, null, null, null) == _lib.TW_OK
-    assert lib.tw_metrics_many(null, 0, null, null, null, null, null, null, null, null, 1000, null, null) == _lib.TW_OK
+    assert lib.tw_metrics_many(null, 0, null, null, null, null, null, null, null, null, 1000, null, 0, null,
+                               null) == _lib.TW_OK
 
 
 def test_exceptions_derive_from_the_host_frameworks_when_present():
