@@ -302,9 +302,12 @@ typedef struct tw_event {
  * ev / ev_off (optional): audited configs get their full event stream in
  * ev[ev_off[c] .. ev_off[c+1]). slot_capacity: per-warp active-list capacity,
  * normally max(max_running) over the configs (configs above it finish with
- * TW_SIM_CAPACITY; at most 4096; capacities whose slot state does not fit 4 warps
- * per CTA in shared memory run fewer warps per CTA). scratch: >= 16 bytes of device memory, zeroed by
- * the call (work counter).
+ * TW_SIM_CAPACITY). Up to 4096 the slot state lives in shared memory (capacities
+ * whose state does not fit 4 warps per CTA run fewer warps per CTA); above 4096 it
+ * lives in scratch (one slice per resident warp). scratch: device memory of
+ * scratch_bytes >= tw_sim_scratch_bytes(n_cfg, slot_capacity) (64 bytes up to 4096;
+ * less than that above 4096 runs fewer resident warps, down to one slice); its first
+ * 4 bytes are zeroed by the call (work counter).
  * Two variants of the same kernel, picked by n_cfg: up to 8 configs per SM (every
  * config resident on its own warp: latency-bound), each CTA stages pset_bytes of the
  * blob in shared memory; above that (throughput-bound), or when the blob does not fit
@@ -316,7 +319,9 @@ int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
                 const int32_t* req_output, tw_sim_result* results,
                 const int64_t* req_base, int64_t* req_first_ns, int64_t* req_finish_ns,
                 const int64_t* ev_off, tw_event* ev, int32_t slot_capacity, void* scratch,
-                void* stream);
+                int64_t scratch_bytes, void* stream);
+/* scratch bytes tw_sim_many wants for these sizes (64 up to slot capacity 4096) */
+int64_t tw_sim_scratch_bytes(int32_t n_cfg, int32_t slot_capacity);
 
 /* Launch geometry the library picked for the last tw_sim_many on this thread
  * (for the bench's roofline bookkeeping). */

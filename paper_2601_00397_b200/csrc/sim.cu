@@ -88,6 +88,7 @@ struct SimParams {
   int32_t* counter;
   int32_t cap;
   int64_t* prof;  // optional: 16 int64 per config (tw_sim_set_profile)
+  int32_t* gslots;  // slot state in global memory (capacities above kMaxSlotCap; sim_big.cu)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -1072,7 +1073,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
 //  * throughput (kTput = true, more configs than resident warps): 4 CTAs per SM at <= 128
 //    registers, the blob read through L1 so shared memory holds only slot state
 //    (16 warps per SM instead of 12: 65,536 configs 335 -> 289 ms).
-template <bool kTput>
+// kGSlots (sim_big.cu only): slot capacities above kMaxSlotCap keep each warp's slot
+// state in a global scratch slice instead of shared memory (max_running has no limit in
+// the reference); the blob is read from global memory as in the throughput variant.
+template <bool kTput, bool kGSlots = false>
 __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS : TWB_SIM_MIN_BLOCKS)
     k_sim(SimParams p) {
   extern __shared__ __align__(128) char smem[];
@@ -1080,7 +1084,9 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
   const char* ps = kTput ? static_cast<const char*>(p.pset) : smem + 128;
   if constexpr (!kTput) tma_stage_to_smem(smem + 128, p.pset, p.pset_bytes, reinterpret_cast<uint64_t*>(smem));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 7 * p.cap;
+  int32_t* base;
+  if constexpr (kGSlots) base = p.gslots + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * 7 * (size_t)p.cap;
+  else base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 7 * p.cap;
   Slots sl;
   sl.req = base;
   sl.prompt = base + p.cap;
@@ -1105,6 +1111,14 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
 // both variants in one translation unit the shared helpers stop being inlined into the
 // latency variant, whose blob reads then turn from LDS into generic loads (164 -> 173
 // registers, 1-2% slower at 1,024 configs).
+#ifdef TWB_SIM_BIG_TU
+int sim_big_prepare(int threads, int* per_sm) {
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true, true>, threads, 128);
+}
+void sim_big_launch(int grid, int threads, cudaStream_t s, const SimParams& p) {
+  k_sim<true, true><<<grid, threads, 128, s>>>(p);
+}
+#else
 int sim_tput_prepare(int threads, size_t smem, int* per_sm) {
   cudaFuncSetAttribute(k_sim<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true>, threads, smem);
@@ -1112,10 +1126,24 @@ int sim_tput_prepare(int threads, size_t smem, int* per_sm) {
 void sim_tput_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p) {
   k_sim<true><<<grid, threads, smem, s>>>(p);
 }
+#endif
 }  // namespace twb
 #else
 int sim_tput_prepare(int threads, size_t smem, int* per_sm);  // sim_tput.cu
 void sim_tput_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
+int sim_big_prepare(int threads, int* per_sm);  // sim_big.cu
+void sim_big_launch(int grid, int threads, cudaStream_t s, const SimParams& p);
+
+// bytes of scratch tw_sim_many needs: the 64-byte work counter, plus the global slot state
+// of every resident warp when the capacity exceeds what shared memory holds
+static int64_t sim_scratch_bytes(int32_t n_cfg, int cap, int sms, int per_sm, int64_t* grid_out) {
+  int64_t grid = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+  const int64_t want = ((int64_t)n_cfg + kSimWarps - 1) / kSimWarps;
+  if (grid > want) grid = want;
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = grid;
+  return 64 + grid * kSimWarps * 7 * (int64_t)sizeof(int32_t) * (int64_t)cap;
+}
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
 static thread_local int64_t* g_prof = nullptr;
@@ -1129,7 +1157,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
                            const int32_t* req_prompt, const int32_t* req_output, tw_sim_result* results,
                            const int64_t* req_base, int64_t* req_first_ns, int64_t* req_finish_ns,
                            const int64_t* ev_off, tw_event* ev, int32_t slot_capacity, void* scratch,
-                           void* stream) {
+                           int64_t scratch_bytes, void* stream) {
   if (!pset || pset_bytes < (int64_t)sizeof(tw_pset_header) || (pset_bytes & 15) ||
       ((uintptr_t)pset & 15)) {
     set_error("tw_sim_many: pset null, misaligned or not a multiple of 16 bytes");
@@ -1143,16 +1171,60 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   }
   if (n_cfg == 0) return TW_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (slot_capacity > (1 << 26)) {
+    set_error("tw_sim_many: slot capacity %d beyond 2^26", slot_capacity);
+    return TW_EINVAL;
+  }
   int cap = slot_capacity < 32 ? 32 : slot_capacity;
   cap = (cap + 31) & ~31;
-  if (cap > kMaxSlotCap) {
-    set_error("tw_sim_many: slot capacity %d exceeds the engine limit %d", slot_capacity, kMaxSlotCap);
-    return TW_ENOSMEM;
-  }
   int dev = 0, sms = 148, per_sm = 0, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  SimParams p;
+  p.gslots = nullptr;
+  if (cap > kMaxSlotCap) {  // slot state in global memory (sim_big.cu), one slice per resident warp
+    sim_big_prepare(kSimThreads, &per_sm);
+    int64_t grid = 0;
+    const int64_t need = sim_scratch_bytes(n_cfg, cap, sms, per_sm, &grid);
+    if (scratch_bytes < need) {
+      const int64_t fit = (scratch_bytes - 64) / ((int64_t)kSimWarps * 7 * (int64_t)sizeof(int32_t) * cap);
+      if (fit < 1) {
+        set_error("tw_sim_many: slot capacity %d needs %lld bytes of scratch (tw_sim_scratch_bytes), got %lld",
+                  cap, (long long)need, (long long)scratch_bytes);
+        return TW_ENOSMEM;
+      }
+      grid = fit;  // fewer resident warps: the work counter still hands out every config
+    }
+    cudaMemsetAsync(scratch, 0, sizeof(int32_t), s);
+    p.pset = pset;
+    p.pset_bytes = (uint32_t)pset_bytes;
+    p.pset_smem = 0;
+    p.cfgs = cfgs;
+    p.n_cfg = n_cfg;
+    p.order = order;
+    p.wl_off = wl_off;
+    p.ts = req_offset_ns;
+    p.prompt = req_prompt;
+    p.output = req_output;
+    p.res = results;
+    p.req_base = req_base;
+    p.first = req_first_ns;
+    p.finish = req_finish_ns;
+    p.ev_off = ev_off;
+    p.ev = ev;
+    p.counter = reinterpret_cast<int32_t*>(scratch);
+    p.cap = cap;
+    p.prof = g_prof;
+    p.gslots = reinterpret_cast<int32_t*>(static_cast<char*>(scratch) + 64);
+    sim_big_launch((int)grid, kSimThreads, s, p);
+    count_launch();
+    g_last[0] = (int32_t)grid;
+    g_last[1] = kSimThreads;
+    g_last[2] = 128;
+    g_last[3] = cap;
+    return check_launch("tw_sim_many");
+  }
   // slot state is 7 int32 arrays of cap per warp: large capacities get fewer warps per CTA
   const size_t per_warp = 7 * sizeof(int32_t) * (size_t)cap;
   // more configs than 8 per SM, or a blob too large to stage next to one warp's slot
@@ -1181,7 +1253,6 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > want) grid = want;
   cudaMemsetAsync(scratch, 0, sizeof(int32_t), s);
-  SimParams p;
   p.pset = pset;
   p.pset_bytes = (uint32_t)pset_bytes;
   p.pset_smem = pset_smem;
@@ -1209,6 +1280,17 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   g_last[2] = (int32_t)smem;
   g_last[3] = cap;
   return check_launch("tw_sim_many");
+}
+
+extern "C" int64_t tw_sim_scratch_bytes(int32_t n_cfg, int32_t slot_capacity) {
+  int cap = slot_capacity < 32 ? 32 : slot_capacity;
+  cap = (cap + 31) & ~31;
+  if (cap <= kMaxSlotCap || n_cfg <= 0) return 64;
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  sim_big_prepare(kSimThreads, &per_sm);
+  return sim_scratch_bytes(n_cfg, cap, sms, per_sm, nullptr);
 }
 
 extern "C" int tw_sim_set_profile(int64_t* per_config_16xi64) {

@@ -286,7 +286,7 @@ class DeviceSweep:
         # memory by the throughput variant (twb200.h, tw_sim_many).
         self.stage_bytes = pset.nbytes
         self.slot_capacity = int(max(32, int(self.cfgs["max_running"].max()) if self.n_cfg else 32))
-        self.slot_capacity = min(self.slot_capacity, 4096)
+        # up to 4096 the slot state lives in shared memory, above it in d_scratch (sim_big.cu)
         dev = self.device
         self.d_pset = pset.device_blob(dev)
         self.d_cfgs = to_device(self.cfgs, dev)
@@ -296,7 +296,8 @@ class DeviceSweep:
         self.d_prompt = to_device(workloads.prompt, dev)
         self.d_output = to_device(workloads.output, dev)
         self.d_res = torch.zeros(self.n_cfg * SIM_RESULT_DTYPE.itemsize + 16, dtype=torch.uint8, device=dev)
-        self.d_scratch = torch.zeros(64, dtype=torch.uint8, device=dev)
+        scratch = int(_lib.load().tw_sim_scratch_bytes(self.n_cfg, self.slot_capacity)) if self.n_cfg else 64
+        self.d_scratch = torch.zeros(max(64, scratch), dtype=torch.uint8, device=dev)
         total_req = int(self.req_base[-1])
         self.per_request = per_request
         if per_request:
@@ -337,7 +338,8 @@ class DeviceSweep:
             self.d_order.data_ptr(), self.d_wl_off.data_ptr(), self.d_ts.data_ptr(),
             self.d_prompt.data_ptr(), self.d_output.data_ptr(), self.d_res.data_ptr(),
             ptr(self.d_req_base), ptr(self.d_first), ptr(self.d_finish), ptr(self.d_ev_off),
-            ptr(self.d_ev), self.slot_capacity, self.d_scratch.data_ptr(), stream_handle(stream),
+            ptr(self.d_ev), self.slot_capacity, self.d_scratch.data_ptr(), self.d_scratch.numel(),
+            stream_handle(stream),
         )
         _lib.check(rc, "tw_sim_many")
 

@@ -625,6 +625,50 @@ def test_sim_large_slot_capacity_equals_oracle():
     assert peak > 1024, peak  # the large capacities were actually used
 
 
+def test_sim_slot_capacity_beyond_shared_memory_equals_oracle():
+    """max_running 8,192 / 6,000 (above the 4,096 whose slot state fits shared memory):
+    the slot state moves to global scratch (sim_big.cu, tw_sim_scratch_bytes) and the
+    records and stamps still equal the oracle's with more than 4,096 requests in flight."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.calibration import csv_path
+    from paper_2601_00397_b200.predictor import PredictorSet, TablePredictor
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SchedulingPolicy, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(31)
+    arrays, cfgs = [], []
+    for k, mr in enumerate([8192, 6000, 300]):
+        n = [9000, 7000, 800][k]
+        ts = np.sort(rng.integers(0, 100_000_000, n)).astype(np.int64)  # all arrive within 0.1 s
+        arrays.append((ts, rng.integers(16, 400, n).astype(np.int32), rng.integers(1, 30, n).astype(np.int32)))
+        eng = EngineConfig(chunk_size=256, max_batch_tokens=1 << 20, max_running=mr, kv_block_tokens=16,
+                           kv_capacity_blocks=1 << 22,
+                           policy=SchedulingPolicy.MIXED if k % 2 else SchedulingPolicy.PREFILL_PRIORITIZED)
+        cfgs.append(SweepConfig(engine=eng, pred_id=0, workload_id=k, timekeeper=bool(k % 2 == 0)))
+    wl = pack_arrays(arrays)
+    ca = config_array(cfgs)
+    pset = PredictorSet([TablePredictor.from_csv(csv_path("8b", 1, 1), allow_extrapolation=True)])
+    dev = DeviceSweep(pset, wl, ca, per_request=True)
+    assert dev.d_scratch.numel() > 64
+    dev.run()
+    out = dev.fetch()
+    launch = _lib.last_sim_launch()
+    assert launch["slot_capacity"] == 8192, launch
+    peak = 0
+    for k in range(len(cfgs)):
+        ts, pr, op = wl.workload(k)
+        res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
+        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+            assert out.results[k][f] == res[f], (k, f)
+        lo, hi = out.req_base[k], out.req_base[k + 1]
+        assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
+        order = np.argsort(first)
+        peak = max(peak, int(np.max(np.searchsorted(np.sort(finish), first[order], side="right") * -1
+                                    + np.arange(1, len(first) + 1))))
+    assert peak > 4096, peak
+
+
 def test_sim_blob_larger_than_shared_memory_equals_oracle():
     """A predictor set larger than a CTA's shared memory (48 irregular 24x24 tables with
     holes, ~460 KB): even a handful of configs take the variant that reads the blob from

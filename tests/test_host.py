@@ -354,7 +354,7 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
 
     cases = [
         ("tw_sim_many", lambda: lib.tw_sim_many(null, 0, null, 1, null, null, null, null, null, null, null, null,
-                                                 null, null, null, 256, null, null)),
+                                                 null, null, null, 256, null, 0, null)),
         ("tw_predict_features", lambda: lib.tw_predict_features(null, 64, null, null, null, null, 10, null, null)),
         ("tw_predict_batches", lambda: lib.tw_predict_batches(ctypes.cast(blob, V), 64, null, null, null, null, 5,
                                                                null, null, null)),
