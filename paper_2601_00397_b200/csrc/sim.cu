@@ -175,6 +175,30 @@ struct Blocks {
   }
 };
 
+// floor(t / d) for t < 2^32 with a per-config magic reciprocal (same bound as Blocks)
+struct Udiv {
+  uint32_t d, magic;
+  __device__ __forceinline__ void init(uint32_t b) {
+    d = b;
+    magic = 0xffffffffu / b;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t t) const {
+    uint32_t q = __umulhi(t, magic);
+    uint32_t r = t - q * d;
+    if (r >= d) { q++; r -= d; }
+    if (r >= d) q++;
+    return q;
+  }
+};
+// repeats of a chunk's take before the step that completes its prompt: floor(rem / take)
+// (rem = remaining prompt - 1); takes equal the config's chunk size except the last
+#ifdef TWB_SIM_CHUNK_MAGIC
+#define CHUNK_REPEATS(rem, take) \
+  ((uint32_t)(take) == cdiv.d ? cdiv.div((uint32_t)(rem)) : (uint32_t)(rem) / (uint32_t)(take))
+#else
+#define CHUNK_REPEATS(rem, take) ((uint32_t)(rem) / (uint32_t)(take))
+#endif
+
 struct Slots {
   int32_t* req;
   int32_t* prompt;
@@ -331,8 +355,16 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
         int64_t m_x = K * S;  // last deadline we may cover: end_all, or below the target
         if (g.disp_ts <= end_all) {
           const int64_t x = g.disp_ts - 1 - now0;
+#ifdef TWB_SIM_RCP_DIV
+          // the target's step index: 0 inside the first step (always when K == 1), else a
+          // reciprocal quotient (x < K*d < 2^52); its stage index needs no division for S <= 2
+          const int64_t fx = x < d ? 0 : div_rcp(x, d, __drcp_rn(__ll2double_rn(d)));
+          const int64_t xr = x - fx * d;
+          const int64_t px = (S == 1) ? 0 : (S == 2 ? (int64_t)(xr >= per) : min((int64_t)(S - 1), cold_div(xr, per)));
+#else
           const int64_t fx = HOT_DIV(x, d);
           const int64_t px = (S > 1) ? min((int64_t)(S - 1), HOT_DIV(x - fx * d, per)) : 0;
+#endif
           m_x = fx * S + px;
         }
         const int64_t R = m_x - m_on;
@@ -612,6 +644,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const int32_t max_running = cfg.max_running;
   Blocks blk;
   blk.init((uint32_t)cfg.kv_block_tokens);
+#ifdef TWB_SIM_CHUNK_MAGIC
+  Udiv cdiv;
+  cdiv.init((uint32_t)chunk);
+#endif
 
   Emitter em;
   em.dig = 0;
@@ -754,7 +790,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           if (dn + take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
           // steps this chunk repeats with the same take before the one that completes
           // the prompt: ceil(rem / take) - 1
-          min_rem = min(min_rem, (int)((uint32_t)(pr - dn - 1) / (uint32_t)take));
+          min_rem = min(min_rem, (int)CHUNK_REPEATS(pr - dn - 1, take));
         }
         n_chunk += __popc(__ballot_sync(kFull, chosen));
         want_before += __shfl_sync(kFull, incl, 31);
@@ -796,7 +832,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           p_l += take;
           if (take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
           // repeats of this first take before the completing chunk (macro horizon)
-          min_rem = min(min_rem, take > 0 ? (int)((uint32_t)(pr - 1) / (uint32_t)take) : 0);
+          min_rem = min(min_rem, take > 0 ? (int)CHUNK_REPEATS(pr - 1, take) : 0);
         }
         if (k == 0) break;
         const int64_t tot_need = __shfl_sync(kFull, NEi, k - 1);  // <= free: exact

@@ -1,4 +1,4 @@
-"""Time tw_metrics_many over the 1,024-config sweep's stamps (A/B helper)."""
+"""Time tw_metrics_many over a sweep's stamps (A/B helper): `python scripts/ab_metrics.py [1024|65536]`."""
 import json
 import statistics
 import sys
@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 from paper_2601_00397_b200 import presets  # noqa: E402
 from paper_2601_00397_b200.sweep import DeviceSweep  # noqa: E402
 
-sw = presets.sweep_1024()
+sw = presets.sweep_65536() if sys.argv[1:] == ["65536"] else presets.sweep_1024()
 dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
 dev.run()
 for _ in range(3):

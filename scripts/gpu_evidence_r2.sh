@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_si
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_features -s 2 -c 1 -f -o gpurun_out/prof_pred python scripts/ab_pred.py > gpurun_out/ncu_pred.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_predict_batches -s 3 -c 1 -f -o gpurun_out/prof_ext python scripts/ab_ext.py > gpurun_out/ncu_ext.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_tk_resolve -s 16 -c 1 -f -o gpurun_out/prof_tk_bulk python scripts/ab_tk.py > gpurun_out/ncu_tk.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_metrics -s 1 -c 1 -f -o gpurun_out/prof_metrics python scripts/ab_metrics.py > gpurun_out/ncu_metrics.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_metrics -s 1 -c 1 -f -o gpurun_out/prof_metrics python scripts/ab_metrics.py 65536 > gpurun_out/ncu_metrics.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_generate_poisson -s 2 -c 1 -f -o gpurun_out/prof_wl python scripts/ab_wl.py > gpurun_out/ncu_wl.log 2>&1
 timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim.log 2>&1
 timeout 300 python scripts/live_latency.py > gpurun_out/live.log 2>&1

@@ -146,8 +146,9 @@ print(f"sanitize driver done: {_lib.launch_count()} launches")
 import gc  # noqa: E402
 
 for name in list(globals()):
-    if not name.startswith("_") and name not in ("gc", "torch", "which", "sys"):
+    if not name.startswith("_") and name not in ("gc", "torch", "which", "sys", "presets"):
         globals().pop(name, None)
+presets._PSET = None  # the cached calibration set holds its device blob
 gc.collect()
 torch.cuda.empty_cache()
 if hasattr(torch._C, "_host_emptyCache"):
