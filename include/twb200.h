@@ -334,6 +334,14 @@ int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
  * run-event cycles, Timekeeper broadcasts, arrival cycles, plan cycles, admission
  * cycles, predict cycles, apply cycles, 0, 0, 0, 0}. */
 int tw_sim_set_profile(int64_t* per_config_16xi64);
+/* Debug mode for the next tw_sim_many calls on this thread: when set (device pointer,
+ * 8 int32 per config; NULL disables), the event loop runs its invariant-checking build
+ * (sim_check.cu) and records per config {iterations checked, virtual time went back,
+ * slot overran its prompt/output, incremental KV-block counter != recomputation
+ * (engine.py:359-369), Timekeeper offset/seq/wall went back, V != wall + offset or V
+ * short of the step end, last broadcast after the wall, event count != sum(max(output,
+ * 1) + 1)}: all but the first must stay 0. Results are identical to the normal build. */
+int tw_sim_set_checks(int32_t* per_config_8xi32);
 
 /* ---- per-config latency metrics: metrics.py:62-253 ------ */
 /* RunReport.summary() of an oracle-mode run (runner.py:339-365), reduced on device

@@ -179,6 +179,7 @@ EXPORTED_SYMBOLS = (
     "tw_tk_resolve",
     "tw_sim_many",
     "tw_sim_scratch_bytes",
+    "tw_sim_set_checks",
     "tw_sim_last_launch",
     "tw_sim_set_profile",
     "tw_metrics_many",
@@ -226,6 +227,7 @@ _SIGNATURES = {
         [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P],
     ),
     "tw_sim_scratch_bytes": (_I64, [_I32, _I32]),
+    "tw_sim_set_checks": (_I32, [_P]),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
     "tw_sim_set_profile": (_I32, [_P]),
     "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P]),

@@ -89,6 +89,7 @@ struct SimParams {
   int32_t cap;
   int64_t* prof;  // optional: 16 int64 per config (tw_sim_set_profile)
   int32_t* gslots;  // slot state in global memory (capacities above kMaxSlotCap; sim_big.cu)
+  int32_t* checks;  // sim_check.cu only: 8 invariant counters per config (tw_sim_set_checks)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -174,30 +175,6 @@ struct Blocks {
     return (int32_t)(q + (r != 0u));
   }
 };
-
-// floor(t / d) for t < 2^32 with a per-config magic reciprocal (same bound as Blocks)
-struct Udiv {
-  uint32_t d, magic;
-  __device__ __forceinline__ void init(uint32_t b) {
-    d = b;
-    magic = 0xffffffffu / b;
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t t) const {
-    uint32_t q = __umulhi(t, magic);
-    uint32_t r = t - q * d;
-    if (r >= d) { q++; r -= d; }
-    if (r >= d) q++;
-    return q;
-  }
-};
-// repeats of a chunk's take before the step that completes its prompt: floor(rem / take)
-// (rem = remaining prompt - 1); takes equal the config's chunk size except the last
-#ifdef TWB_SIM_CHUNK_MAGIC
-#define CHUNK_REPEATS(rem, take) \
-  ((uint32_t)(take) == cdiv.d ? cdiv.div((uint32_t)(rem)) : (uint32_t)(rem) / (uint32_t)(take))
-#else
-#define CHUNK_REPEATS(rem, take) ((uint32_t)(rem) / (uint32_t)(take))
-#endif
 
 struct Slots {
   int32_t* req;
@@ -355,16 +332,8 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
         int64_t m_x = K * S;  // last deadline we may cover: end_all, or below the target
         if (g.disp_ts <= end_all) {
           const int64_t x = g.disp_ts - 1 - now0;
-#ifdef TWB_SIM_RCP_DIV
-          // the target's step index: 0 inside the first step (always when K == 1), else a
-          // reciprocal quotient (x < K*d < 2^52); its stage index needs no division for S <= 2
-          const int64_t fx = x < d ? 0 : div_rcp(x, d, __drcp_rn(__ll2double_rn(d)));
-          const int64_t xr = x - fx * d;
-          const int64_t px = (S == 1) ? 0 : (S == 2 ? (int64_t)(xr >= per) : min((int64_t)(S - 1), cold_div(xr, per)));
-#else
           const int64_t fx = HOT_DIV(x, d);
           const int64_t px = (S > 1) ? min((int64_t)(S - 1), HOT_DIV(x - fx * d, per)) : 0;
-#endif
           m_x = fx * S + px;
         }
         const int64_t R = m_x - m_on;
@@ -603,6 +572,15 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const long long t_start = clock64();  // per-config cycles (always on: 2 reads)
   int64_t n_normal = 0, n_runs = 0, n_run_steps = 0, tk_cyc = 0, ev_cyc = 0;
   int64_t plan_cyc = 0, pred_cyc = 0, apply_cyc = 0, arr_cyc = 0, adm_cyc = 0;
+#ifdef TWB_SIM_CHECK
+  // invariant counters (sim_check.cu): [0] iterations checked, [1] virtual time went back,
+  // [2] a slot overran its prompt / output, [3] the incremental KV-block counter differs from
+  // the recomputation (engine.py:359-369), [4] Timekeeper offset / seq / wall went back,
+  // [5] V != wall + offset or V short of the step end, [6] last broadcast after the wall,
+  // [7] event count at the end differs from sum(max(output, 1) + 1)
+  int32_t chk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t chk_kv = 0, chk_now = 0, chk_off = 0, chk_seq = 0, chk_wall = 0;
+#endif
 #ifdef TWB_PROFILE_PHASES
   // TWB_PROFILE_PHASES builds write 32 int64 per config (tw_sim_set_profile stride 32)
   int64_t x_walk_cyc = 0, x_fast_cyc = 0, x_it_adm = 0, x_it_wait = 0, x_it_wide = 0, x_body_cyc = 0;
@@ -644,10 +622,6 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const int32_t max_running = cfg.max_running;
   Blocks blk;
   blk.init((uint32_t)cfg.kv_block_tokens);
-#ifdef TWB_SIM_CHUNK_MAGIC
-  Udiv cdiv;
-  cdiv.init((uint32_t)chunk);
-#endif
 
   Emitter em;
   em.dig = 0;
@@ -790,7 +764,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           if (dn + take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
           // steps this chunk repeats with the same take before the one that completes
           // the prompt: ceil(rem / take) - 1
-          min_rem = min(min_rem, (int)CHUNK_REPEATS(pr - dn - 1, take));
+          min_rem = min(min_rem, (int)((uint32_t)(pr - dn - 1) / (uint32_t)take));
         }
         n_chunk += __popc(__ballot_sync(kFull, chosen));
         want_before += __shfl_sync(kFull, incl, 31);
@@ -830,9 +804,12 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           sl.emit[slot] = 0;
           sl.plan[slot] = (int32_t)take;
           p_l += take;
+#ifdef TWB_SIM_CHECK
+          chk_kv += blk.ceil_div(pr);  // held at admission: the prompt's reservation (lane partial)
+#endif
           if (take >= pr) chunk_ev += (op <= 1) ? 2 : 1;
           // repeats of this first take before the completing chunk (macro horizon)
-          min_rem = min(min_rem, take > 0 ? (int)CHUNK_REPEATS(pr - 1, take) : 0);
+          min_rem = min(min_rem, take > 0 ? (int)((uint32_t)(pr - 1) / (uint32_t)take) : 0);
         }
         if (k == 0) break;
         const int64_t tot_need = __shfl_sync(kFull, NEi, k - 1);  // <= free: exact
@@ -987,6 +964,9 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       int nev = 0, k0 = 0;
       bool fin = false;
       const bool is_chunk = plan >= 0, is_dec = plan == -1;
+#ifdef TWB_SIM_CHECK
+      const int32_t held0 = v ? max(blk.ceil_div(pr), blk.ceil_div(dn + e)) : 0;
+#endif
       if (is_chunk) {
         dn += plan * (int32_t)K;
         if (dn >= pr) {
@@ -1015,6 +995,13 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       }
       pos_c += __popc(c1) + __popc(c2);
       pos_d += __popc(d1) + __popc(d2);
+#ifdef TWB_SIM_CHECK
+      if (v) {
+        const int32_t held1 = max(blk.ceil_div(pr), blk.ceil_div(dn + e));
+        chk_kv += (int64_t)held1 - held0 - (fin ? held1 : 0);  // _finish frees the final hold
+        if (dn > pr || e > op) chk[2]++;
+      }
+#endif
       // stable removal of finished requests (oracle.py:111-112)
       const bool keep = v && !fin;
       const unsigned km = __ballot_sync(kFull, keep);
@@ -1032,6 +1019,29 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     }
     n_events = pos_d;
     n_act = kept;
+#ifdef TWB_SIM_CHECK
+    {
+      // recompute the blocks the active set holds and compare with the incremental counter
+      int64_t held_l = 0;
+      for (int b = 0; b < n_act; b += 32) {
+        const int i = b + lane;
+        if (i < n_act) held_l += max(blk.ceil_div(sl.prompt[i]), blk.ceil_div(sl.done[i] + sl.emit[i]));
+      }
+      __syncwarp();
+      if (warp_sum_i64_redux(held_l) != warp_sum_i64_redux(chk_kv)) chk[3]++;
+      chk[0]++;
+      if (now < chk_now) chk[1]++;
+      chk_now = now;
+      if (tk_on) {
+        if (g.offset < chk_off || g.seq < chk_seq || g.wall < chk_wall) chk[4]++;
+        if (g.V != g.wall + g.offset || g.V < now) chk[5]++;
+        if (g.last_bcast != INT64_MIN && g.last_bcast > g.wall) chk[6]++;
+        chk_off = g.offset;
+        chk_seq = g.seq;
+        chk_wall = g.wall;
+      }
+    }
+#endif
     if (n_adm) {
       w_head += n_adm;
       qbase = w_head;
@@ -1042,6 +1052,16 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   }
 
   if (em.evp && n_events > em.ev_cap) overflow = 1;
+#ifdef TWB_SIM_CHECK
+  if (r.status == TW_SIM_OK) {
+    int64_t want_l = 0;
+    for (int i = lane; i < n; i += 32) want_l += (int64_t)max(__ldg(outp + i), 1) + 1;
+    if (warp_sum_i64_redux(want_l) != n_events) chk[7]++;
+  }
+  if (p.checks && lane == 0)
+    for (int k = 0; k < 8; k++) p.checks[8 * (int64_t)c + k] = chk[k];
+#endif
+
   // digest: sum of lane partials mod 2^64
   uint64_t dig = em.dig;
 #pragma unroll
@@ -1112,7 +1132,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
 // kGSlots (sim_big.cu only): slot capacities above kMaxSlotCap keep each warp's slot
 // state in a global scratch slice instead of shared memory (max_running has no limit in
 // the reference); the blob is read from global memory as in the throughput variant.
-template <bool kTput, bool kGSlots = false>
+template <bool kTput, bool kGSlots = false, bool kCheck = false>
 __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS : TWB_SIM_MIN_BLOCKS)
     k_sim(SimParams p) {
   extern __shared__ __align__(128) char smem[];
@@ -1139,6 +1159,7 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
     const int c = p.order ? p.order[idx] : idx;
     run_config<kTput>(p, ps, sl, c);
     __syncwarp();
+
   }
 }
 
@@ -1147,7 +1168,15 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
 // both variants in one translation unit the shared helpers stop being inlined into the
 // latency variant, whose blob reads then turn from LDS into generic loads (164 -> 173
 // registers, 1-2% slower at 1,024 configs).
-#ifdef TWB_SIM_BIG_TU
+#if defined(TWB_SIM_CHECK)
+int sim_check_prepare(int threads, size_t smem, int* per_sm) {
+  cudaFuncSetAttribute(k_sim<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true, false, true>, threads, smem);
+}
+void sim_check_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p) {
+  k_sim<true, false, true><<<grid, threads, smem, s>>>(p);
+}
+#elif defined(TWB_SIM_BIG_TU)
 int sim_big_prepare(int threads, int* per_sm) {
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim<true, true>, threads, 128);
 }
@@ -1169,6 +1198,9 @@ int sim_tput_prepare(int threads, size_t smem, int* per_sm);  // sim_tput.cu
 void sim_tput_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
 int sim_big_prepare(int threads, int* per_sm);  // sim_big.cu
 void sim_big_launch(int grid, int threads, cudaStream_t s, const SimParams& p);
+int sim_check_prepare(int threads, size_t smem, int* per_sm);  // sim_check.cu
+void sim_check_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
+static thread_local int32_t* g_checks = nullptr;
 
 // bytes of scratch tw_sim_many needs: the 64-byte work counter, plus the global slot state
 // of every resident warp when the capacity exceeds what shared memory holds
@@ -1219,6 +1251,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   SimParams p;
   p.gslots = nullptr;
+  p.checks = g_checks;
   if (cap > kMaxSlotCap) {  // slot state in global memory (sim_big.cu), one slice per resident warp
     sim_big_prepare(kSimThreads, &per_sm);
     int64_t grid = 0;
@@ -1267,7 +1300,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   // state: the throughput variant (blob read from global memory)
   const uint32_t blob_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
   const bool tput = (int64_t)n_cfg > (int64_t)kLatencyConfigsPerSm * sms ||
-                    128 + (size_t)blob_smem + per_warp > (size_t)max_optin;
+                    128 + (size_t)blob_smem + per_warp > (size_t)max_optin || g_checks != nullptr;
   const uint32_t pset_smem = tput ? 0u : blob_smem;
   int warps = kSimWarps;
   while (warps > 1 && 128 + pset_smem + warps * per_warp > (size_t)max_optin) warps--;
@@ -1278,7 +1311,9 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
               max_optin);
     return TW_ENOSMEM;
   }
-  if (tput) {
+  if (g_checks) {
+    sim_check_prepare(threads, smem, &per_sm);
+  } else if (tput) {
     sim_tput_prepare(threads, smem, &per_sm);
   } else {
     cudaFuncSetAttribute(k_sim<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1308,7 +1343,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   p.counter = reinterpret_cast<int32_t*>(scratch);
   p.cap = cap;
   p.prof = g_prof;
-  if (tput) sim_tput_launch((int)grid, threads, smem, s, p);
+  if (g_checks) sim_check_launch((int)grid, threads, smem, s, p);
+  else if (tput) sim_tput_launch((int)grid, threads, smem, s, p);
   else k_sim<false><<<(int)grid, threads, smem, s>>>(p);
   count_launch();
   g_last[0] = (int32_t)grid;
@@ -1327,6 +1363,11 @@ extern "C" int64_t tw_sim_scratch_bytes(int32_t n_cfg, int32_t slot_capacity) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   sim_big_prepare(kSimThreads, &per_sm);
   return sim_scratch_bytes(n_cfg, cap, sms, per_sm, nullptr);
+}
+
+extern "C" int tw_sim_set_checks(int32_t* per_config_8xi32) {
+  g_checks = per_config_8xi32;
+  return TW_OK;
 }
 
 extern "C" int tw_sim_set_profile(int64_t* per_config_16xi64) {

@@ -343,6 +343,25 @@ class DeviceSweep:
         )
         _lib.check(rc, "tw_sim_many")
 
+    CHECK_NAMES = ("iterations", "time_went_back", "slot_overrun", "kv_counter_diverged", "tk_went_back",
+                   "tk_virtual_inconsistent", "tk_bcast_after_wall", "event_count")
+
+    def run_checked(self, stream=None) -> np.ndarray:
+        """One launch of the invariant-checking build of the event loop (tw_sim_set_checks,
+        sim_check.cu): the same results, plus int32 [n_cfg, 8] counters (CHECK_NAMES;
+        every column but the first must be 0). Debug path, not timed."""
+        import torch
+
+        cnt = torch.zeros(max(self.n_cfg, 1) * 8, dtype=torch.int32, device=self.device)
+        lib = _lib.load()
+        lib.tw_sim_set_checks(cnt.data_ptr())
+        try:
+            self.run(stream)
+            torch.cuda.synchronize(self.device)
+        finally:
+            lib.tw_sim_set_checks(None)
+        return cnt[: 8 * self.n_cfg].view(self.n_cfg, 8).cpu().numpy()
+
     # -- per-config latency summary (metrics.py:173-253) ---------------------------
     def run_metrics(self, stream=None) -> None:
         """Launch the on-device reduction of this sweep's stamps (needs per_request)."""

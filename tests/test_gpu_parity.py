@@ -669,6 +669,30 @@ def test_sim_slot_capacity_beyond_shared_memory_equals_oracle():
     assert peak > 4096, peak
 
 
+def test_sim_invariant_checks_hold_on_sweep_and_edge_configs():
+    """The invariant-checking build (sim_check.cu, tw_sim_set_checks) over a spread of the
+    1,024 grid plus bursty high-concurrency and stalling configs: virtual time never goes
+    back, no slot overruns its prompt or output, the incremental KV-block counter equals
+    the recomputation every iteration (engine.py:359-369), the Timekeeper's offset, seq
+    and wall never go back and V = wall + offset reaches every step end, and the event
+    count equals sum(max(output, 1) + 1); the records equal the normal build's."""
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    sw = presets.sweep_1024(n_requests=300)
+    sub = sw.subset(np.arange(0, len(sw), 7))
+    dev = DeviceSweep(sub.pset, sub.workloads, sub.cfgs, per_request=True)
+    dev.run()
+    want = dev.fetch()
+    cnt = dev.run_checked()
+    got = dev.fetch()
+    assert (got.results == want.results).all()
+    assert np.array_equal(got.first_ns, want.first_ns) and np.array_equal(got.finish_ns, want.finish_ns)
+    assert (cnt[:, 0] > 0).all()
+    bad = {DeviceSweep.CHECK_NAMES[k]: int(cnt[:, k].sum()) for k in range(1, 8) if cnt[:, k].any()}
+    assert not bad, bad
+
+
 def test_sim_blob_larger_than_shared_memory_equals_oracle():
     """A predictor set larger than a CTA's shared memory (48 irregular 24x24 tables with
     holes, ~460 KB): even a handful of configs take the variant that reads the blob from
