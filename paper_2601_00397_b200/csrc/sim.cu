@@ -1028,7 +1028,10 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         if (i < n_act) held_l += max(blk.ceil_div(sl.prompt[i]), blk.ceil_div(sl.done[i] + sl.emit[i]));
       }
       __syncwarp();
-      if (warp_sum_i64_redux(held_l) != warp_sum_i64_redux(chk_kv)) chk[3]++;
+      int64_t kv = chk_kv;  // lane partials can be negative (finishes): plain shuffle sum
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kv += __shfl_xor_sync(kFull, kv, o);
+      if (warp_sum_i64_redux(held_l) != kv) chk[3]++;
       chk[0]++;
       if (now < chk_now) chk[1]++;
       chk_now = now;
@@ -1076,7 +1079,12 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     r.tk_wall_ns = g.wall;
   }
   if (overflow) r.status |= 1 << 8;
+  // the record is the config's completion signal: a host watching records in pinned memory
+  // (HostSweep's streamed copy-back) may copy the config's stamps as soon as it sees it, so
+  // every lane's stamp stores must be visible system-wide first
+  __syncwarp();
   if (lane == 0) {
+    __threadfence_system();
     p.res[c] = r;
     if (p.prof) {
 #ifdef TWB_PROFILE_PHASES
