@@ -783,7 +783,11 @@ def measure_sweep(sw, args, world, rank, device, cdev, dist_on, label):
         res["e2e"] = None
         return res
     host = HostSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
-    ids_dev = torch.from_numpy(np.asarray(sw.global_ids, np.int64)).to(cdev)
+    # the streamed mode keeps its records in pull order (host.perm): ids follow them
+    rec_ids = np.asarray(sw.global_ids, np.int64)
+    if host.perm is not None:
+        rec_ids = rec_ids[host.perm]
+    ids_dev = torch.from_numpy(rec_ids).to(cdev)
     merged_host = torch.empty((sw.n_global, 8), dtype=torch.int64, pin_memory=True) if dist_on else None
     e_durs = []
     for i in range(args.warmup + args.steps):
@@ -802,8 +806,9 @@ def measure_sweep(sw, args, world, rank, device, cdev, dist_on, label):
             e_durs.append(a.elapsed_time(b))
     e_ms = sum(e_durs) / len(e_durs)
     hr = host.host_results()
-    if not (hr == out.results).all() or not np.array_equal(host._pairs_out[2][1].numpy()[: n_req_e2e(host)],
-                                                              out.finish_ns):
+    h_first, h_finish = host.host_stamps()
+    if not (hr == out.results).all() or not np.array_equal(h_finish, out.finish_ns) or \
+            not np.array_equal(h_first, out.first_ns):
         raise SystemExit(f"rank {rank}: e2e host results differ from the device run")
     d2h = host.d2h_bytes
     if dist_on:
@@ -821,7 +826,9 @@ def measure_sweep(sw, args, world, rank, device, cdev, dist_on, label):
                   "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": int(d2h),
                   "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps / (e_ms / 1e3), 1),
                   "outputs": ("zero-copy: the kernel stores records and stamps into pinned host memory"
-                              if host.zero_copy else "records and stamps copied to pinned host memory after the kernel")
+                              if host.zero_copy else
+                              "streamed: records into pinned host memory, and each finished prefix of configs' stamps "
+                              "copied on a second stream while the kernel runs (the last ones after it)")
                   + ("; then the NCCL all-gather of every rank's records and the merge by config id, on device, "
                      "copied to host" if dist_on else "")}
     del host

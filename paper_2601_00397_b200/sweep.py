@@ -518,26 +518,47 @@ def simulate(arrivals, cfg, predictor, epoch_ns: int = 0) -> list[dict]:
 
 class HostSweep(DeviceSweep):
     """A sweep driven from HOST buffers: every ``run_from_host()`` copies the inputs
-    from pinned host memory to HBM and runs the event-loop kernel, all stream-ordered.
-    The result records and per-request stamps land in pinned host memory: with
-    ``zero_copy`` (the default up to 256 MB of outputs) the kernel stores them there
-    directly over PCIe as it produces them (host memory is device-addressable under
-    UVA), so no copy follows the kernel; otherwise they are copied back after it. This is the end-to-end path a
-    host caller pays for (bench.py ``e2e``)."""
+    from pinned host memory to HBM and runs the event-loop kernel, all stream-ordered,
+    and leaves the result records and per-request stamps in pinned host memory. This is
+    the end-to-end path a host caller pays for (bench.py ``e2e``). Two output modes:
 
-    # Zero-copy wins for small outputs (config 4, 16 MB of stamps: 7.98 vs 8.3 ms per step);
-    # for 1 GB of stamps (config 5) the kernel's scattered PCIe stores cost more than one
-    # bulk copy after it (316 vs 308-315 ms; scripts/ab_e2e65.py).
+    * ``zero_copy`` (default up to 256 MB of outputs): the kernel stores records and
+      stamps straight into pinned host memory over PCIe as it produces them (UVA), so
+      nothing follows the kernel (config 4, 16 MB of stamps: 7.98 vs 8.3 ms per step
+      with a copy after it);
+    * streamed (above that; config 5 has 1 GB of stamps): the configs are laid out in
+      their pull order (largest estimated cost first), so they finish roughly in stamp
+      order; the kernel writes each config's record into pinned memory after a
+      system-scope fence, and the host watches the records and copies each finished
+      prefix of the stamps on a second stream while the kernel still runs. Only the
+      last configs' stamps are copied after it.
+
+    Records and stamps are returned in the caller's config order (``host_results``,
+    ``host_stamps``)."""
+
     ZERO_COPY_MAX_BYTES = 256 << 20
+    STREAM_CHUNK_CONFIGS = 4096  # copy granularity of the streamed mode
 
-    def __init__(self, *args, zero_copy: bool | None = None, **kwargs) -> None:
+    def __init__(self, pset, workloads, cfgs, *args, zero_copy: bool | None = None, **kwargs) -> None:
         import torch
 
-        super().__init__(*args, **kwargs)
+        cfgs = np.ascontiguousarray(cfgs)
+        n_req = int(workloads.sizes()[cfgs["workload_id"]].sum()) if len(cfgs) else 0
+        per_request = kwargs.get("per_request", True)
         if zero_copy is None:
-            out_bytes = self.d_res.numel() + (16 * int(self.req_base[-1]) if self.per_request else 0)
-            zero_copy = out_bytes <= self.ZERO_COPY_MAX_BYTES
-        self.zero_copy = zero_copy
+            zero_copy = 64 * len(cfgs) + (16 * n_req if per_request else 0) <= self.ZERO_COPY_MAX_BYTES
+        self.zero_copy = bool(zero_copy)
+        self.streamed = not self.zero_copy and per_request
+        self.perm = None
+        if self.streamed:
+            # configs in pull order: the kernel then pulls them in stamp order (order = identity)
+            order = kwargs.pop("order", None)
+            if order is None:
+                order = np.argsort(-estimate_cost(pset, cfgs, workloads), kind="stable")
+            self.perm = np.asarray(order, np.int64)  # pull index -> caller's config index
+            cfgs = cfgs[self.perm]
+            kwargs["order"] = np.arange(len(cfgs), dtype=np.int32)
+        super().__init__(pset, workloads, cfgs, *args, **kwargs)
         self._pairs_in = []
         staged = self.d_pset[: self.stage_bytes]  # what the event loop reads of the blob
         for d in (staged, self.d_cfgs, self.d_order, self.d_wl_off, self.d_ts, self.d_prompt, self.d_output):
@@ -552,10 +573,14 @@ class HostSweep(DeviceSweep):
         if self.per_request:
             for d in (self.d_first, self.d_finish):
                 self._pairs_out.append((d, torch.full(d.shape, -1, dtype=d.dtype, pin_memory=True)))
-        if zero_copy:  # the kernel writes its outputs straight into the pinned buffers
+        if self.zero_copy or self.streamed:  # records straight into pinned memory
             self.d_res = self._pairs_out[0][1]
-            if self.per_request:
-                self.d_first, self.d_finish = self._pairs_out[1][1], self._pairs_out[2][1]
+        if self.zero_copy and self.per_request:  # stamps too
+            self.d_first, self.d_finish = self._pairs_out[1][1], self._pairs_out[2][1]
+        if self.streamed:
+            raw = self._pairs_out[0][1].numpy().view(np.uint8)[: self.n_cfg * SIM_RESULT_DTYPE.itemsize]
+            self._rec_view = raw.view(SIM_RESULT_DTYPE)
+            self._copy_stream = torch.cuda.Stream(device=self.device)
 
     @property
     def h2d_bytes(self) -> int:
@@ -566,13 +591,67 @@ class HostSweep(DeviceSweep):
         return int(sum(h.numel() * h.element_size() for _, h in self._pairs_out))
 
     def run_from_host(self, stream=None) -> None:
+        import time
+
+        import torch
+
+        if self.streamed:
+            self._rec_view["final_now_ns"] = np.iinfo(np.int64).min  # "not finished" marks
         for d, h in self._pairs_in:
             d.copy_(h, non_blocking=True)
         self.run(stream)
-        if not self.zero_copy:
+        if self.zero_copy:
+            return
+        if not self.streamed:
             for d, h in self._pairs_out:
                 h.copy_(d, non_blocking=True)
+            return
+        # streamed copy-back: copy each finished prefix of configs (pull order = stamp order)
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        cs = self._copy_stream  # no wait on `main`: that would hold every copy until the kernel ends;
+        # a region is copied only after the host saw its configs' fenced records
+        fin = self._rec_view["final_now_ns"]
+        unset = np.iinfo(np.int64).min
+        rb = self.req_base
+        (d1, h1), (d2, h2) = self._pairs_out[1], self._pairs_out[2]
+        n, done, copied = self.n_cfg, 0, 0
+        with torch.cuda.stream(cs):
+            while copied < n:
+                hi = min(n, done + 8192)
+                miss = np.flatnonzero(fin[done:hi] == unset)
+                done = done + int(miss[0]) if miss.size else hi
+                if done - copied >= self.STREAM_CHUNK_CONFIGS or done == n:
+                    lo_r, hi_r = int(rb[copied]), int(rb[done])
+                    if hi_r > lo_r:
+                        h1[lo_r:hi_r].copy_(d1[lo_r:hi_r], non_blocking=True)
+                        h2[lo_r:hi_r].copy_(d2[lo_r:hi_r], non_blocking=True)
+                    copied = done
+                elif miss.size:
+                    time.sleep(2e-4)
+        main.wait_stream(cs)
 
     def host_results(self) -> np.ndarray:
+        """The records, in the caller's config order."""
         raw = self._pairs_out[0][1].numpy().view(np.uint8)[: self.n_cfg * SIM_RESULT_DTYPE.itemsize]
-        return raw.view(SIM_RESULT_DTYPE).copy()
+        recs = raw.view(SIM_RESULT_DTYPE).copy()
+        if self.perm is None:
+            return recs
+        out = np.empty_like(recs)
+        out[self.perm] = recs
+        return out
+
+    def host_stamps(self):
+        """(first_ns, finish_ns) from pinned host memory, laid out as for the caller's config
+        order (config c's requests at [base[c], base[c+1]), base by cumulative sizes)."""
+        first, finish = self._pairs_out[1][1].numpy(), self._pairs_out[2][1].numpy()
+        n_req = int(self.req_base[-1])
+        if self.perm is None:
+            return first[:n_req].copy(), finish[:n_req].copy()
+        inv = np.empty(self.n_cfg, np.int64)
+        inv[self.perm] = np.arange(self.n_cfg)
+        sizes = np.diff(self.req_base)[inv]  # caller order
+        base = np.zeros(self.n_cfg + 1, np.int64)
+        np.cumsum(sizes, out=base[1:])
+        cfg_of = np.repeat(np.arange(self.n_cfg), sizes)
+        src = self.req_base[:-1][inv][cfg_of] + (np.arange(n_req, dtype=np.int64) - base[:-1][cfg_of])
+        return first[src], finish[src]

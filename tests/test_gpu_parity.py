@@ -693,6 +693,32 @@ def test_sim_invariant_checks_hold_on_sweep_and_edge_configs():
     assert not bad, bad
 
 
+def test_host_sweep_output_modes_equal_the_device_run():
+    """HostSweep's end-to-end output modes (zero-copy, streamed copy-back of finished
+    prefixes in pull order, copy after the kernel) return the device run's records and
+    stamps in the caller's config order."""
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep, HostSweep
+
+    sw = presets.sweep_1024(n_requests=200)
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+    dev.run()
+    want = dev.fetch()
+    for kw, chunk in (({"zero_copy": True}, None), ({"zero_copy": False}, 64), ({"zero_copy": False}, 1 << 30)):
+        host = HostSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True, **kw)
+        if chunk:
+            host.STREAM_CHUNK_CONFIGS = chunk
+        assert host.streamed == (not kw["zero_copy"])
+        for _ in range(2):
+            host.run_from_host()
+            import torch
+
+            torch.cuda.synchronize()
+            first, finish = host.host_stamps()
+            assert (host.host_results() == want.results).all(), kw
+            assert np.array_equal(first, want.first_ns) and np.array_equal(finish, want.finish_ns), kw
+
+
 def test_sim_blob_larger_than_shared_memory_equals_oracle():
     """A predictor set larger than a CTA's shared memory (48 irregular 24x24 tables with
     holes, ~460 KB): even a handful of configs take the variant that reads the blob from
