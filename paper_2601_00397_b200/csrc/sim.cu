@@ -253,7 +253,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
 #ifdef TWB_PROFILE_PHASES
   g.prof_calls++;
 #endif
-#ifndef TWB_SIM_TPUT_TU
+#if !defined(TWB_SIM_TPUT_TU) || defined(TWB_TPUT_TK_FAST)
   // One or two stages, steady state on the run's start (every stage gap > cJ), no
   // dispatcher target inside the run: the K*S deadlines each resolve as sleep cJ +
   // broadcast, which is the loop's steady-state closed form with R = K*S, without the
@@ -351,14 +351,11 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
           s = (int)(m_x - fx * S);
           m_walk = m_x + 1;
           tgt = (s == S - 1) ? base + d : base + per * (s + 1);
-#ifndef TWB_SIM_TPUT_TU
           // below the dispatcher's target (m_x < K*S): the next pass would find R = 0 and
           // resolve the round at min(target, next deadline); do that round now (latency
-          // variant: with the wall-bound fast path, 8.10 -> 7.94 ms; throughput: +1 ms)
+          // variant: with the wall-bound fast path, 8.10 -> 7.94 ms; throughput variant, round
+          // 2: 241.3 -> 239.7 ms)
           if (g.V >= end_all) continue;
-#else
-          continue;
-#endif
         }
       }
     }
