@@ -1,11 +1,14 @@
 # round-2 evidence for profiles/: tests, smoke, bench (config 5 headline + config 4 + projections + CPU
-# baselines), reference arm, launch list, ncu --set full of k_sim (both variants) and the HBM kernels
+# baselines), reference arm, multi-rank dry runs, launch list, ncu --set full of k_sim (both variants)
+# and the HBM kernels, sanitizer
 mkdir -p gpurun_out
 nproc > gpurun_out/box.txt; nvidia-smi -L >> gpurun_out/box.txt
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29501 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline --no-projection --no-config4 --no-configs13 > gpurun_out/bench_nccl1.log 2>&1; echo "nccl1 rc=$?" >> gpurun_out/bench_nccl1.log
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29502 bench.py --gpus 2 --steps 3 --warmup 3 --share-device > gpurun_out/bench_dry2.log 2>&1; echo "dry2 rc=$?" >> gpurun_out/bench_dry2.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-projection --no-configs13 > gpurun_out/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -f -o gpurun_out/prof_sim65k python scripts/ab_c5.py model 1 > gpurun_out/ncu_sim65k.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 1 -f -o gpurun_out/prof_sim python scripts/ab_c5.py model1k 1 > gpurun_out/ncu_sim.log 2>&1
@@ -16,4 +19,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_me
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_generate_poisson -s 2 -c 1 -f -o gpurun_out/prof_wl python scripts/ab_wl.py > gpurun_out/ncu_wl.log 2>&1
 timeout 300 python scripts/prof_sim.py > gpurun_out/prof_sim.log 2>&1
 timeout 300 python scripts/live_latency.py > gpurun_out/live.log 2>&1
+bash scripts/sanitize.sh > gpurun_out/sanitize_summary.log 2>&1
 tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -c 400 gpurun_out/bench.log
