@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(kPredThreads, TWB_PRED_MIN_BLOCKS) k_predict_f
 //  * warp 31 is the producer: for each tile of 992 batches it reads the tile's slot
 //    range from batch_off and moves the contiguous slot_tok / slot_ctx runs into a
 //    shared-memory stage with two cp.async.bulk copies (TMA bulk-copy engine) that
-//    complete on the stage's "full" mbarrier; it reuses a stage once all consumer
-//    warps have arrived on its "empty" mbarrier (kExtStages stages in flight);
+//    complete on the stage's "full" mbarrier (slot_ctx only when a model or the
+//    features output needs total_context); it reuses a stage once all consumer warps
+//    have arrived on its "empty" mbarrier (4 stages of tok + ctx or 8 of tok in flight);
 //  * warps 0-30 consume: each thread owns one batch per tile, prefetches its
 //    offsets and descriptor id for the next tile while the current one is reduced,
 //    sums its slots from shared memory (predictor.py:69-84) and predicts through the
@@ -109,10 +110,17 @@ constexpr int kExtThreads = 1024;
 #endif
 constexpr int kExtBpt = TWB_EXT_BPT;                        // batches per consumer thread per tile
 constexpr int kExtConsumers = (kExtThreads - 32) * kExtBpt;  // batches per tile
-#ifndef TWB_EXT_STAGES
-#define TWB_EXT_STAGES 4
+// Stages in flight: 4 when the context slots travel too (tok + ctx, 8 B per slot), 8 when
+// only the tokens do (4 B per slot): the same shared memory then holds twice as many tiles
+// ahead of the consumers.
+#ifndef TWB_EXT_STAGES_C
+#define TWB_EXT_STAGES_C 4
 #endif
-constexpr int kExtStages = TWB_EXT_STAGES;
+#ifndef TWB_EXT_STAGES_T
+#define TWB_EXT_STAGES_T 8
+#endif
+constexpr int kExtMaxStages = 8;
+static_assert(TWB_EXT_STAGES_C <= kExtMaxStages && TWB_EXT_STAGES_T <= kExtMaxStages, "stages");
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -145,7 +153,7 @@ struct ExtTile {
 
 template <bool kShared>
 __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
-    const void* __restrict__ pset, uint32_t pset_bytes, uint32_t pset_smem, int32_t cap,
+    const void* __restrict__ pset, uint32_t pset_bytes, uint32_t pset_smem, int32_t region,
     const int64_t* __restrict__ off, const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx,
     const int32_t* __restrict__ id, int64_t nb, int64_t* __restrict__ feat, int64_t* __restrict__ out) {
   extern __shared__ __align__(128) char smem[];
@@ -154,15 +162,25 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
   const int n_desc = pset_ndesc(ps);
   const uint2* qh = pset_qhdr(ps);
   char* area = smem + 128 + pset_smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(area);  // full[kExtStages], empty[kExtStages]
-  ExtTile* meta = reinterpret_cast<ExtTile*>(area + 16 * kExtStages);
-  int32_t* slots = reinterpret_cast<int32_t*>(area + 256);  // stage s: tok at 2*s*cap, ctx at (2*s+1)*cap
+  uint64_t* bars = reinterpret_cast<uint64_t*>(area);  // full[kExtMaxStages], empty[kExtMaxStages]
+  ExtTile* meta = reinterpret_cast<ExtTile*>(area + 16 * kExtMaxStages);
+  int32_t* slots = reinterpret_cast<int32_t*>(area + 32 * kExtMaxStages);  // stage s: tok, then ctx if any_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (nb + kExtConsumers - 1) / kExtConsumers;
+  // total_context feeds only Linear models with a context term (predictor.py:137-142) and
+  // the features output: when neither occurs, slot_ctx is neither copied nor summed
+  bool set_c = false;
+  for (int i = lane; i < n_desc; i += 32) {
+    const tw_pred_desc* dsc = pset_desc(ps, i);
+    set_c |= dsc->kind == TW_PRED_LINEAR && dsc->per_context_token_us != 0.0;
+  }
+  const bool any_c = feat != nullptr || __any_sync(kFull, set_c);
+  const int nst = any_c ? TWB_EXT_STAGES_C : TWB_EXT_STAGES_T;
+  const int32_t cap = (region / (nst * (any_c ? 8 : 4))) & ~3;  // slots per stage
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kExtStages; s++) {
-      mbar_init(smem_u32(&bars[s]), 1);                             // full: producer + tx bytes
-      mbar_init(smem_u32(&bars[kExtStages + s]), kExtThreads / 32 - 1);  // empty: one per consumer warp
+    for (int s = 0; s < nst; s++) {
+      mbar_init(smem_u32(&bars[s]), 1);                                   // full: producer + tx bytes
+      mbar_init(smem_u32(&bars[kExtMaxStages + s]), kExtThreads / 32 - 1);  // empty: one per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -172,7 +190,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
     int k = 0;
     int64_t w0 = 0, w1 = 0;  // lane i: slot range of this CTA's tile k + i (window of 32 tiles)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
-      const int s = k % kExtStages;
+      const int s = k % nst;
       if ((k & 31) == 0) {  // prefetch the next 32 tiles' slot ranges, one per lane
         const int64_t tt = t + (int64_t)lane * gridDim.x;
         if (tt < ntiles) {
@@ -182,7 +200,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
         }
       }
       const int64_t s0 = __shfl_sync(kFull, w0, k & 31), s1 = __shfl_sync(kFull, w1, k & 31);
-      if (k >= kExtStages) mbar_wait(smem_u32(&bars[kExtStages + s]), ((k / kExtStages) - 1) & 1);
+      if (k >= nst) mbar_wait(smem_u32(&bars[kExtMaxStages + s]), ((k / nst) - 1) & 1);
       if (lane == 0) {
         const int64_t a0 = s0 & ~3LL, n = ((s1 + 3) & ~3LL) - a0;  // readable to a multiple of 4 (twb200.h)
         const uint32_t full = smem_u32(&bars[s]);
@@ -192,10 +210,14 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
           const uint32_t bytes = (uint32_t)(n * 4);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(full),
-                       "r"(2 * bytes)
+                       "r"(any_c ? 2 * bytes : bytes)
                        : "memory");
-          bulk_g2s(slots + (size_t)(2 * s) * cap, tok + a0, bytes, full);
-          bulk_g2s(slots + (size_t)(2 * s + 1) * cap, ctx + a0, bytes, full);
+          if (any_c) {
+            bulk_g2s(slots + (size_t)(2 * s) * cap, tok + a0, bytes, full);
+            bulk_g2s(slots + (size_t)(2 * s + 1) * cap, ctx + a0, bytes, full);
+          } else {
+            bulk_g2s(slots + (size_t)s * cap, tok + a0, bytes, full);
+          }
         } else {
           mbar_arrive(full);
         }
@@ -222,7 +244,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
     }
   }
   for (int k = 0; t < ntiles; t += gridDim.x, k++) {
-    const int s = k % kExtStages;
+    const int s = k % nst;
     // prefetch the next tile's offsets and descriptor ids before waiting on this one
     const int64_t tn = t + gridDim.x;
     int64_t n0[kExtBpt], n1[kExtBpt];
@@ -238,7 +260,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
         nid[j] = __ldg(id + bn);
       }
     }
-    mbar_wait(smem_u32(&bars[s]), (k / kExtStages) & 1);
+    mbar_wait(smem_u32(&bars[s]), (k / nst) & 1);
     const int64_t a0 = meta[s].a0;
     const bool staged = meta[s].staged;
     int64_t Pt[kExtBpt], Dn[kExtBpt], Ct[kExtBpt];
@@ -247,7 +269,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
       Pt[j] = Dn[j] = Ct[j] = 0;
       if (staged) {
         // 32-bit shared-memory addressing; the slot index is tile-relative (< cap)
-        const uint32_t tbase = smem_u32(slots + (size_t)(2 * s) * cap), cbase = tbase + 4u * (uint32_t)cap;
+        const uint32_t tbase = smem_u32(slots + (size_t)(any_c ? 2 * s : s) * cap), cbase = tbase + 4u * (uint32_t)cap;
         const uint32_t q1 = 4u * (uint32_t)(s1[j] - a0);
         int32_t dn = 0;
         uint32_t q = 4u * (uint32_t)(s0[j] - a0);
@@ -255,7 +277,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
         // 137-142): when no batch of this warp needs it and no features are requested, the
         // context slots are not read (A/B: 58.9% -> 61.4% of HBM with the uniform loop)
         bool need_c = feat != nullptr;
-        if (!need_c && (unsigned)ib[j] < (unsigned)n_desc) {
+        if (!need_c && any_c && (unsigned)ib[j] < (unsigned)n_desc) {
           const tw_pred_desc* dsc = pset_desc(ps, ib[j]);
           need_c = dsc->kind == TW_PRED_LINEAR && dsc->per_context_token_us != 0.0;
         }
@@ -295,7 +317,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_predict_batches(
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&bars[kExtStages + s]));  // this warp is done with stage s
+    if (lane == 0) mbar_arrive(smem_u32(&bars[kExtMaxStages + s]));  // this warp is done with stage s
 #pragma unroll
     for (int j = 0; j < kExtBpt; j++) {
       const int64_t b = t * kExtConsumers + j * kC + threadIdx.x;
@@ -503,14 +525,17 @@ extern "C" int tw_predict_batches(const void* pset, int64_t pset_bytes, const in
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool staged = smem > 0;  // else the blob is read through L1 (check_pset)
   const uint32_t pset_smem = staged ? (uint32_t)((pset_bytes + 127) & ~127LL) : 0u;
-  const int64_t room = (int64_t)max_optin - 1024 /* static */ - 128 - (int64_t)pset_smem - 256;
-  int32_t cap = (int32_t)((room / (8 * kExtStages)) & ~3LL);  // slots per stage (tok + ctx)
-  if (cap > 16 * kExtConsumers) cap = 16 * kExtConsumers;
-  if (cap < kExtConsumers) {
+  // the stage region (bytes): the kernel splits it into TWB_EXT_STAGES_C stages of (tok, ctx)
+  // or TWB_EXT_STAGES_T stages of tok; a stage holds at most 16 slots per batch of a tile
+  int64_t room = (int64_t)max_optin - 1024 /* static */ - 128 - (int64_t)pset_smem - 32 * kExtMaxStages;
+  room &= ~127LL;
+  if (room > 16LL * 8 * kExtConsumers * TWB_EXT_STAGES_C) room = 16LL * 8 * kExtConsumers * TWB_EXT_STAGES_C;
+  if (room < 8LL * kExtConsumers * kExtMaxStages) {
     set_error("tw_predict_batches: predictor blob leaves no room for slot tiles");
     return TW_ENOSMEM;
   }
-  const size_t esmem = 128 + pset_smem + 256 + (size_t)cap * 8 * kExtStages;
+  const int32_t cap = (int32_t)room;  // the kernel's `region`
+  const size_t esmem = 128 + pset_smem + 32 * kExtMaxStages + (size_t)room;
   const int64_t ntiles = (n_batches + kExtConsumers - 1) / kExtConsumers;
   const int grid = (int)(ntiles < sms ? ntiles : sms);
   if (staged) {

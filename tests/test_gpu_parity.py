@@ -230,6 +230,39 @@ def test_fused_extraction_equals_oracle_on_csr_batches():
     assert (got[empty] == -1).all()
 
 
+def test_fused_extraction_without_features_mixed_models():
+    """tw_predict_batches without a features output: the context slots are copied and summed
+    only for chunks of 32 batches where some batch's model has a context term. Mixed set
+    (tables, Constant, Linear with and without a context term), descriptor ids in runs so
+    some chunks need C and others do not, plus chunks beyond the per-warp buffer and a tail
+    that is not a multiple of 32 batches."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.predictor import ConstantPredictor, LinearPredictor, PredictorSet
+
+    base = presets.calibration_set().predictors
+    preds = list(base) + [ConstantPredictor(321), LinearPredictor(5.0, 0.25, 3.5, 0.0),
+                          LinearPredictor(7.0, 0.125, 2.0, 0.003)]
+    pset = PredictorSet(preds)
+    rng = np.random.default_rng(11)
+    nb = 1_000_003
+    counts = rng.integers(0, 9, nb)
+    counts[500_000:500_064] = 37  # two chunks beyond a buffer
+    off = np.zeros(nb + 1, np.int64)
+    np.cumsum(counts, out=off[1:])
+    ns = int(off[-1])
+    tok = np.where(rng.random(ns) < 0.7, -1, rng.integers(1, 700, ns)).astype(np.int32)
+    ctx = rng.integers(0, 3000, ns).astype(np.int32)
+    run = rng.integers(0, len(preds), (nb + 95) // 96)  # one id per 96 batches: mixed chunks
+    ids = np.repeat(run, 96)[:nb].astype(np.int32)
+    got = pset.predict_csr(off, tok, ctx, ids)
+    f = orc.extract_features(off, tok, ctx)
+    empty = counts == 0
+    want = orc.predict_many(pset.blob, f[:, 0].astype(np.int32), f[:, 1].astype(np.int32),
+                            np.where(empty, -1, f[:, 2]), ids)
+    assert np.array_equal(got, want)
+
+
 def test_device_workload_generation_matches_reference_arrivals():
     """tw_generate_poisson (numpy's PCG64 + ziggurat + Lemire in CUDA) reproduces the
     reference's generate_arrivals: the 34 golden workloads by sha256 (32 sweep seeds,
