@@ -461,7 +461,7 @@ def cpu_baseline(sw, budget_s: float, n_threads: int):
     return {
         "value": round(vsec / t_est, 1), "unit": "virtual-s/wall-s", "cores": n_threads, "kind": "port",
         "sample": f"{take} of {n} configs (evenly spaced), C oracle (oracle/twb_oracle.c) on {n_threads} host threads",
-        "predictions_per_s": round(steps / t_est, 1), "seconds": round(t_est, 3),
+        "steps_per_s": round(steps / t_est, 1), "seconds": round(t_est, 3),
     }
 
 
@@ -613,7 +613,7 @@ def run_reference(args):
         "impl": "reference", "metric": "emulated virtual-sec/wall-sec over config sweep", "value": round(v, 1),
         "unit": "virtual-s/wall-s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int64+f64",
-        "data": "synthetic", "config": config, "predictions_per_s": round(statistics.median(preds), 1),
+        "data": "synthetic", "config": config, "steps_per_s": round(statistics.median(preds), 1),
         "cpu_baseline": {"value": round(v, 1), "unit": "virtual-s/wall-s", "cores": threads, "kind": "port",
                          "sample": f"{sample} configs per step of {n} (C oracle restating oracle.simulate)"},
         "e2e": {"value": round(v, 1), "unit": "virtual-s/wall-s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -845,7 +845,7 @@ def measure_sweep(sw, args, world, rank, device, cdev, dist_on, label):
         res["merged"] = m
     res["e2e"] = {"value": round(vsec / (e_ms / 1e3), 1), "unit": "virtual-s/wall-s",
                   "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": int(d2h),
-                  "ms_per_step": round(e_ms, 4), "predictions_per_s": round(steps / (e_ms / 1e3), 1),
+                  "ms_per_step": round(e_ms, 4), "steps_per_s": round(steps / (e_ms / 1e3), 1),
                   "outputs": ("zero-copy: the kernel stores records and stamps into pinned host memory"
                               if host.zero_copy else
                               "streamed: records into pinned host memory, and each finished prefix of configs' stamps "

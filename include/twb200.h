@@ -82,7 +82,11 @@ extern "C" {
 #define TW_PRED_CONSTANT 0        /* predictor.py:100-111 */
 #define TW_PRED_LINEAR 1          /* predictor.py:114-146 */
 #define TW_PRED_TABLE 2           /* predictor.py:149-242 */
-#define TW_TABLE_HOLE (-1)
+/* grid cell with no calibration row (table values may be negative: TablePredictor(rows)
+ * accepts them, predictor.py:164-170; only from_csv rejects them); the int32 copy of a
+ * grid, present only when every value lies in [0, 2^31), marks holes with -1 */
+#define TW_TABLE_HOLE (-9223372036854775807LL - 1)
+#define TW_TABLE_HOLE32 (-1)
 
 typedef struct tw_pset_header {
   uint32_t magic;
@@ -111,6 +115,8 @@ typedef struct tw_pred_desc {
 
 /* ---- bulk predictor (kernel 2 of the north star) -------------------------- */
 /* out_ns[i] = predict(features i) in ns (multiple of 1000) or a TW_PRED_* code.
+ * Durations are whole microseconds x 1000, so a value < 0 that is a multiple of 1000 is a
+ * (negative) duration from a table with negative rows and any other value < 0 is a code.
  * Features are the reference's BatchComposition totals (predictor.py:69-84):
  * P = total_prefill_tokens, D = num_decodes, C = total_context; a batch is empty
  * iff it has no slots, which the feature-only entry point encodes as
@@ -276,9 +282,12 @@ typedef struct tw_sim_result {
   int64_t steps;        /* non-empty batches = predictions */
   int64_t events;       /* token events emitted */
   uint64_t digest;      /* order-sensitive digest of the event stream (tw_event_hash) */
-  int64_t tk_seq;       /* Timekeeper CLOCK_UPDATE count (TW_SIM_TIMEKEEPER) */
-  int64_t tk_offset_ns; /* final Timekeeper offset */
-  int64_t tk_wall_ns;   /* final FakeClock wall */
+  int64_t tk_seq;       /* Timekeeper CLOCK_UPDATE count (TW_SIM_TIMEKEEPER)            */
+  int64_t tk_offset_ns; /* final Timekeeper offset                                       */
+  int64_t tk_wall_ns;   /* final FakeClock wall. The three tk_* fields are the IDEALIZED */
+                        /* protocol (workers between steps or parked count as exempt):   */
+                        /* the minimum wall a live run needs; DESIGN.md §5 measures the  */
+                        /* reference live stack against it                               */
   int32_t status;       /* TW_SIM_* (+ overflow bit) */
   int32_t pred_code;    /* TW_PRED_* when status == TW_SIM_PRED_ERROR */
 } tw_sim_result;        /* 64 B */

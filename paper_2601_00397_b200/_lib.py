@@ -24,7 +24,7 @@ TW_PRED_EMPTY_BATCH, TW_PRED_NEGATIVE, TW_PRED_TABLE_MISS, TW_PRED_BAD_DESC = -1
 TW_PRED_NAN, TW_PRED_OVERFLOW = -5, -6
 TW_PSET_MAGIC = 0x54534550
 TW_PRED_CONSTANT, TW_PRED_LINEAR, TW_PRED_TABLE = 0, 1, 2
-TW_TABLE_HOLE = -1
+TW_TABLE_HOLE = -(2**63)  # int64 grid; the int32 copy uses -1 (twb200.h)
 TW_QHDR_FAST = 0x80000000
 
 TW_OP_REGISTER_ACTOR, TW_OP_REGISTER_OBSERVER, TW_OP_SEAL, TW_OP_JUMP = 0, 1, 2, 3

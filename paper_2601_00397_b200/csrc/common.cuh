@@ -303,15 +303,16 @@ __device__ __forceinline__ int64_t table_corners32(const TableView& t, int p0, i
   return us_to_ns_rn(us);
 }
 
-// bilinear evaluation from bracket indices and their axis values; holes (-1) are the
-// only negative grid entries, so one OR of the corners detects any of them
+// bilinear evaluation from bracket indices and their axis values (int64 grid: values may
+// be negative, holes are TW_TABLE_HOLE)
 __device__ __forceinline__ int64_t table_corners2(const TableView& t, int p0, int p1, int d0, int d1, int64_t P0,
                                                   int64_t P1, int64_t D0, int64_t D1, int64_t P, int64_t D) {
   const int64_t c00 = t.grid[p0 * t.nd + d0];
   const int64_t c10 = t.grid[p1 * t.nd + d0];
   const int64_t c01 = t.grid[p0 * t.nd + d1];
   const int64_t c11 = t.grid[p1 * t.nd + d1];
-  if ((c00 | c10 | c01 | c11) < 0) return TW_PRED_TABLE_MISS;
+  if (c00 == TW_TABLE_HOLE || c10 == TW_TABLE_HOLE || c01 == TW_TABLE_HOLE || c11 == TW_TABLE_HOLE)
+    return TW_PRED_TABLE_MISS;
   double us;
   if (P1 == P0) {
     us = (D1 == D0) ? __ll2double_rn(c00) : lerp_int(c00, c01, D0, D1, D, t.rd[d0]);

@@ -849,7 +849,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     pred_cyc += TWB_CLK() - q3;
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
-      r.pred_code = (int32_t)d;
+      r.pred_code = (d % 1000 != 0) ? (int32_t)d : TW_PRED_NEGATIVE;  // a negative table row: engine limit
       break;
     }
 

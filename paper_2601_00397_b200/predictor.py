@@ -117,9 +117,17 @@ class HardwareSpec:
     parameters: dict = field(default_factory=dict)
 
 
+def is_code(values):
+    """True where a kernel output is a TW_PRED_* code rather than a duration: durations are
+    whole microseconds x 1000 (negative ones come from tables with negative rows), the
+    codes are small negatives that are not multiples of 1000 (twb200.h)."""
+    v = np.asarray(values)
+    return (v < 0) & (v % 1000 != 0)
+
+
 def raise_for_code(code: int, context: str = "") -> None:
     """Map a kernel's per-element code to the reference exception (predictor.py:27-44)."""
-    if code >= 0:
+    if code >= 0 or code % 1000 == 0:  # a duration (negative only from a table's own rows)
         return
     if code == TW_PRED_EMPTY_BATCH:
         raise EmptyBatch("cannot predict a duration for an empty batch")
@@ -174,9 +182,11 @@ class _DevicePredictor:
     def predict_many(self, batches: Sequence, raise_errors: bool = True) -> np.ndarray:
         """Bulk prediction over many batch compositions in one launch."""
         out = self.predictor_set.predict_batches(batches, np.zeros(len(batches), np.int32))
-        if raise_errors and len(out) and out.min() < 0:
-            i = int(np.argmin(out))
-            raise_for_code(int(out[i]), _describe(batches[i]))
+        if raise_errors and len(out):
+            bad = np.flatnonzero(is_code(out))
+            if bad.size:
+                i = int(bad[0])
+                raise_for_code(int(out[i]), _describe(batches[i]))
         return out
 
 
@@ -248,10 +258,8 @@ class TablePredictor(_DevicePredictor):
         for (p, d), v in self._rows.items():
             if not (-(2**31) <= p < 2**31 and -(2**31) <= d < 2**31):
                 raise TableParseError(f"table key {(p, d)} outside the int32 range of the device grid")
-            if v < 0:
-                # The reference only rejects negatives in from_csv; the device grid
-                # reserves negative values for holes and error codes.
-                raise NegativeDuration(f"table value {v}us at {(p, d)} is negative")
+            # negative values are valid rows (the reference rejects them only in from_csv):
+            # predictions are then negative multiples of 1000 ns (is_code tells codes apart)
         # exactness of the int lerp numerator on device: |(b-a)*(x-lo)| < 2^53
         vals = list(self._rows.values())
         span = max(vals) - min(vals)
@@ -421,12 +429,13 @@ class PredictorSet:
                                for k in range(len(dax))], np.float64)
                 blob = axes + grid.tobytes() + rp.tobytes() + rd.tobytes()
                 blob += _bitlen_lut(pax).tobytes() + _bitlen_lut(dax).tobytes()
-                # int32 copy of the grid for the bulk kernel's gathers (half the bytes);
-                # tables with values >= 2^31 us carry none and use the int64 grid
-                small = bool(grid.max() < 2**31)
+                # int32 copy of the grid for the bulk kernel's gathers (half the bytes;
+                # holes -1): only for values in [0, 2^31), others use the int64 grid
+                vals = grid[grid != TW_TABLE_HOLE]
+                small = bool(vals.size and vals.min() >= 0 and vals.max() < 2**31)
                 descs[i]["pad"] = 1 if small else 0
                 if small:
-                    blob += grid.astype(np.int32).tobytes()
+                    blob += np.where(grid == TW_TABLE_HOLE, -1, grid).astype(np.int32).tobytes()
                 blob += b"\0" * (_align(len(blob), 16) - len(blob))
                 descs[i]["table_off"] = cursor
                 pool.append(blob)
@@ -451,14 +460,14 @@ class PredictorSet:
             pax, dax, grid = tab
             if not (descs[i]["pad"] == 1 and pax[0] >= 0 and dax[0] >= 0
                     and len(pax) < 2**15 and len(dax) < 2**15):
-                continue  # generic path only (int64-grid or negative-axis tables)
+                continue  # generic path only (int64-grid, negative-valued or negative-axis tables)
             need = 16 * len(pax) * len(dax) + sum(
                 32 * 16 for a in (pax, dax) if np.asarray(a, np.int32).tobytes() not in sets)
             if core + len(fast) + need > PSET_SMEM_BUDGET:
                 continue  # the whole blob must fit the kernels' shared-memory staging budget
             prec, drec = axis_set(pax), axis_set(dax)
             quads = core + len(fast)
-            fast.extend(_quads(grid.astype(np.int32)).tobytes())
+            fast.extend(_quads(np.where(grid == TW_TABLE_HOLE, -1, grid).astype(np.int32)).tobytes())
             qhdr[i, 0] = (quads // 16) | ((prec // 16) << 16)
             qhdr[i, 1] = (drec // 16) | (len(dax) << 16) | TW_QHDR_FAST
         fast[: qhdr.nbytes] = qhdr.tobytes()

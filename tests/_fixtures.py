@@ -28,8 +28,9 @@ def _npz(name):
 
 
 @functools.lru_cache(maxsize=None)
-def predictor_golden():
-    z = _npz("predictor.npz")
+def predictor_golden(name: str = "predictor.npz"):
+    """predictor.npz; predictor_neg.npz: tables with negative rows."""
+    z = _npz(name)
     specs = json.loads(bytes(z["specs"]).decode())
     preds = [predictor_from_spec(s) for s in specs]
     return specs, preds, z["P"], z["D"], z["C"], z["desc"], z["expected"]

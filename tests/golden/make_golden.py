@@ -11,6 +11,7 @@ file. The GPU box never reads /root/reference: tests only read these fixtures.
 
 Fixtures:
   predictor.npz  queries -> reference predict() ns / exception, per predictor case
+  predictor_neg.npz  the same for tables with negative rows (TablePredictor(rows))
   barrier.npz    BarrierCore op streams (run_random_schedule seeds 0-999, the
                  scripted replay harness, hand-written scenarios) -> acks,
                  broadcast/release events, final state
@@ -160,6 +161,60 @@ def make_predictor_golden(rng):
         desc=np.asarray(I, np.int32), expected=np.asarray(E, np.int64),
     )
     print("predictor:", len(cases), "cases,", len(P), "queries,", sum(e < 0 for e in E), "error codes")
+
+
+def make_predictor_neg_golden():
+    """predictor_neg.npz: TablePredictor(rows) with NEGATIVE values, which the reference
+    accepts (it only rejects them in from_csv, predictor.py:164-192): predictions are then
+    negative multiples of 1000 ns. Includes a -1 us row (the round-1 device hole marker),
+    holes, exact hits, interpolation and nearest-row extrapolation. Same layout as
+    predictor.npz; its own seed, so predictor.npz is unchanged."""
+    rng = np.random.default_rng(397_2)
+    cases = []
+    mixed = {(0, 1): -100, (0, 8): 800, (512, 1): -2000, (512, 8): 3000, (1024, 1): -1, (1024, 8): -5200}
+    holey = {(0, 1): -1, (512, 1): -2000, (512, 8): 3000, (2048, 4): -7}
+    for rows, name in ((mixed, "neg_mixed"), (holey, "neg_holey")):
+        for ext in (False, True):
+            cases.append(({"kind": "table", "rows": rows, "ext": ext, "name": f"{name}_ext{int(ext)}"},
+                          ref_pred.TablePredictor(rows, allow_extrapolation=ext)))
+    for k in range(4):
+        pax = sorted(set(int(x) for x in rng.integers(0, 5000, size=int(rng.integers(2, 12)))))
+        dax = sorted(set(int(x) for x in rng.integers(0, 300, size=int(rng.integers(2, 12)))))
+        lo, hi = (-200_000, 200_000) if k % 2 else (-300_000, 0)
+        rows = {(p, d): int(rng.integers(lo, hi)) for p in pax for d in dax if rng.random() < 0.75}
+        if not rows:
+            rows[(pax[0], dax[0])] = -3
+        ext = bool(k // 2)
+        cases.append(({"kind": "table", "rows": rows, "ext": ext, "name": f"neg_random_{k}"},
+                      ref_pred.TablePredictor(rows, allow_extrapolation=ext)))
+    specs, P, D, C, I, E = [], [], [], [], [], []
+    for ci, (spec, pred) in enumerate(cases):
+        specs.append({**spec, "rows": [[k[0], k[1], v] for k, v in spec["rows"].items()]})
+        ps = sorted({k[0] for k in spec["rows"]})
+        ds = sorted({k[1] for k in spec["rows"]})
+        n = 3000
+        qp = rng.integers(0, ps[-1] + 200, size=n)
+        qd = rng.integers(0, ds[-1] + 20, size=n)
+        k = n // 4
+        qp[:k] = rng.choice(ps, size=k)
+        qd[k : 2 * k] = rng.choice(ds, size=k)
+        qc = rng.integers(0, 600_000, size=n)
+        for p, d, c in zip(qp.tolist(), qd.tolist(), qc.tolist()):
+            P.append(p)
+            D.append(d)
+            C.append(c)
+            I.append(ci)
+            E.append(ref_predict(pred, p, d, c))
+    np.savez_compressed(
+        os.path.join(HERE, "predictor_neg.npz"),
+        specs=np.frombuffer(json.dumps(specs).encode(), np.uint8),
+        P=np.asarray(P, np.int32), D=np.asarray(D, np.int32), C=np.asarray(C, np.int64),
+        desc=np.asarray(I, np.int32), expected=np.asarray(E, np.int64),
+    )
+    neg = sum(1 for e in E if e < 0 and e % 1000 == 0)
+    print("predictor_neg:", len(cases), "cases,", len(P), "queries,", neg, "negative durations,",
+          sum(1 for e in E if e < 0 and e % 1000), "error codes")
+
 
 
 # ------------------------------------------------------------------------------
@@ -1058,10 +1113,13 @@ def make_metrics_golden():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"predictor", "barrier", "oracle", "tkgrid", "arrivals", "metrics", "core", "wide"}
+    which = set(sys.argv[1:]) or {"predictor", "predictor_neg", "barrier", "oracle", "tkgrid", "arrivals", "metrics",
+                                  "core", "wide"}
     rng = np.random.default_rng(20260100397)
     if "predictor" in which:
         make_predictor_golden(rng)
+    if "predictor_neg" in which:
+        make_predictor_neg_golden()
     if "barrier" in which:
         make_barrier_golden()
     if "arrivals" in which:

@@ -41,6 +41,30 @@ def test_predict_features_matches_reference_vectors():
     assert bad.size == 0, [(specs[desc[i]]["name"], P[i], D[i], C[i], got[i], expected[i]) for i in bad[:5]]
 
 
+def test_negative_table_rows_match_reference():
+    """Tables with negative rows (TablePredictor(rows) accepts them; only from_csv rejects
+    them): the bulk kernel, the fused CSR kernel and the drop-in predict() return the
+    reference's negative multiples of 1000 ns; codes stay distinguishable (is_code)."""
+    from paper_2601_00397_b200.predictor import BatchComposition, DecodeSlot, PredictorSet, is_code
+
+    specs, preds, P, D, C, desc, expected = predictor_golden("predictor_neg.npz")
+    pset = PredictorSet(preds)
+    got = pset.predict_features(P, D, C, desc)
+    assert np.array_equal(got, expected)
+    neg = np.flatnonzero((expected < 0) & ~is_code(expected))
+    assert neg.size > 1000
+    for i in neg[:: max(1, neg.size // 40)]:  # drop-in predict() on decode-only batches
+        if C[i] >= 0 and P[i] == 0 and D[i] > 0:
+            b = BatchComposition((), tuple(DecodeSlot(f"r{k}", 1) for k in range(int(D[i]))))
+            assert preds[desc[i]].predict(b) == expected[i]
+    # CSR: one decode slot per batch (P = 0, D = 1)
+    sel = np.flatnonzero((P == 0) & (D == 1))
+    off = np.arange(len(sel) + 1, dtype=np.int64)
+    tok = np.full(len(sel) + 4, -1, np.int32)
+    ctx = np.ones(len(sel) + 4, np.int32)
+    assert np.array_equal(pset.predict_csr(off, tok, ctx, desc[sel]), expected[sel])
+
+
 def test_predict_features_equals_oracle_on_random_sweep():
     """>= 10^6 random queries against the C oracle."""
     from oracle import oracle as orc
@@ -998,6 +1022,20 @@ def test_drop_in_simulate_matches_reference_timeline():
         simulate([Arrival("r00000", 0, 256, 1)], EngineConfig(chunk_size=512, max_batch_tokens=1024, max_running=8,
                                                               kv_block_tokens=16, kv_capacity_blocks=8),
                  ConstantPredictor(10_000))
+
+
+def test_simulate_with_negative_table_duration_raises():
+    """A step whose predicted duration is negative (a table with negative rows) stops the
+    event loop with NegativeDuration: the engine's one deliberate limit here (the
+    reference's oracle.simulate would move its clock backwards)."""
+    from paper_2601_00397_b200.predictor import NegativeDuration, TablePredictor
+    from paper_2601_00397_b200.sweep import EngineConfig, simulate
+    from paper_2601_00397_b200.workload import Arrival
+
+    pred = TablePredictor({(0, 0): -5, (0, 8): -5, (512, 0): -5, (512, 8): -5})
+    arrivals = [Arrival(f"r{i}", i * 1000, 100, 4) for i in range(4)]
+    with pytest.raises(NegativeDuration):
+        simulate(arrivals, EngineConfig(), pred)
 
 
 def test_drop_in_simulate_with_zero_and_negative_outputs():

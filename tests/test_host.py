@@ -7,6 +7,8 @@ import subprocess
 import numpy as np
 import pytest
 
+from paper_2601_00397_b200._lib import TW_TABLE_HOLE
+
 from paper_2601_00397_b200 import _lib, calibration, presets
 from paper_2601_00397_b200._lib import PRED_DESC_DTYPE, PSET_HEADER_DTYPE
 from paper_2601_00397_b200.predictor import (
@@ -87,12 +89,14 @@ def test_pset_blob_layout_round_trips():
     g0 = off + ((4 * (np_ + nd) + 7) // 8) * 8
     grid = blob[g0 : g0 + 8 * np_ * nd].view(np.int64).reshape(np_, nd)
     assert pax.tolist() == [0, 512] and dax.tolist() == [1, 8]
-    assert grid.tolist() == [[100, -1], [2000, 3000]]
+    assert grid.tolist() == [[100, TW_TABLE_HOLE], [2000, 3000]]
 
 
 def test_predictor_construction_errors_mirror_reference(tmp_path):
     with pytest.raises(TableParseError):
         TablePredictor({})
+    # negative rows are valid through the constructor (only from_csv rejects them)
+    assert TablePredictor({(0, 1): -5, (8, 1): 3})._rows[(0, 1)] == -5
     with pytest.raises(NegativeDuration):
         build_predictor({"kind": "constant", "duration_us": -1})
     with pytest.raises(PredictorError):
@@ -268,10 +272,12 @@ def test_bulk_lookup_section_decodes_to_the_tables():
     for k, p in enumerate(ps.predictors):
         tab = p._table()
         if not (int(qh[k, 1]) & _lib.TW_QHDR_FAST):
-            assert tab is None or tab[2].max() >= 2**31 or tab[0][0] < 0 or tab[1][0] < 0
+            assert tab is None or tab[2].max() >= 2**31 or tab[0][0] < 0 or tab[1][0] < 0 or \
+                tab[2][tab[2] != TW_TABLE_HOLE].min() < 0
             continue
         n_fast += 1
         pax, dax, grid = tab
+        grid = np.where(grid == TW_TABLE_HOLE, -1, grid)  # the int32 quads mark holes with -1
         nd = (int(qh[k, 1]) >> 16) & 0x7FFF
         assert nd == len(dax)
         quads = int(qh[k, 0]) & 0xFFFF

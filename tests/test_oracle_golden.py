@@ -41,6 +41,15 @@ def test_oracle_predictor_matches_reference():
     assert bad.size == 0, [(specs[desc[i]]["name"], P[i], D[i], C[i], got[i], expected[i]) for i in bad[:5]]
 
 
+def test_oracle_predictor_negative_rows_match_reference():
+    """TablePredictor(rows) with negative values (the reference accepts them outside
+    from_csv): negative multiples of 1000 ns, a -1 us row that is not a hole."""
+    specs, preds, P, D, C, desc, expected = predictor_golden("predictor_neg.npz")
+    got = orc.predict_many(PredictorSet(preds).blob, P, D, C, desc)
+    assert np.array_equal(got, expected)
+    assert ((expected < 0) & (expected % 1000 == 0)).any()
+
+
 def test_oracle_predictor_empty_batch_code():
     specs, preds, *_ = predictor_golden()
     blob = PredictorSet(preds).blob
