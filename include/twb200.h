@@ -193,6 +193,9 @@ int tw_selftest_division(int64_t n, uint64_t seed, unsigned long long* mismatche
 
 #define TW_TK_MAX_CLIENTS 32
 #define TW_TK_MAX_GROUPS 32
+/* tw_tk_replay_wide: the same replay for streams with up to 1,024 clients and 64 groups */
+#define TW_TK_MAX_CLIENTS_WIDE 1024
+#define TW_TK_MAX_GROUPS_WIDE 64
 
 typedef struct tw_tk_op {
   int64_t arg;
@@ -229,6 +232,14 @@ int tw_tk_replay(const tw_tk_op* ops, const int64_t* op_off, int32_t n_streams,
                  const int64_t* wall0_ns, const int64_t* cooldown_ns,
                  const uint8_t* suppress, int32_t* ack, tw_tk_event* ev,
                  const int64_t* ev_off, tw_tk_final* fin, void* stream);
+
+/* The same replay for wide streams (up to TW_TK_MAX_CLIENTS_WIDE clients and
+ * TW_TK_MAX_GROUPS_WIDE groups; BarrierCore has no limit): one warp per stream with its
+ * client and group state in shared memory, lanes striding over clients. */
+int tw_tk_replay_wide(const tw_tk_op* ops, const int64_t* op_off, int32_t n_streams,
+                      const int64_t* wall0_ns, const int64_t* cooldown_ns,
+                      const uint8_t* suppress, int32_t* ack, tw_tk_event* ev,
+                      const int64_t* ev_off, tw_tk_final* fin, void* stream);
 
 /* Bulk min-advance (the _try_resolve/_resolve arithmetic, timekeeper.py:318-366)
  * for C independent Timekeepers with A actor slots each, one round:

@@ -41,7 +41,9 @@ ACK_NAMES = {
     8: "EngineLimit",
 }
 TW_TK_MAX_CLIENTS = 32
+TW_TK_MAX_CLIENTS_WIDE = 1024
 TW_TK_MAX_GROUPS = 32
+TW_TK_MAX_GROUPS_WIDE = 64
 
 TW_POLICY_MIXED, TW_POLICY_PREFILL_PRIORITIZED = 0, 1
 TW_SIM_TIMEKEEPER = 1
@@ -176,6 +178,7 @@ EXPORTED_SYMBOLS = (
     "tw_service_stop",
     "tw_selftest_division",
     "tw_tk_replay",
+    "tw_tk_replay_wide",
     "tw_tk_resolve",
     "tw_sim_many",
     "tw_sim_scratch_bytes",
@@ -221,6 +224,7 @@ _SIGNATURES = {
     "tw_service_stop": (_I32, [_P]),
     "tw_selftest_division": (_I32, [_I64, ctypes.c_uint64, _P, _P]),
     "tw_tk_replay": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "tw_tk_replay_wide": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tw_tk_resolve": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),
     "tw_sim_many": (
         _I32,

@@ -600,7 +600,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   if (cfg.chunk_size < 1 || cfg.max_batch_tokens < cfg.chunk_size || cfg.kv_block_tokens < 1 ||
       cfg.kv_capacity_blocks < 1 || TP < 1 || S < 1 || (cfg.policy != 0 && cfg.policy != 1)) {
     r.status = TW_SIM_BAD_CONFIG;  // engine.py:109-120
-  } else if (cfg.max_running > p.cap || (tk_on && 1 + TP * S > 32)) {
+  } else if (cfg.max_running > p.cap) {
     r.status = TW_SIM_CAPACITY;
   }
   if (r.status != TW_SIM_OK) {

@@ -37,7 +37,9 @@ from ._lib import (
     TW_OP_REGISTER_OBSERVER,
     TW_OP_SEAL,
     TW_TK_MAX_CLIENTS,
+    TW_TK_MAX_CLIENTS_WIDE,
     TW_TK_MAX_GROUPS,
+    TW_TK_MAX_GROUPS_WIDE,
 )
 
 DEFAULT_COOLDOWN_NS = 500_000  # timekeeper.py:36
@@ -105,8 +107,8 @@ class OpStream:
     def enter(self, client_id: str, group: str, expected: int) -> None:
         c, ok = self._client(client_id)
         g = self._groups.setdefault(group, len(self._groups))
-        if g >= TW_TK_MAX_GROUPS:
-            raise ValueError(f"more than {TW_TK_MAX_GROUPS} collective groups in one stream")
+        if g >= TW_TK_MAX_GROUPS_WIDE:
+            raise ValueError(f"more than {TW_TK_MAX_GROUPS_WIDE} collective groups in one stream")
         self._op(TW_OP_ENTER if ok else TW_OP_BAD_CLIENT, expected, c, g)
 
     def deregister(self, client_id: str) -> None:
@@ -153,8 +155,10 @@ def ack_name(code: int):
     return ACK_NAMES.get(int(code), f"code{code}")
 
 
-def replay_arrays(ops, op_off, wall0, cooldown, suppress=None, ev_cap_per_stream=4096, device=None) -> ReplayResult:
-    """Replay packed op streams on the GPU (tw_tk_replay)."""
+def replay_arrays(ops, op_off, wall0, cooldown, suppress=None, ev_cap_per_stream=4096, device=None,
+                  wide: bool = False) -> ReplayResult:
+    """Replay packed op streams on the GPU (tw_tk_replay; tw_tk_replay_wide for streams with
+    more than 32 clients or groups)."""
     import torch
 
     from ._device import require_cuda, stream_handle, to_device, to_numpy_struct
@@ -174,12 +178,14 @@ def replay_arrays(ops, op_off, wall0, cooldown, suppress=None, ev_cap_per_stream
     d_evoff = to_device(ev_off, dev)
     d_ev = torch.zeros(max(int(ev_off[-1]), 1) * TK_EVENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     d_fin = torch.zeros(n * TK_FINAL_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    rc = _lib.load().tw_tk_replay(
+    lib = _lib.load()
+    fn = lib.tw_tk_replay_wide if wide else lib.tw_tk_replay
+    rc = fn(
         d_ops.data_ptr(), d_off.data_ptr(), n, d_w.data_ptr(), d_c.data_ptr(),
         d_s.data_ptr() if d_s is not None else None, d_ack.data_ptr(), d_ev.data_ptr(), d_evoff.data_ptr(),
         d_fin.data_ptr(), stream_handle(),
     )
-    _lib.check(rc, "tw_tk_replay")
+    _lib.check(rc, "tw_tk_replay_wide" if wide else "tw_tk_replay")
     fin = to_numpy_struct(d_fin, TK_FINAL_DTYPE, n)
     ev = to_numpy_struct(d_ev, TK_EVENT_DTYPE, int(ev_off[-1]))
     events = [ev[ev_off[s] : ev_off[s] + min(int(fin[s]["n_events"]), ev_cap_per_stream)] for s in range(n)]
@@ -187,11 +193,13 @@ def replay_arrays(ops, op_off, wall0, cooldown, suppress=None, ev_cap_per_stream
 
 
 def replay_many(streams: Sequence[OpStream], ev_cap_per_stream: int = 4096, device=None) -> ReplayResult:
+    """Replay op streams; streams beyond 32 clients or groups take the wide kernel."""
     ops, op_off, wall0, cool, sup = pack_streams(streams)
     for s in streams:
-        if s._n_clients > TW_TK_MAX_CLIENTS:
-            raise ValueError(f"more than {TW_TK_MAX_CLIENTS} clients in one Timekeeper stream")
-    return replay_arrays(ops, op_off, wall0, cool, sup, ev_cap_per_stream, device)
+        if s._n_clients > TW_TK_MAX_CLIENTS_WIDE:
+            raise ValueError(f"more than {TW_TK_MAX_CLIENTS_WIDE} clients in one Timekeeper stream")
+    wide = any(s._n_clients > TW_TK_MAX_CLIENTS or len(s._groups) > TW_TK_MAX_GROUPS for s in streams)
+    return replay_arrays(ops, op_off, wall0, cool, sup, ev_cap_per_stream, device, wide=wide)
 
 
 def resolve_round(pending, eligible_mask, A: int, cooldown_ns: int, offset, seq, wall, last_bcast, stream=None):

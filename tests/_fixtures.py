@@ -48,7 +48,8 @@ def predictor_from_spec(s):
 
 @functools.lru_cache(maxsize=None)
 def barrier_golden(name: str = "barrier.npz"):
-    """barrier.npz: 1-5 actors (run_random_schedule); barrier_wide.npz: 6-32 clients."""
+    """barrier.npz: 1-5 actors (run_random_schedule); barrier_wide.npz: 6-32 clients;
+    barrier_xwide.npz: 33-257 clients, up to 48 groups (tw_tk_replay_wide)."""
     z = _npz(name)
     ops = z["ops"].view(TK_OP_DTYPE)
     return {k: z[k] for k in z.files if k != "ops"} | {"ops": ops}
@@ -119,7 +120,8 @@ def tk_case_inputs(case):
     arr = generate_arrivals(WorkloadSpec.from_doc(doc))
     eng = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
                        kv_capacity_blocks=32768, workers_per_replica=case["tp"], pp_stages=case["pp"])
-    pset = PredictorSet([TablePredictor.from_csv(calibration.csv_path(case["model"], case["tp"], case["pp"]),
+    ttp, tpp = case.get("table_tp", case["tp"]), case.get("table_pp", case["pp"])
+    pset = PredictorSet([TablePredictor.from_csv(calibration.csv_path(case["model"], ttp, tpp),
                                                  allow_extrapolation=True)])
     cfgs = config_array([SweepConfig(engine=eng, epoch_ns=case["epoch"], timekeeper=True,
                                      tk_cooldown_ns=case["cooldown"])])

@@ -233,6 +233,7 @@ class Recorder:
         self.ops = []
         self.acks = []
         self.groups = {}
+        self.ids = {}  # client id -> registration index, as the core issued them
         orig = h.core.handle
 
         def handle(msg, reply=None):
@@ -251,19 +252,17 @@ class Recorder:
         h.clock.advance = advance
 
     def _cid(self, client_id):
-        if not client_id:
-            return -1
-        digits = "".join(ch for ch in client_id if ch.isdigit())
-        name = "".join(ch for ch in client_id if not ch.isdigit())
-        if name not in ("actor", "observer") or not digits:
-            return -1
-        return int(digits) - 1
+        """Registration index of an id the core issued; -1 for anything else (the core
+        answers UnknownClient, e.g. 'actor46' when registration 46 was an observer)."""
+        return self.ids.get(client_id or "", -1)
 
     def _record(self, msg, ack):
         t = msg.type
         err = None if ack.error is None else ack.error.split(":")[0]
         if t is MessageType.REGISTER:
             op = (0, 0 if msg.role == "ACTOR" else 1, 0, 0)
+            if err is None:
+                self.ids[ack.client_id] = len(self.ids)
         elif t is MessageType.SEAL:
             op = (0, 2, 0, 0)
         elif t is MessageType.JUMP_REQUEST:
@@ -411,7 +410,7 @@ WIDE_ACTORS = (6, 7, 8, 9, 9, 9, 12, 16, 17, 17, 17, 24, 31, 32, 32)
 WIDE_COOLDOWNS = (0, 1, 500_000, 500_000, 2_000_000, 123_000_000)
 
 
-def wide_schedule(seed, transcript=None):
+def wide_schedule(seed, transcript=None, actor_counts=None, n_groups=4, obs_max=None):
     """One CoreHarness-driven schedule with 6-32 clients (A up to 17 and beyond).
 
     Unlike run_random_schedule (pkg/tests/_support.py:99, 1-5 actors), collectives here
@@ -422,8 +421,11 @@ def wide_schedule(seed, transcript=None):
     interleaved with real traffic. Every message goes through the reference BarrierCore.
     """
     rng = random.Random(seed)
-    n_act = rng.choice(WIDE_ACTORS)
-    n_obs = 0 if n_act >= 32 else rng.randint(0, min(2, 32 - n_act))
+    n_act = rng.choice(actor_counts or WIDE_ACTORS)
+    if obs_max is None:
+        n_obs = 0 if n_act >= 32 else rng.randint(0, min(2, 32 - n_act))
+    else:
+        n_obs = rng.randint(0, obs_max)
     cooldown = rng.choice(WIDE_COOLDOWNS)
     suppress = rng.random() < 0.15
     h = _support.CoreHarness.build(cooldown_ns=cooldown, suppress=suppress)
@@ -472,7 +474,7 @@ def wide_schedule(seed, transcript=None):
         elif roll < 0.58:
             h.clock.advance(rng.choice((0, 1, rng.randint(1, 2_000_000))))
         elif roll < 0.70:
-            g = f"g{rng.randint(0, 3)}"
+            g = f"g{rng.randint(0, n_groups - 1)}"
             if groups.get(g) is None:
                 groups[g] = rng.choice((len(alive), rng.randint(1, len(alive))))
             size = groups[g] if rng.random() > 0.04 else groups[g] + 1  # occasional ExpectedMismatch
@@ -621,6 +623,21 @@ def make_wide_golden():
         arrs |= {f"pending{A}": pend, f"elig{A}": elig, f"in{A}": st_in, f"out{A}": st_out, f"flag{A}": flag}
         print(f"resolve A={A}:", {k: int((flag == k).sum()) for k in (-1, 0, 1)})
     np.savez_compressed(os.path.join(HERE, "resolve_wide.npz"), **arrs)
+
+
+XWIDE_ACTORS = (33, 40, 48, 64, 65, 100, 130, 257)
+
+
+def make_xwide_golden():
+    """barrier_xwide.npz: CoreHarness-driven schedules beyond 32 clients (33-257 actors plus
+    up to 3 observers) and, in half of them, up to 48 collective groups: what
+    tw_tk_replay_wide must reproduce (BarrierCore has no client limit)."""
+    streams = []
+    for seed in range(48):
+        streams.append(wide_schedule(91_000 + seed, None, XWIDE_ACTORS, 48 if seed % 2 else 4, 3))
+    n_ops, n_ev = save_streams(streams, "barrier_xwide.npz")
+    acts = sorted({sum(1 for o in r.ops if o[1] == 0) for _, r, _, _ in streams})
+    print("barrier_xwide:", len(streams), "streams,", n_ops, "ops,", n_ev, "events; actor counts", acts)
 
 
 # ------------------------------------------------------------------------------
@@ -912,19 +929,29 @@ def make_tkgrid_golden():
         ("tk_config1_tp1", w1, 1, 1, 0, "8b", 500_000),
         ("tk_config2_tp4", w1, 4, 1, 0, "8b", 500_000),
         ("tk_config_tp4pp2", w1, 4, 2, 0, "8b", 500_000),
+        # wide actor grids (round 2): more than 32 actors, and more stages than the presets'
+        # tables (table_tp / table_pp name the calibration table a grid uses)
+        ("tk_small_tp8pp8_wide", w_small, 8, 8, 0, "8b", 500_000, 8, 2),
+        ("tk_small_tp4pp16_wide", w_small, 4, 16, 777, "70b", 200_000, 4, 2),
+        ("tk_small_tp16pp4_wide", w_small, 16, 4, 0, "8b", 0, 8, 1),
+        ("tk_config_tp8pp5_wide", w1, 8, 5, 0, "8b", 500_000, 8, 2),
     ]
-    for name, arr, tp, pp, epoch, model, cool in grid:
+    for name, arr, tp, pp, epoch, model, cool, *table in grid:
         cfg = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
                            kv_capacity_blocks=32768, workers_per_replica=tp, pp_stages=pp)
-        pred = ref_pred.TablePredictor.from_csv(calibration.csv_path(model, tp, pp), allow_extrapolation=True)
+        ttp, tpp = table if table else (tp, pp)
+        pred = ref_pred.TablePredictor.from_csv(calibration.csv_path(model, ttp, tpp), allow_extrapolation=True)
         events, off, seq, wall, bd = ref_simulate_with_tk(arr, cfg, pred, epoch, cool)
         plain = ref_oracle.simulate(arr, cfg, pred, epoch_ns=epoch)
         assert events == plain, name  # the restated loop is the reference loop
         order = sorted(range(len(arr)), key=lambda i: arr[i].offset_ns)
         idx = {arr[i].request_id: k for k, i in enumerate(order)}
-        recs.append({"name": name, "n": len(arr), "seed": 5 if arr is w_small else 1, "tp": tp, "pp": pp,
-                     "epoch": epoch, "model": model, "cooldown": cool, "offset": off, "seq": seq, "wall": wall,
-                     "bdigest": str(bd), "digest": str(digest_of_docs(events, idx)), "n_events": len(events)})
+        rec = {"name": name, "n": len(arr), "seed": 5 if arr is w_small else 1, "tp": tp, "pp": pp,
+               "epoch": epoch, "model": model, "cooldown": cool, "offset": off, "seq": seq, "wall": wall,
+               "bdigest": str(bd), "digest": str(digest_of_docs(events, idx)), "n_events": len(events)}
+        if table:
+            rec["table_tp"], rec["table_pp"] = ttp, tpp
+        recs.append(rec)
         print(f"  tk case {name}: seq {seq} offset {off} wall {wall}")
     with open(os.path.join(HERE, "tkgrid.json"), "w") as fh:
         json.dump(recs, fh, indent=1)
@@ -1114,7 +1141,7 @@ def make_metrics_golden():
 
 if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"predictor", "predictor_neg", "barrier", "oracle", "tkgrid", "arrivals", "metrics",
-                                  "core", "wide"}
+                                  "core", "wide", "xwide"}
     rng = np.random.default_rng(20260100397)
     if "predictor" in which:
         make_predictor_golden(rng)
@@ -1134,3 +1161,5 @@ if __name__ == "__main__":
         make_core_golden()
     if "wide" in which:
         make_wide_golden()
+    if "xwide" in which:
+        make_xwide_golden()

@@ -392,12 +392,16 @@ def test_reference_known_answers_through_drop_in_predict():
 # ---------------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("name", ["barrier.npz", "barrier_wide.npz"])
-def test_tk_replay_matches_reference_barriercore(name):
+@pytest.mark.parametrize("name,wide", [("barrier.npz", False), ("barrier_wide.npz", False), ("barrier.npz", True),
+                                       ("barrier_wide.npz", True), ("barrier_xwide.npz", True)])
+def test_tk_replay_matches_reference_barriercore(name, wide):
+    """k_tk_replay (<= 32 clients) and k_tk_replay_wide (up to 1,024 clients, 64 groups)
+    against the reference BarrierCore's acks, broadcasts, releases and final state;
+    barrier_xwide.npz has 33-257 clients and up to 48 groups."""
     from paper_2601_00397_b200.timekeeper import replay_arrays
 
     g = barrier_golden(name)
-    r = replay_arrays(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"])
+    r = replay_arrays(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"], wide=wide)
     assert np.array_equal(r.acks, g["acks"])
     for s in range(len(g["op_off"]) - 1):
         want = g["events"][g["ev_off"][s] : g["ev_off"][s + 1]]

@@ -57,7 +57,7 @@ def test_oracle_predictor_empty_batch_code():
     assert out.tolist() == [-1, -1]
 
 
-@pytest.mark.parametrize("name", ["barrier.npz", "barrier_wide.npz"])
+@pytest.mark.parametrize("name", ["barrier.npz", "barrier_wide.npz", "barrier_xwide.npz"])
 def test_oracle_barrier_replay_matches_reference(name):
     g = barrier_golden(name)
     ack, events, fin = orc.tk_replay(g["ops"], g["op_off"], g["wall0"], g["cooldown"], g["suppress"])
