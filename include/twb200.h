@@ -241,6 +241,12 @@ int tw_tk_replay_wide(const tw_tk_op* ops, const int64_t* op_off, int32_t n_stre
                       const uint8_t* suppress, int32_t* ack, tw_tk_event* ev,
                       const int64_t* ev_off, tw_tk_final* fin, void* stream);
 
+/* tw_tk_resolve for any A >= 1: eligible_words holds ceil(A/32) uint32 words per
+ * Timekeeper (bit a of word a/32 = actor a eligible); one warp per Timekeeper. */
+int tw_tk_resolve_wide(int64_t* pending, const uint32_t* eligible_words, int32_t n_cfg, int32_t A,
+                       int64_t cooldown_ns, int64_t* offset_ns, int64_t* seq, int64_t* wall_ns,
+                       int64_t* last_bcast_ns, int8_t* broadcast, void* stream);
+
 /* Bulk min-advance (the _try_resolve/_resolve arithmetic, timekeeper.py:318-366)
  * for C independent Timekeepers with A actor slots each, one round:
  * pending[c*A + a] = requested target or INT64_MAX (no request / not eligible);

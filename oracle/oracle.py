@@ -60,6 +60,8 @@ def load():
         lib.orc_tk_replay.restype = None
         lib.orc_tk_resolve.argtypes = [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P]
         lib.orc_tk_resolve.restype = None
+        lib.orc_tk_resolve_wide.argtypes = [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P]
+        lib.orc_tk_resolve_wide.restype = None
         lib.orc_simulate.argtypes = [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64]
         lib.orc_simulate.restype = None
         lib.orc_sim_many.argtypes = [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32]
@@ -99,6 +101,15 @@ def tk_replay(ops: np.ndarray, op_off: np.ndarray, wall0, cooldown, suppress=Non
     )
     events = [ev[ev_off[s] : ev_off[s] + min(int(fin[s]["n_events"]), ev_cap_per_stream)] for s in range(n)]
     return ack[: len(ops)], events, fin
+
+
+def tk_resolve_wide(pending, elig_words, A, cooldown, offset, seq, wall, last_bcast):
+    """elig_words: [C, ceil(A/32)] uint32 eligibility masks."""
+    n = len(elig_words)
+    bc = np.zeros(n, np.int8)
+    load().orc_tk_resolve_wide(_p(pending), _p(np.ascontiguousarray(elig_words, np.uint32)), n, A, cooldown,
+                               _p(offset), _p(seq), _p(wall), _p(last_bcast), _p(bc))
+    return bc
 
 
 def tk_resolve(pending, elig, A, cooldown, offset, seq, wall, last_bcast):

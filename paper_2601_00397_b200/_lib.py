@@ -180,6 +180,7 @@ EXPORTED_SYMBOLS = (
     "tw_tk_replay",
     "tw_tk_replay_wide",
     "tw_tk_resolve",
+    "tw_tk_resolve_wide",
     "tw_sim_many",
     "tw_sim_scratch_bytes",
     "tw_sim_set_checks",
@@ -226,6 +227,7 @@ _SIGNATURES = {
     "tw_tk_replay": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tw_tk_replay_wide": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tw_tk_resolve": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),
+    "tw_tk_resolve_wide": (_I32, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),
     "tw_sim_many": (
         _I32,
         [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P],

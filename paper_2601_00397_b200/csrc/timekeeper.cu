@@ -499,6 +499,64 @@ __global__ void __launch_bounds__(32 * kTkWarps2) k_tk_resolve_rows(
   }
 }
 
+// One round for Timekeepers of A > 32 actor slots (eligibility: ceil(A/32) words each):
+// one warp per Timekeeper, lanes striding over its A pending targets (coalesced), the
+// eligible and pending counts one REDUX each and t_min one warp min: the per-config
+// segmented reduction; lane 0 applies _resolve and the warp clears the row
+// (timekeeper.py:318-366).
+constexpr int kTkWideRes = 8;  // warps (Timekeepers) per CTA
+__global__ void __launch_bounds__(32 * kTkWideRes) k_tk_resolve_wide(
+    int64_t* __restrict__ pending, const uint32_t* __restrict__ elig, int32_t n_cfg, int32_t A,
+    int64_t cooldown, int64_t conv_cooldown, int64_t* __restrict__ offset, int64_t* __restrict__ seq,
+    int64_t* __restrict__ wall, int64_t* __restrict__ last_bcast, int8_t* __restrict__ bcast) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * kTkWideRes + (threadIdx.x >> 5);
+  if (c >= n_cfg) return;  // warp-uniform
+  const int W = (A + 31) >> 5;
+  int64_t* row = pending + c * A;
+  const uint32_t* m = elig + c * W;
+  int nel = 0, nhas = 0;
+  int64_t t = INT64_MAX;
+  for (int a = lane; a < A; a += 32) {
+    if ((__ldg(m + (a >> 5)) >> (a & 31)) & 1u) {
+      const int64_t v = row[a];
+      nel++;
+      if (v != INT64_MAX) {
+        nhas++;
+        t = v < t ? v : t;
+      }
+    }
+  }
+  nel = (int)__reduce_add_sync(kFull, (unsigned)nel);
+  nhas = (int)__reduce_add_sync(kFull, (unsigned)nhas);
+  const bool resolves = nel > 0 && nhas == nel;  // sealed assumed; |pending| == eligible
+  t = warp_min_i64(t);
+  if (lane == 0) {
+    if (!resolves) {
+      bcast[c] = -1;
+    } else {
+      int64_t w = wall[c];
+      const int64_t lb = last_bcast[c];
+      if (w < t && lb != INT64_MIN && cooldown > 0) {
+        const int64_t wait = lb + cooldown - w;
+        if (wait > 0) w += (wait == cooldown) ? conv_cooldown : fake_sleep_ns(wait);
+      }
+      wall[c] = w;
+      if (w < t) {
+        const int64_t cand = t - w;
+        if (cand > offset[c]) offset[c] = cand;
+        seq[c] += 1;
+        last_bcast[c] = w;
+        bcast[c] = 1;
+      } else {
+        bcast[c] = 0;
+      }
+    }
+  }
+  if (resolves)  // pending.clear()
+    for (int a = lane; a < A; a += 32) row[a] = INT64_MAX;
+}
+
 }  // namespace twb
 
 using namespace twb;
@@ -540,6 +598,23 @@ extern "C" int tw_tk_replay_wide(const tw_tk_op* ops, const int64_t* op_off, int
                                                                  suppress, ack, ev, ev_off, fin);
   count_launch();
   return check_launch("tw_tk_replay_wide");
+}
+
+extern "C" int tw_tk_resolve_wide(int64_t* pending, const uint32_t* eligible_words, int32_t n_cfg, int32_t A,
+                                  int64_t cooldown_ns, int64_t* offset_ns, int64_t* seq, int64_t* wall_ns,
+                                  int64_t* last_bcast_ns, int8_t* broadcast, void* stream) {
+  if (A < 1 || n_cfg < 0 || cooldown_ns < 0) {
+    set_error("tw_tk_resolve_wide: need A >= 1, n_cfg >= 0, cooldown >= 0");
+    return TW_EINVAL;
+  }
+  if (n_cfg == 0) return TW_OK;
+  const double secs = (double)cooldown_ns / 1e9;  // as tw_tk_resolve
+  const int64_t conv = cooldown_ns > 0 ? (int64_t)nearbyint(secs * 1e9) : 0;
+  const int blocks = (int)(((int64_t)n_cfg + kTkWideRes - 1) / kTkWideRes);
+  k_tk_resolve_wide<<<blocks, 32 * kTkWideRes, 0, (cudaStream_t)stream>>>(
+      pending, eligible_words, n_cfg, A, cooldown_ns, conv, offset_ns, seq, wall_ns, last_bcast_ns, broadcast);
+  count_launch();
+  return check_launch("tw_tk_resolve_wide");
 }
 
 extern "C" int tw_tk_resolve(int64_t* pending, const uint32_t* eligible_mask, int32_t n_cfg, int32_t A,

@@ -202,6 +202,24 @@ def replay_many(streams: Sequence[OpStream], ev_cap_per_stream: int = 4096, devi
     return replay_arrays(ops, op_off, wall0, cool, sup, ev_cap_per_stream, device, wide=wide)
 
 
+def resolve_round_wide(pending, eligible_words, A: int, cooldown_ns: int, offset, seq, wall, last_bcast,
+                       stream=None):
+    """resolve_round for any A: eligible_words is a [C, ceil(A/32)] int32 tensor of masks
+    (tw_tk_resolve_wide, one warp per Timekeeper)."""
+    import torch
+
+    from ._device import stream_handle
+
+    C = eligible_words.shape[0]
+    out = torch.empty(C, dtype=torch.int8, device=pending.device)
+    rc = _lib.load().tw_tk_resolve_wide(
+        pending.data_ptr(), eligible_words.data_ptr(), C, A, cooldown_ns, offset.data_ptr(), seq.data_ptr(),
+        wall.data_ptr(), last_bcast.data_ptr(), out.data_ptr(), stream_handle(stream),
+    )
+    _lib.check(rc, "tw_tk_resolve_wide")
+    return out
+
+
 def resolve_round(pending, eligible_mask, A: int, cooldown_ns: int, offset, seq, wall, last_bcast, stream=None):
     """One bulk min-advance round over CUDA int64 tensors (updated in place).
 

@@ -62,6 +62,12 @@ def resolve_golden():
     return {A: {k: z[f"{k}{A}"] for k in ("pending", "elig", "in", "out", "flag")} for A in (9, 17, 32)}
 
 
+def resolve_xwide_golden():
+    """The same at A = 33, 65, 257 with [C, ceil(A/32)] eligibility words (tw_tk_resolve_wide)."""
+    z = _npz("resolve_xwide.npz")
+    return {A: {k: z[f"{k}{A}"] for k in ("pending", "elig", "in", "out", "flag")} for A in (33, 65, 257)}
+
+
 @functools.lru_cache(maxsize=None)
 def oracle_golden():
     z = _npz("oracle.npz")

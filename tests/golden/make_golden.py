@@ -524,7 +524,7 @@ def wide_schedule(seed, transcript=None, actor_counts=None, n_groups=4, obs_max=
     return h, rec, cooldown, suppress
 
 
-def resolve_rounds(A, C, rng):
+def resolve_rounds(A, C, rng, words=False):
     """Single resolve rounds for C Timekeepers of A actor slots, each computed by the
     reference BarrierCore._try_resolve/_resolve (timekeeper.py:318-366) on a FakeClock.
 
@@ -533,7 +533,8 @@ def resolve_rounds(A, C, rng):
     outputs (broadcast flag 1 / silent 0 / unresolved -1, and the post-round state)."""
     I64MAX, I64MIN = np.iinfo(np.int64).max, np.iinfo(np.int64).min
     pend = np.full(C * A, I64MAX, np.int64)
-    elig = np.zeros(C, np.uint32)
+    W = (A + 31) // 32
+    elig = np.zeros((C, W), np.uint32) if words else np.zeros(C, np.uint32)
     st_in = np.zeros((C, 4), np.int64)
     st_out = np.zeros((C, 4), np.int64)
     flag = np.zeros(C, np.int8)
@@ -564,7 +565,10 @@ def resolve_rounds(A, C, rng):
         for a, cid in enumerate(ids):
             if cid in core.pending:
                 pend[c * A + a] = core.pending[cid]
-        elig[c] = mask
+        if words:
+            elig[c] = [(mask >> (32 * k)) & 0xFFFFFFFF for k in range(W)]
+        else:
+            elig[c] = mask
         last = core.last_broadcast_wall_ns
         st_in[c] = (core.offset_ns, core.seq, wall, I64MIN if last is None else last)
         seq0 = core.seq
@@ -626,6 +630,18 @@ def make_wide_golden():
 
 
 XWIDE_ACTORS = (33, 40, 48, 64, 65, 100, 130, 257)
+
+
+def make_resolve_xwide_golden():
+    """resolve_xwide.npz: single rounds of the reference BarrierCore._resolve for A = 33,
+    65 (TP8 x PP8 + dispatcher) and 257 actor slots (tw_tk_resolve_wide)."""
+    rng = random.Random(20261017)
+    arrs = {}
+    for A in (33, 65, 257):
+        pend, elig, st_in, st_out, flag = resolve_rounds(A, 600, rng, words=True)
+        arrs |= {f"pending{A}": pend, f"elig{A}": elig, f"in{A}": st_in, f"out{A}": st_out, f"flag{A}": flag}
+        print(f"resolve_xwide A={A}:", {k: int((flag == k).sum()) for k in (-1, 0, 1)})
+    np.savez_compressed(os.path.join(HERE, "resolve_xwide.npz"), **arrs)
 
 
 def make_xwide_golden():
@@ -1163,3 +1179,4 @@ if __name__ == "__main__":
         make_wide_golden()
     if "xwide" in which:
         make_xwide_golden()
+        make_resolve_xwide_golden()

@@ -14,6 +14,7 @@ import pytest
 from _fixtures import (
     barrier_golden,
     resolve_golden,
+    resolve_xwide_golden,
     case_events,
     case_inputs,
     oracle_golden,
@@ -446,6 +447,24 @@ def test_tk_resolve_matches_reference_resolve(A):
     pend = dv[0].cpu().numpy()
     assert (pend[np.repeat(g["flag"] >= 0, A)] == np.iinfo(np.int64).max).all()
     assert np.array_equal(pend[np.repeat(g["flag"] < 0, A)], g["pending"][np.repeat(g["flag"] < 0, A)])
+
+
+@pytest.mark.parametrize("A", [33, 65, 257])
+def test_tk_resolve_wide_matches_reference_resolve(A):
+    """k_tk_resolve_wide (one warp per Timekeeper) against rounds of the reference
+    BarrierCore._resolve with 33-257 actor slots (TP8 x PP8 + dispatcher is 65)."""
+    import torch
+
+    from paper_2601_00397_b200.timekeeper import resolve_round_wide
+
+    g = resolve_xwide_golden()[A]
+    dv = [torch.from_numpy(g["pending"].copy()).cuda()] + [torch.from_numpy(g["in"][:, k].copy()).cuda()
+                                                           for k in range(4)]
+    flag = resolve_round_wide(dv[0], torch.from_numpy(g["elig"].view(np.int32)).cuda(), A, 500_000, *dv[1:])
+    assert np.array_equal(flag.cpu().numpy(), g["flag"])
+    assert np.array_equal(np.stack([d.cpu().numpy() for d in dv[1:]], axis=1), g["out"])
+    pend = dv[0].cpu().numpy()
+    assert (pend[np.repeat(g["flag"] >= 0, A)] == np.iinfo(np.int64).max).all()
 
 
 @pytest.mark.parametrize("A", [1, 2, 5, 9, 17, 32])

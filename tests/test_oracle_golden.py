@@ -23,6 +23,7 @@ from _fixtures import (
     case_inputs,
     oracle_golden,
     predictor_golden,
+    resolve_xwide_golden,
     tk_case_inputs,
     tkgrid_golden,
 )
@@ -228,3 +229,12 @@ def test_oracle_linear_quantisation_extremes():
                            np.arange(n, dtype=np.int32))
     assert got.tolist() == [w for _, w in cases]
 
+
+
+@pytest.mark.parametrize("A", [33, 65, 257])
+def test_oracle_wide_resolve_rounds_match_reference_resolve(A):
+    g = resolve_xwide_golden()[A]
+    st = [g["pending"].copy()] + [g["in"][:, k].copy() for k in range(4)]
+    flag = orc.tk_resolve_wide(st[0], g["elig"], A, 500_000, *st[1:])
+    assert np.array_equal(flag, g["flag"])
+    assert np.array_equal(np.stack(st[1:], axis=1), g["out"])
