@@ -348,6 +348,22 @@ int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cfg* cfgs,
                 int64_t scratch_bytes, void* stream);
 /* scratch bytes tw_sim_many wants for these sizes (64 up to slot capacity 4096) */
 int64_t tw_sim_scratch_bytes(int32_t n_cfg, int32_t slot_capacity);
+/* Scratch bytes for the latency regime's busy-period segments (0: n_cfg is not in that
+ * regime). With scratch_bytes >= this (total_requests = req_base[n_cfg]), req_base given,
+ * no event dump and slot capacity <= 4096, tw_sim_many splits each config's arrivals at
+ * likely regeneration points (an arrival that finds the engine empty restarts the
+ * timeline, oracle.py:78-83), simulates the segments speculatively in parallel and joins
+ * the valid pieces (serially re-running any piece whose boundary was not one), so one
+ * config's serial chain no longer bounds the sweep. Records and stamps are identical to
+ * the serial loop's, except that when a config stops early (stall or prediction error)
+ * stamps a speculative segment wrote past the stop are reset to -1. */
+int64_t tw_sim_seg_scratch_bytes(int32_t n_cfg, int64_t total_requests);
+/* Opt-in statistics of the segmented path for the next tw_sim_many calls on this thread
+ * (device pointer, 8 int32 per config; NULL disables): {segments, pieces joined from a
+ * segment's run, pieces re-run serially by the join pass, Timekeeper carry-overs refused,
+ * segments out of log / overrun room, stops that were not regeneration points of the next
+ * run, 0, 0}. */
+int tw_sim_set_seg_stats(int32_t* per_config_8xi32);
 
 /* Launch geometry the library picked for the last tw_sim_many on this thread
  * (for the bench's roofline bookkeeping). */

@@ -183,6 +183,8 @@ EXPORTED_SYMBOLS = (
     "tw_tk_resolve_wide",
     "tw_sim_many",
     "tw_sim_scratch_bytes",
+    "tw_sim_seg_scratch_bytes",
+    "tw_sim_set_seg_stats",
     "tw_sim_set_checks",
     "tw_sim_last_launch",
     "tw_sim_set_profile",
@@ -233,6 +235,8 @@ _SIGNATURES = {
         [_P, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P],
     ),
     "tw_sim_scratch_bytes": (_I64, [_I32, _I32]),
+    "tw_sim_seg_scratch_bytes": (_I64, [_I32, _I64]),
+    "tw_sim_set_seg_stats": (_I32, [_P]),
     "tw_sim_set_checks": (_I32, [_P]),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
     "tw_sim_set_profile": (_I32, [_P]),

@@ -27,6 +27,9 @@
 //    position/time/step per request, so a run's body sums in closed form) and
 //    FIRST_TOKEN / FINISHED stamps are stored per request; full event dumps only
 //    for audited configs.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace twb {
@@ -214,18 +217,47 @@ struct TkGrid {
   int64_t disp_ts;
   int32_t disp;
   ArrWindow win;
+  // speculative segments (kSpec): the run started from a guessed wall clock; a true run
+  // whose wall is this one's + delta takes the same decisions iff d_lo <= delta < d_hi
+  int64_t d_lo, d_hi;
 #ifdef TWB_PROFILE_PHASES
   int64_t prof_calls, prof_fast, prof_loops;
 #endif
 };
 
+// The Timekeeper's decisions depend on its FakeClock wall only through `wall < t_min` and
+// `offset >= cJ` (sleeps use last_bcast - wall, broadcasts set offset = t_min - wall, so
+// V = wall + offset and everything else move with V alone). A speculative segment records,
+// for each such comparison, the range of wall shifts delta that keep its outcome.
+template <bool kSpec>
+__device__ __forceinline__ bool tk_wall_lt(TkGrid& g, int64_t t) {
+  const bool r = g.wall < t;
+  if constexpr (kSpec) {  // wall + delta < t  <=>  delta < t - wall
+    const int64_t m = t - g.wall;
+    if (r) g.d_hi = min(g.d_hi, m);
+    else g.d_lo = max(g.d_lo, m);
+  }
+  return r;
+}
+template <bool kSpec>
+__device__ __forceinline__ bool tk_off_ge(TkGrid& g, int64_t cj) {
+  const bool r = g.offset >= cj;
+  if constexpr (kSpec) {  // offset - delta >= cj  <=>  delta < offset - cj + 1
+    const int64_t m = g.offset - cj + 1;
+    if (r) g.d_hi = min(g.d_hi, m);
+    else g.d_lo = max(g.d_lo, m);
+  }
+  return r;
+}
+
+template <bool kSpec = false>
 __device__ __forceinline__ void tk_resolve(TkGrid& g, int64_t t_min) {
   // timekeeper.py:326-366 with FakeClock sleep (pkg/tests/_support.py:33-34)
-  if (g.wall < t_min && g.last_bcast != INT64_MIN && g.cooldown > 0) {
+  if (tk_wall_lt<kSpec>(g, t_min) && g.last_bcast != INT64_MIN && g.cooldown > 0) {
     const int64_t wait = g.last_bcast + g.cooldown - g.wall;
     if (wait > 0) g.wall += (wait == g.cooldown) ? g.conv_cooldown : cold_fake_sleep(wait);
   }
-  if (g.wall < t_min) {
+  if (tk_wall_lt<kSpec>(g, t_min)) {
     const int64_t cand = t_min - g.wall;
     if (cand > g.offset) g.offset = cand;
     g.seq++;
@@ -247,6 +279,7 @@ __device__ __forceinline__ void tk_dispatch(TkGrid& g, const int64_t* __restrict
 // only resolves targets beyond V; a V that jumped several steps ahead (the FakeClock
 // wall outrunning short steps) is skipped in O(1). Each resolve is one BarrierCore
 // round with t_min = min(dispatcher's next arrival, the stage deadline).
+template <bool kSpec = false>
 TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                        int S, int64_t now0, int64_t d, int64_t K) {
   // deadline m (m >= 1) of this run: now0 + (m / S) * d + per * (m % S); m = 0 is now0
@@ -274,7 +307,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
   }
   // Wall-bound state (every stage gap <= cJ <= offset): the loop's first closed form,
   // then the dispatcher catches up (the walk's second pass).
-  if (S <= 2 && g.last_bcast == g.wall && g.conv_cooldown > 0 && d > 0 && g.offset >= g.conv_cooldown &&
+  if (S <= 2 && g.last_bcast == g.wall && g.conv_cooldown > 0 && d > 0 && tk_off_ge<kSpec>(g, g.conv_cooldown) &&
       (S == 1 ? d : d - (d >> 1)) <= g.conv_cooldown && g.V < now0 + K * d) {
     const int64_t cj1 = g.conv_cooldown;
     const int64_t R = div_rcp(now0 + K * d - g.V + cj1 - 1, cj1, g.rcp_cooldown);
@@ -316,7 +349,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
       // up to end_all are R = ceil((end_all - V) / cJ): wall += R*cJ, seq += R.
       // Dispatcher targets inside that window change no clock value, only which
       // arrivals have been passed (tk_dispatch).
-      if (wallbound_ok && g.offset >= cj) {
+      if (wallbound_ok && tk_off_ge<kSpec>(g, cj)) {
         const int64_t R = div_rcp(end_all - g.V + cj - 1, cj, g.rcp_cooldown);
         g.wall += R * cj;
         g.seq += R;
@@ -378,7 +411,7 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
       }
     }
     const int64_t t_min = g.disp_ts < tgt ? g.disp_ts : tgt;
-    tk_resolve(g, t_min);
+    tk_resolve<kSpec>(g, t_min);
     m_on = g.V == tgt ? m_walk : -1;
   }
 }
@@ -388,13 +421,14 @@ TWB_TK_FN void tk_run(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int6
 #else
 #define TWB_IDLE_FN TWB_TK_FN
 #endif
+template <bool kSpec = false>
 TWB_IDLE_FN void tk_idle(TkGrid& g, const int64_t* __restrict__ ts, int32_t n, int64_t epoch,
                                         int64_t end) {
   // idle jump: only the dispatcher drives time (its target is <= end while V < end)
   for (;;) {
     tk_dispatch(g, ts, n, epoch);
     if (g.V >= end) return;
-    tk_resolve(g, g.disp_ts);
+    tk_resolve<kSpec>(g, g.disp_ts);
   }
 }
 
@@ -506,7 +540,8 @@ void cold_dump_event(tw_event* evp, int64_t pos, int32_t rq, int kind, int64_t t
 }
 
 struct Emitter {
-  uint64_t dig;  // lane-partial digest
+  uint64_t dig;   // lane-partial digest
+  uint64_t msum;  // lane-partial sum of the multipliers (segments only; dead code otherwise)
   int64_t* first;
   int64_t* finish;
   tw_event* evp;
@@ -517,7 +552,9 @@ struct Emitter {
   }
   // u = tw_event_u(ts, step), the step-uniform part of the hash, computed once per step
   __device__ __forceinline__ void event_u(int64_t pos, int32_t rq, int kind, uint64_t u, int64_t ts, int64_t step) {
-    dig += tw_event_mult((uint64_t)rq, (uint64_t)kind) * ((uint64_t)pos * TW_DIG_A + u);
+    const uint64_t m = tw_event_mult((uint64_t)rq, (uint64_t)kind);
+    dig += m * ((uint64_t)pos * TW_DIG_A + u);
+    msum += m;
     if (evp && pos < ev_cap) cold_dump_event(evp, pos, rq, kind, ts, step);
   }
 };
@@ -561,9 +598,98 @@ TWB_WIDE_FN int64_t wide_held(Slots sl, int n_act, Blocks blk) {
   return warp_sum_i64_redux(held_l);
 }
 
-// kTput: the throughput variant (predictor blob read from global memory, see k_sim)
-template <bool kTput>
-__device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) {
+// ---- busy-period segments (sim_seg.cu, DESIGN.md §4.1 "Busy-period segments") ----------
+// A config's timeline restarts from the same state whenever an arrival finds the engine
+// empty (nothing running or waiting: oracle.py:78-83 jumps `now` to the arrival): from
+// there on the event stream depends only on the arrivals, not on the history. Such an
+// arrival is a regeneration point. The latency regime splits each config's arrivals into
+// segments at likely regeneration points and simulates them speculatively in parallel
+// (mode 1); a join pass (mode 2 for the rare mismatches) chains the valid pieces.
+constexpr int32_t kSegOverflow = -1;  // a segment ran out of log or overrun-stamp room
+constexpr int kSegLogPerReq = 8;      // Timekeeper log records per request of a segment
+// Room per segment: kSegLogPerReq log records and 4 overrun stamps per own request, plus
+// the same for SegParams::xtra more requests (an overrun past the segment's end needs room
+// for the next busy period; xtra is set from the segment count so the total stays bounded)
+struct TkLog {  // one Timekeeper call of the loop: K >= 1 tk_run(now0, d, K); K = 0 tk_idle(now0)
+  int64_t now0, d, K;
+};
+struct TkState {                      // a Timekeeper state as the join pass needs it
+  int64_t wall, seq, last_bcast, offset;
+  int32_t disp, pad;
+};
+struct SegRegen {  // a segment's counters and speculative Timekeeper at the idle point before arrival j
+  int64_t events;
+  uint64_t dig;
+  uint64_t msum;
+  int32_t steps;
+  int32_t pad;
+  TkState tk;
+};
+struct SegSummary {  // one per (config, segment)
+  int32_t j_stop;    // next arrival at the stop (n: the config's end)
+  int32_t status;    // TW_SIM_* or kSegOverflow
+  int32_t last_regen;  // last regeneration point recorded (a0 if none)
+  int32_t adm_end;     // requests [.., adm_end) admitted at the stop
+  int64_t final_now;
+  int64_t events;
+  uint64_t dig;
+  uint64_t msum;  // sum of the event multipliers (frame shifts)
+  int32_t steps;
+  int32_t pred_code;
+  int32_t log_len;       // Timekeeper log records of this segment
+  int32_t pad;
+  TkState tk;            // speculative Timekeeper at the stop
+  int64_t d_lo, d_hi;    // wall shifts that keep every Timekeeper decision of this run
+};
+struct SegCtx {
+  int32_t a0, a1;         // arrival range: own [a0, a1); mode 2: start a0, a1 = n
+  TkLog* log;             // mode 1: this segment's Timekeeper calls, replayed after its run
+  int32_t log_cap;
+  int32_t log_len;        // mode 1: out
+  int64_t* side;          // mode 1: (first, finish) of requests a1 + i admitted in the overrun
+  int32_t side_cap;
+  int32_t* regpos;        // per request of the config: log position at a regeneration point, else -1
+  SegRegen* reg;          // per request of the config: counters at that point
+  TkGrid* g;              // mode 2: the Timekeeper state (in/out)
+  SegSummary out;         // mode 2: result (mode 1 writes its own summary to `sum`)
+  SegSummary* sum;        // mode 1: where the summary goes
+};
+
+struct SegParams {
+  int32_t wmax;          // segment slots per config
+  int32_t min_req;       // requests per segment at least
+  int32_t* nseg;         // [n_cfg]; 0 = not segmented (the join pass runs the config serially)
+  int32_t* seg_a0;       // [n_cfg * wmax] first arrival of each segment
+  SegSummary* summ;      // [n_cfg * wmax]
+  int32_t* regpos;       // [r_max], -1 = not a regeneration point
+  SegRegen* reg;         // [r_max]
+  TkLog* log;            // [kSegLogPerReq * (r_max + xtra * n_cfg * wmax)]
+  int64_t* side;         // [2 * 4 * (r_max + xtra * n_cfg * wmax)]
+  int64_t r_max;
+  int64_t xtra;          // extra requests of room per segment
+  int32_t cap_div;       // test hook (TWB_SIM_SEG_CAPDIV): log / overrun room divided by this
+  int32_t* stats;        // optional, 8 int32 per config (tw_sim_set_seg_stats)
+  int32_t* counter;      // [0..1] segment work counter (64-bit), [2] join work counter
+};
+
+__device__ __forceinline__ TkState tk_state(const TkGrid& g) {
+  TkState t;
+  t.wall = g.wall;
+  t.seq = g.seq;
+  t.last_bcast = g.last_bcast;
+  t.offset = g.offset;
+  t.disp = g.disp;
+  t.pad = 0;
+  return t;
+}
+
+// kTput: the throughput variant (predictor blob read from global memory, see k_sim).
+// kMode: 0 the whole config (k_sim); 1 one speculative segment (k_sim_seg: local frame,
+// Timekeeper calls logged for the segment's replay, stops at the first idle point at or
+// past a1); 2 the join pass's serial piece (k_sim_join: the true Timekeeper inline, stops at
+// the first idle point that its owner segment also recorded as a regeneration point).
+template <bool kTput, int kMode = 0>
+__device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c, SegCtx* sx = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const long long t_start = clock64();  // per-config cycles (always on: 2 reads)
@@ -604,7 +730,21 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     r.status = TW_SIM_CAPACITY;
   }
   if (r.status != TW_SIM_OK) {
-    if (lane == 0) p.res[c] = r;
+    if constexpr (kMode == 0) {
+      if (lane == 0) p.res[c] = r;
+    } else {
+      SegSummary o = {};
+      o.j_stop = sx->a0;
+      o.status = r.status;
+      o.last_regen = sx->a0;
+      o.adm_end = sx->a0;
+      o.final_now = cfg.epoch_ns;
+      if constexpr (kMode == 1) {
+        if (lane == 0) *sx->sum = o;
+      } else {
+        sx->out = o;
+      }
+    }
     return;
   }
 
@@ -622,6 +762,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
 
   Emitter em;
   em.dig = 0;
+  em.msum = 0;
   em.first = p.first ? p.first + p.req_base[c] : nullptr;
   em.finish = p.finish ? p.finish + p.req_base[c] : nullptr;
   em.evp = nullptr;
@@ -650,7 +791,11 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   const uint2* qh = (hdr->fast_off > 0 && p.pset_bytes >= (uint32_t)hdr->total_bytes) ? pset_qhdr(ps) : nullptr;
   const bool macro_ok = !pc.uses_c && cfg.pred_id >= 0 && cfg.pred_id < pset_ndesc(ps);
 
-  TkGrid g;
+  TkGrid g_own;
+  TkGrid& g = (kMode == 2) ? *sx->g : g_own;  // mode 2 continues the join pass's Timekeeper
+  g.d_lo = INT64_MIN;
+  g.d_hi = INT64_MAX;
+  if constexpr (kMode != 2) {
   g.wall = epoch;
   g.offset = 0;
   g.seq = 0;
@@ -665,18 +810,40 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
 #endif
   g.win.load(ts, n, epoch, 0);
   g.disp_ts = n > 0 ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
+  }
 
+  // segments start at arrival a0 (the engine empty, `now` jumping to it); mode 0 at 0
+  const int32_t a0 = kMode != 0 ? sx->a0 : 0;
+  const int32_t a1 = kMode == 1 ? sx->a1 : n;
   ArrWindow arr;
-  arr.load(ts, n, epoch, 0);
+  arr.load(ts, n, epoch, a0);
   int64_t now = epoch, n_events = 0;
-  int32_t step = 0, fut = 0, w_head = 0, n_act = 0;  // waiting = [w_head, fut), future = [fut, n)
-  int64_t next_arr = n > 0 ? __shfl_sync(kFull, arr.v, 0) : INT64_MAX;
+  int32_t step = 0, fut = a0, w_head = a0, n_act = 0;  // waiting = [w_head, fut), future = [fut, n)
+  int64_t next_arr = a0 < n ? __shfl_sync(kFull, arr.v, 0) : INT64_MAX;
   // waiting-queue window: lane l holds prompt/output of request w_head + l, reloaded
   // (prefetched) right after every admission so the next admission finds it in registers
-  int32_t qbase = 0;
-  int32_t q_pr = (lane < n) ? __ldg(prm + lane) : 0;
-  int32_t q_op = (lane < n) ? __ldg(outp + lane) : 0;
+  int32_t qbase = a0;
+  int32_t q_pr = (a0 + lane < n) ? __ldg(prm + a0 + lane) : 0;
+  int32_t q_op = (a0 + lane < n) ? __ldg(outp + a0 + lane) : 0;
   int overflow = 0;
+  int32_t last_regen = a0, j_stop = n, log_len = 0;
+  if constexpr (kMode != 0) {
+    if (kMode == 1 && lane == 0) {  // the segment's start is its first regeneration point
+      sx->reg[a0] = SegRegen{0, 0, 0, 0, 0, TkState{}};
+      sx->regpos[a0] = 0;
+    }
+    if (a0 > 0 && a0 < n) {  // the idle jump to the first arrival (oracle.py:81-83)
+      now = next_arr;
+      if constexpr (kMode == 1) {
+        if (tk_on) {
+          if (lane == 0) sx->log[0] = TkLog{now, 0, 0};
+          log_len = 1;
+        }
+      } else if (tk_on) {
+        tk_idle(g, ts, n, epoch, now);
+      }
+    }
+  }
 
   while (fut < n || w_head < fut || n_act > 0) {
     // ---- arrivals with epoch + offset <= now join the waiting queue (oracle.py:73-75)
@@ -686,6 +853,12 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       next_arr = fut < n ? arr.get(ts, n, epoch, fut) : INT64_MAX;
     }
     const bool waiting = w_head < fut;
+    if constexpr (kMode == 1) {  // room for this iteration's log record and overrun stamps
+      if (log_len + 2 > sx->log_cap || fut - a1 > sx->side_cap) {
+        r.status = kSegOverflow;
+        break;
+      }
+    }
     const long long q1 = TWB_CLK();
     arr_cyc += q1 - q0;
 
@@ -794,6 +967,17 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
           const int slot = n_act + n_adm + lane;
           const int64_t take = min(want, budget - WE);
           sl.req[slot] = idx;
+          if constexpr (kMode == 1) {
+            if (idx >= a1) {  // overrun: its stamps go to the side buffer (unset = -1)
+              sx->side[2 * (int64_t)(idx - a1)] = -1;
+              sx->side[2 * (int64_t)(idx - a1) + 1] = -1;
+            }
+          } else if constexpr (kMode == 2) {
+            // a serial piece crosses other segments' ranges, whose speculative stamps of a
+            // request still running when the config stops must not survive
+            if (em.first) em.first[idx] = -1;
+            if (em.finish) em.finish[idx] = -1;
+          }
           sl.prompt[slot] = pr;
           const int32_t op = inwin ? q_op : __ldg(outp + idx);
           sl.output[slot] = op;
@@ -828,12 +1012,41 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
         r.status = n_act > 0 ? TW_SIM_STALLED_ACTIVE : TW_SIM_STALLED_KV;
         break;
       }
+      if constexpr (kMode == 1) {  // the engine is empty and arrival fut is next
+        if (fut >= a1) {             // past this segment's arrivals: stop here
+          j_stop = fut;
+          break;
+        }
+        uint64_t dg = em.dig, ms = em.msum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          dg += __shfl_xor_sync(kFull, dg, o);
+          ms += __shfl_xor_sync(kFull, ms, o);
+        }
+        if (lane == 0) {  // a regeneration point of this segment's run
+          sx->reg[fut] = SegRegen{n_events, dg, ms, step, 0, TkState{}};
+          sx->regpos[fut] = log_len;
+        }
+        last_regen = fut;
+      } else if constexpr (kMode == 2) {  // converged with the owner segment's run
+        if (sx->regpos && fut > a0 && __ldg(sx->regpos + fut) >= 0) {
+          j_stop = fut;
+          break;
+        }
+      }
       now = next_arr;  // idle until the next arrival (oracle.py:81-83)
 #ifdef TWB_PROFILE_PHASES
       const long long i0 = clock64();
       x_it_idle++;
 #endif
-      if (tk_on) tk_idle(g, ts, n, epoch, now);
+      if constexpr (kMode == 1) {
+        if (tk_on) {
+          if (lane == 0) sx->log[log_len] = TkLog{now, 0, 0};
+          log_len++;
+        }
+      } else {
+        if (tk_on) tk_idle(g, ts, n, epoch, now);
+      }
 #ifdef TWB_PROFILE_PHASES
       x_idle_cyc += clock64() - i0;
 #endif
@@ -850,6 +1063,7 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
     if (d < 0) {
       r.status = TW_SIM_PRED_ERROR;
       r.pred_code = (d % 1000 != 0) ? (int32_t)d : TW_PRED_NEGATIVE;  // a negative table row: engine limit
+      if constexpr (kMode != 0) w_head += n_adm;  // admitted (unstamped) before the error
       break;
     }
 
@@ -885,7 +1099,14 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       x_it_k1 += K == 1;
 #endif
       const long long c0 = TWB_CLK();
-      if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);  // WorkerGrid stage deadlines
+      if constexpr (kMode == 1) {  // logged, replayed after the segment's run (k_sim_seg)
+        if (tk_on) {
+          if (lane == 0) sx->log[log_len] = TkLog{now0, d, K};
+          log_len++;
+        }
+      } else {
+        if (tk_on) tk_run(g, ts, n, epoch, S, now0, d, K);  // WorkerGrid stage deadlines
+      }
       tk_cyc += TWB_CLK() - c0;
 #ifdef TWB_PROFILE_PHASES
       if (tk_on) {
@@ -910,7 +1131,11 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
       const uint64_t mA = m * TW_DIG_A;
 #pragma unroll 1
       for (int i = lane; i < D; i += 32)
-        em.dig += tw_event_mult((uint64_t)sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN) * (U + mA * (uint64_t)i);
+      {
+        const uint64_t mi = tw_event_mult((uint64_t)sl.req[sl.dlist[i]], TW_EV_OUTPUT_TOKEN);
+        em.dig += mi * (U + mA * (uint64_t)i);
+        em.msum += mi * m;
+      }
       if (em.evp) {  // audited config: the body's events themselves, flattened over the lanes
         const int q32 = 32 / D, r32 = 32 % D;
         int64_t j = lane / D;
@@ -987,8 +1212,14 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
                                      : pos_d + __popc(d1 & lt) + __popc(d2 & lt);
 #pragma unroll 1
         for (int t = 0; t < nev; t++) em.event_u(ps0 + t, rq, t ? TW_EV_FINISHED : k0, u_now, now, step);
-        if (k0 == TW_EV_FIRST_TOKEN && em.first) em.first[rq] = now;
-        if (nev == 2 && em.finish) em.finish[rq] = now;
+        if (kMode == 1 && rq >= a1) {  // overrun request: side buffer
+          int64_t* sp = sx->side + 2 * (int64_t)(rq - a1);
+          if (k0 == TW_EV_FIRST_TOKEN) sp[0] = now;
+          if (nev == 2) sp[1] = now;
+        } else {
+          if (k0 == TW_EV_FIRST_TOKEN && em.first) em.first[rq] = now;
+          if (nev == 2 && em.finish) em.finish[rq] = now;
+        }
       }
       pos_c += __popc(c1) + __popc(c2);
       pos_d += __popc(d1) + __popc(d2);
@@ -1066,6 +1297,35 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c) 
   uint64_t dig = em.dig;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dig += __shfl_xor_sync(kFull, dig, o);
+  if constexpr (kMode != 0) {
+    uint64_t ms = em.msum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ms += __shfl_xor_sync(kFull, ms, o);
+    SegSummary o;
+    o.j_stop = (r.status == TW_SIM_OK) ? j_stop : fut;
+    o.status = r.status;
+    o.last_regen = last_regen;
+    o.adm_end = w_head;
+    o.final_now = now;
+    o.events = n_events;
+    o.dig = dig;
+    o.msum = ms;
+    o.steps = step;
+    o.pred_code = r.pred_code;
+    o.log_len = log_len;
+    o.pad = 0;
+    o.tk = tk_state(g);  // mode 1: filled in by the replay (k_seg_tk)
+    o.d_lo = g.d_lo;
+    o.d_hi = g.d_hi;
+    if constexpr (kMode == 1) sx->log_len = log_len;
+    if constexpr (kMode == 1) {
+      __syncwarp();
+      if (lane == 0) *sx->sum = o;
+    } else {
+      sx->out = o;
+    }
+    return;
+  }
   r.final_now_ns = now;
   r.steps = step;
   r.events = n_events;
@@ -1168,7 +1428,483 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
   }
 }
 
-#ifdef TWB_SIM_TPUT_TU
+#ifdef TWB_SIM_SEG_TU
+// ---- busy-period segments: planner, speculative segments, join (sim_seg.cu) -------------
+
+// Segment boundaries: W = min(wmax, n / min_req) equal shares of the arrivals, each
+// boundary moved (within +-15 arrivals) to the largest inter-arrival gap, where the
+// engine is most likely to be empty. One warp per config.
+__global__ void __launch_bounds__(128) k_seg_plan(SimParams p, SegParams q) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= p.n_cfg) return;
+  const tw_sim_cfg cfg = p.cfgs[c];
+  const int64_t wl0 = p.wl_off[cfg.workload_id];
+  const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - wl0);
+  const int64_t* __restrict__ ts = p.ts + wl0;
+  int32_t W = n / q.min_req;
+  W = W < 1 ? 1 : (W > q.wmax ? q.wmax : W);
+  if (p.req_base[p.n_cfg] > q.r_max) W = 0;  // scratch too small for the per-request records
+  if (lane == 0) {
+    q.nseg[c] = W;
+    q.seg_a0[(int64_t)c * q.wmax] = 0;
+  }
+  if (W <= 1) return;
+  const int32_t len = n / W;
+  const int32_t h = min(15, len / 2 - 1);
+  for (int k = 1; k < W; k++) {
+    const int32_t center = (int32_t)((int64_t)k * n / W);
+    const int32_t j = center - h + lane;
+    int64_t gap = -1;
+    if (lane <= 2 * h && j >= 1 && j < n) gap = __ldg(ts + j) - __ldg(ts + j - 1);
+    const int64_t best = -warp_min_i64(-gap);
+    const unsigned m = __ballot_sync(kFull, gap == best);
+    if (lane == 0) q.seg_a0[(int64_t)c * q.wmax + k] = center - h + (__ffs(m) - 1);
+  }
+}
+
+// A segment's Timekeeper, replayed from its log after the run (a tight loop of its own,
+// so the event loop's code stays small): the config's start state for segment 0, else a
+// guess at arrival a0 (just broadcast, so last broadcast = wall; every earlier arrival
+// dispatched; wall 0). Records the state at each regeneration point and at the stop, and
+// the wall shifts [d_lo, d_hi) that keep every decision (tk_compose checks the truth).
+#ifdef TWB_SEG_REPLAY_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void seg_tk_replay(const SimParams& p, int c, int32_t a0, int32_t a1, int32_t n,
+                                           const TkLog* __restrict__ log, int32_t len_log,
+                                           const int32_t* __restrict__ regpos, SegRegen* reg, SegSummary* sum) {
+  const int lane = threadIdx.x & 31;
+  const tw_sim_cfg cfg = p.cfgs[c];
+  const int64_t wl0 = p.wl_off[cfg.workload_id];
+  const int64_t* __restrict__ ts = p.ts + wl0;
+  const int64_t epoch = cfg.epoch_ns;
+  const int S = cfg.pp_stages;
+  TkGrid g;
+  g.cooldown = cfg.tk_cooldown_ns;
+  g.conv_cooldown = g.cooldown > 0 ? cold_fake_sleep(g.cooldown) : 0;
+  g.rcp_cooldown = g.conv_cooldown > 0 ? __drcp_rn(__ll2double_rn(g.conv_cooldown)) : 0.0;
+  g.seq = 0;
+  g.d_lo = INT64_MIN;
+  g.d_hi = INT64_MAX;
+#ifdef TWB_PROFILE_PHASES
+  g.prof_calls = g.prof_fast = g.prof_loops = 0;
+#endif
+  if (a0 == 0) {
+    g.wall = epoch;
+    g.offset = 0;
+    g.last_bcast = INT64_MIN;
+    g.V = epoch;
+  } else {
+    g.wall = 0;
+    g.offset = 0;
+    g.last_bcast = 0;
+    g.V = 0;
+  }
+  g.disp = a0;
+  g.win.load(ts, n, epoch, a0);
+  g.disp_ts = a0 < n ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
+  // the regeneration points in order: jn (next), pn its log position
+  int32_t jn = a0, pn = 0;
+  auto next_regen = [&](int32_t from) {  // first j >= from in [from, a1) with regpos[j] >= 0
+    for (int32_t b = from; b < a1; b += 32) {
+      const int32_t j = b + lane;
+      const unsigned m = __ballot_sync(kFull, j < a1 && regpos[j] >= 0);
+      if (m) {
+        jn = b + __ffs(m) - 1;
+        pn = regpos[jn];
+        return;
+      }
+    }
+    jn = a1;
+    pn = INT32_MAX;
+  };
+  auto mark = [&](int32_t idx) {  // states at the regeneration points logged at idx
+    while (pn == idx) {
+      if (lane == 0) reg[jn].tk = tk_state(g);
+      next_regen(jn + 1);
+    }
+  };
+#pragma unroll 1
+  for (int32_t b = 0; b < len_log; b += 32) {
+    int64_t x0 = 0, x1 = 0, x2 = 0;
+    if (b + lane < len_log) {
+      const TkLog* e = log + b + lane;
+      x0 = e->now0;
+      x1 = e->d;
+      x2 = e->K;
+    }
+    const int m = min(32, len_log - b);
+#pragma unroll 1
+    for (int k = 0; k < m; k++) {
+      mark(b + k);
+      const int64_t now0 = __shfl_sync(kFull, x0, k), d = __shfl_sync(kFull, x1, k), K = __shfl_sync(kFull, x2, k);
+      if (K == 0) tk_idle<true>(g, ts, n, epoch, now0);
+      else tk_run<true>(g, ts, n, epoch, S, now0, d, K);
+    }
+  }
+  mark(len_log);
+  if (lane == 0) {
+    sum->tk = tk_state(g);
+    sum->d_lo = g.d_lo;
+    sum->d_hi = g.d_hi;
+  }
+}
+
+// Speculative segments: warps pull (config, segment) pairs, heaviest configs first.
+__global__ void __launch_bounds__(kSimThreads, TWB_SIM_TPUT_MIN_BLOCKS) k_sim_seg(SimParams p, SegParams q) {
+  extern __shared__ __align__(128) char smem[];
+  const char* ps = static_cast<const char*>(p.pset);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* base = reinterpret_cast<int32_t*>(smem + 128) + (size_t)warp * 7 * p.cap;
+  Slots sl;
+  sl.req = base;
+  sl.prompt = base + p.cap;
+  sl.output = base + 2 * p.cap;
+  sl.done = base + 3 * p.cap;
+  sl.emit = base + 4 * p.cap;
+  sl.plan = base + 5 * p.cap;
+  sl.dlist = base + 6 * p.cap;
+  const int64_t n_items = (int64_t)p.n_cfg * q.wmax;
+  for (;;) {
+    int64_t idx = 0;
+    if (lane == 0) idx = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(q.counter), 1ULL);
+    idx = __shfl_sync(kFull, idx, 0);
+    if (idx >= n_items) break;
+    const int32_t rank = (int32_t)(idx / q.wmax), w = (int32_t)(idx - (int64_t)rank * q.wmax);
+    const int c = p.order ? p.order[rank] : rank;
+    const int32_t W = q.nseg[c];
+    if (w >= W) continue;
+    const tw_sim_cfg& cfg = p.cfgs[c];
+    const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - p.wl_off[cfg.workload_id]);
+    const int64_t rb = p.req_base[c];
+    SegCtx sx;
+    sx.a0 = q.seg_a0[(int64_t)c * q.wmax + w];
+    sx.a1 = (w + 1 < W) ? q.seg_a0[(int64_t)c * q.wmax + w + 1] : n;
+    const int32_t len = sx.a1 - sx.a0;
+    const int64_t unit = rb + sx.a0 + q.xtra * ((int64_t)c * q.wmax + w);  // this segment's room
+    sx.log = q.log + (int64_t)kSegLogPerReq * unit;
+    sx.log_cap = (int32_t)(kSegLogPerReq * (len + q.xtra) / q.cap_div);
+    sx.side = q.side + 8 * unit;
+    sx.side_cap = (int32_t)(4 * (len + q.xtra) / q.cap_div);
+    sx.regpos = q.regpos + rb;
+    sx.reg = q.reg + rb;
+    sx.g = nullptr;
+    sx.sum = q.summ + (int64_t)c * q.wmax + w;
+    run_config<true, 1>(p, ps, sl, c, &sx);
+    __syncwarp();
+    if (lane == 0) sx.sum->log_len = sx.log_len;
+    __syncwarp();
+  }
+}
+
+// The segments' Timekeeper replays, one warp per (config, segment), in a kernel of their
+// own: inside k_sim_seg the replay loop next to the event loop pushed the kernel's code
+// past the instruction caches (ncu: stall_no_inst 46%, 7.3 ms vs 3.8 + this kernel).
+__global__ void __launch_bounds__(128) k_seg_tk(SimParams p, SegParams q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_items = (int64_t)p.n_cfg * q.wmax;
+  for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < n_items;
+       idx += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int32_t rank = (int32_t)(idx / q.wmax), w = (int32_t)(idx - (int64_t)rank * q.wmax);
+    const int c = p.order ? p.order[rank] : rank;
+    const int32_t W = q.nseg[c];
+    if (w >= W) continue;
+    const tw_sim_cfg& cfg = p.cfgs[c];
+    if (!(cfg.flags & TW_SIM_TIMEKEEPER)) continue;
+    const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - p.wl_off[cfg.workload_id]);
+    const int64_t rb = p.req_base[c];
+    const int32_t a0 = q.seg_a0[(int64_t)c * q.wmax + w];
+    const int32_t a1 = (w + 1 < W) ? q.seg_a0[(int64_t)c * q.wmax + w + 1] : n;
+    SegSummary* sum = q.summ + (int64_t)c * q.wmax + w;
+    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY) continue;
+    seg_tk_replay(p, c, a0, a1, n, q.log + (int64_t)kSegLogPerReq * (rb + a0 + q.xtra * ((int64_t)c * q.wmax + w)),
+                  sum->log_len, q.regpos + rb,
+                  q.reg + rb, sum);
+    (void)lane;
+  }
+}
+
+// Carries the true Timekeeper g across a speculative piece: E is the piece's speculative
+// state before the idle round at its entry arrival j, T its state at the piece's end,
+// [d_lo, d_hi) the wall shifts its decisions allow. Both runs are empty at j; the idle
+// round at j lands both on V = ts_j after the same sleep when (a) both dispatchers wait
+// for arrival j, (b) last broadcast - wall agree, (c) both V lie below ts_j - sleep. From
+// there the true run is the speculative one with its wall shifted by delta (offset by
+// -delta), provided delta keeps every wall decision. Returns false when that cannot be
+// shown (the caller re-runs the piece serially); `exact` (the config's own start) copies.
+__device__ __forceinline__ bool tk_compose(TkGrid& g, const TkState& E, const TkState& T, int64_t d_lo,
+                                           int64_t d_hi, bool exact, int32_t j, const int64_t* __restrict__ ts,
+                                           int32_t n, int64_t epoch) {
+  int64_t delta = 0;
+  if (!exact) {
+    if (g.disp != j || E.disp != j) return false;
+    const bool set_t = g.last_bcast != INT64_MIN, set_e = E.last_bcast != INT64_MIN;
+    if (set_t != set_e || (set_t && g.last_bcast - g.wall != E.last_bcast - E.wall)) return false;
+    int64_t slp = 0;
+    if (set_t && g.cooldown > 0) {
+      const int64_t wait = g.last_bcast + g.cooldown - g.wall;
+      if (wait > 0) slp = (wait == g.cooldown) ? g.conv_cooldown : cold_fake_sleep(wait);
+    }
+    const int64_t tj = epoch + __ldg(ts + j);
+    if (!(g.wall + g.offset < tj - slp) || !(E.wall + E.offset < tj - slp)) return false;
+    delta = g.wall - E.wall;
+    if (delta < d_lo || delta >= d_hi) return false;
+  }
+  g.wall = T.wall + delta;
+  g.seq += T.seq - E.seq;
+  g.last_bcast = T.last_bcast == INT64_MIN ? INT64_MIN : T.last_bcast + delta;
+  g.offset = T.offset - delta;
+  g.V = g.wall + g.offset;
+  g.disp = T.disp;
+  g.win.load(ts, n, epoch, T.disp);
+  g.disp_ts = T.disp < n ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
+  return true;
+}
+
+// The join pass: one warp per config walks the chain of valid pieces (a segment from its
+// entry point to its stop; where a segment's stop is not a regeneration point of the next
+// run, or its Timekeeper cannot be carried over, a serial piece in mode 2 until the chain
+// meets a regeneration point again), adds each piece's counters in the true frame
+// (positions and steps shifted: digest += msum * (dk*A + ds*G)), carries the Timekeeper,
+// copies overrun stamps and writes the config's record.
+__global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegParams q) {
+  extern __shared__ __align__(128) char smem[];
+  const char* ps = static_cast<const char*>(p.pset);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* base = reinterpret_cast<int32_t*>(smem + 128) + (size_t)warp * 7 * p.cap;
+  Slots sl;
+  sl.req = base;
+  sl.prompt = base + p.cap;
+  sl.output = base + 2 * p.cap;
+  sl.done = base + 3 * p.cap;
+  sl.emit = base + 4 * p.cap;
+  sl.plan = base + 5 * p.cap;
+  sl.dlist = base + 6 * p.cap;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(q.counter + 2, 1);
+    idx = __shfl_sync(kFull, idx, 0);
+    if (idx >= p.n_cfg) break;
+    const int c = p.order ? p.order[idx] : idx;
+    const tw_sim_cfg cfg = p.cfgs[c];
+    const int64_t wl0 = p.wl_off[cfg.workload_id];
+    const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - wl0);
+    const int64_t* __restrict__ ts = p.ts + wl0;
+    const int64_t epoch = cfg.epoch_ns;
+    const bool tk_on = (cfg.flags & TW_SIM_TIMEKEEPER) != 0;
+    const int64_t rb = p.req_base[c];
+    const int32_t W = q.nseg[c];
+    const int32_t* a0s = q.seg_a0 + (int64_t)c * q.wmax;
+    const SegSummary* sm = q.summ + (int64_t)c * q.wmax;
+    int32_t* regpos = q.regpos + rb;
+    SegRegen* reg = q.reg + rb;
+    int64_t* first = p.first ? p.first + rb : nullptr;
+    int64_t* finish = p.finish ? p.finish + rb : nullptr;
+
+    TkGrid g;
+    g.wall = epoch;
+    g.offset = 0;
+    g.seq = 0;
+    g.last_bcast = INT64_MIN;
+    g.V = epoch;
+    g.cooldown = cfg.tk_cooldown_ns;
+    g.conv_cooldown = g.cooldown > 0 ? cold_fake_sleep(g.cooldown) : 0;
+    g.rcp_cooldown = g.conv_cooldown > 0 ? __drcp_rn(__ll2double_rn(g.conv_cooldown)) : 0.0;
+    g.disp = 0;
+    g.d_lo = INT64_MIN;
+    g.d_hi = INT64_MAX;
+#ifdef TWB_PROFILE_PHASES
+    g.prof_calls = g.prof_fast = g.prof_loops = 0;
+#endif
+    g.win.load(ts, n, epoch, 0);
+    g.disp_ts = n > 0 ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
+
+    int64_t ev_t = 0, now_t = epoch;
+    uint64_t dig_t = 0;
+    int32_t st_t = 0, status = TW_SIM_OK, pred_code = 0, adm_end = 0;
+    bool invalid_cfg = false;
+    // a piece's counters relative to its entry record e, moved into the true frame
+    auto add = [&](int64_t ev, uint64_t dg, uint64_t ms, int32_t st, const SegRegen& e) {
+      const uint64_t dm = ms - e.msum;
+      dig_t += (dg - e.dig) +
+               ((uint64_t)(ev_t - e.events) * TW_DIG_A + (uint64_t)(int64_t)(st_t - e.steps) * TW_DIG_G) * dm;
+      ev_t += ev - e.events;
+      st_t += st - e.steps;
+    };
+    auto copy_side = [&](int32_t w, int32_t lo, int32_t hi) {  // overrun stamps of segment w
+      const int64_t* side = q.side + 8 * (rb + a0s[w] + q.xtra * ((int64_t)c * q.wmax + w));
+      const int32_t a1 = (w + 1 < W) ? a0s[w + 1] : n;
+      for (int32_t i = lo + lane; i < hi; i += 32) {
+        if (first) first[i] = side[2 * (int64_t)(i - a1)];
+        if (finish) finish[i] = side[2 * (int64_t)(i - a1) + 1];
+      }
+    };
+    auto owner = [&](int32_t j) {
+      int32_t lo = 0, hi = W - 1;  // the last segment whose first arrival is <= j
+      while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) >> 1;
+        if (a0s[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+
+    int32_t w = 0, j_in = 0, js = 0, n_joined = 0, n_serial = 0, n_tkfail = 0, n_ovf = 0, n_noconv = 0;
+    SegRegen e{};
+    bool exact = true;     // the chain's first piece starts with the config (no guess)
+    bool serial = W == 0;  // not segmented: the whole config serially from arrival 0
+    for (;;) {
+      if (!serial) {
+        const SegSummary s = sm[w];
+        const int32_t a1w = (w + 1 < W) ? a0s[w + 1] : n;
+        if (s.status == TW_SIM_BAD_CONFIG || s.status == TW_SIM_CAPACITY) {
+          status = s.status;
+          invalid_cfg = true;
+          break;
+        }
+        if (exact) e = reg[0];
+        if (s.status == kSegOverflow) {
+          // valid from the entry up to its last regeneration point, serial from there
+          n_ovf++;
+          const int32_t jr = s.last_regen;
+          const SegRegen E = reg[jr];
+          if (!tk_on || tk_compose(g, e.tk, E.tk, s.d_lo, s.d_hi, exact, j_in, ts, n, epoch)) {
+            add(E.events, E.dig, E.msum, E.steps, e);
+            js = jr;
+          } else {
+            js = j_in;
+            n_tkfail++;
+          }
+          serial = true;
+        } else if (tk_on && !tk_compose(g, e.tk, s.tk, s.d_lo, s.d_hi, exact, j_in, ts, n, epoch)) {
+          js = j_in;  // the Timekeeper guess does not carry over: this piece serially
+          serial = true;
+          n_tkfail++;
+        } else {
+          n_joined++;
+          add(s.events, s.dig, s.msum, s.steps, e);
+          now_t = s.final_now;
+          if (s.status != TW_SIM_OK) {
+            status = s.status;
+            pred_code = s.pred_code;
+            adm_end = s.adm_end;
+            if (adm_end > a1w) copy_side(w, a1w, adm_end);
+            break;
+          }
+          if (s.j_stop > a1w) copy_side(w, a1w, s.j_stop);
+          if (s.j_stop >= n) break;
+          js = s.j_stop;
+          if (regpos[js] >= 0) {  // the owner's run was empty at js too: continue with it
+            w = owner(js);
+            e = reg[js];
+            j_in = js;
+            exact = false;
+            continue;
+          }
+          n_noconv++;
+          serial = true;
+        }
+      }
+      // a serial piece from arrival js (the engine empty there), the true Timekeeper inline
+      SegCtx sx;
+      sx.a0 = js;
+      sx.a1 = n;
+      sx.side = nullptr;
+      sx.side_cap = 0;
+      sx.regpos = W > 0 ? regpos : nullptr;
+      sx.reg = reg;
+      sx.g = &g;
+      sx.sum = nullptr;
+      run_config<true, 2>(p, ps, sl, c, &sx);
+      n_serial++;
+      const SegSummary s2 = sx.out;
+      const SegRegen z{};
+      if (s2.status == TW_SIM_BAD_CONFIG || s2.status == TW_SIM_CAPACITY) {
+        status = s2.status;
+        invalid_cfg = true;
+        break;
+      }
+      add(s2.events, s2.dig, s2.msum, s2.steps, z);
+      now_t = s2.final_now;
+      if (s2.status != TW_SIM_OK) {
+        status = s2.status;
+        pred_code = s2.pred_code;
+        adm_end = s2.adm_end;
+        break;
+      }
+      if (s2.j_stop >= n) break;
+      js = s2.j_stop;  // converged: a regeneration point of its owner's run
+      w = owner(js);
+      e = reg[js];
+      j_in = js;
+      exact = false;
+      serial = false;
+    }
+    if (status != TW_SIM_OK && !invalid_cfg && W > 0) {
+      // the run stopped early: requests a speculative segment stamped past the stop are
+      // reset to unset (-1)
+      for (int32_t v = 0; v < W; v++) {
+        const int32_t a0v = a0s[v], a1v = (v + 1 < W) ? a0s[v + 1] : n;
+        const int32_t lo = max(a0v, adm_end), hi = min(a1v, sm[v].adm_end);
+        for (int32_t i = lo + lane; i < hi; i += 32) {
+          if (first) first[i] = -1;
+          if (finish) finish[i] = -1;
+        }
+      }
+    }
+    tw_sim_result r;
+    r.final_now_ns = invalid_cfg ? epoch : now_t;
+    r.steps = invalid_cfg ? 0 : st_t;
+    r.events = invalid_cfg ? 0 : ev_t;
+    r.digest = invalid_cfg ? 0 : dig_t;
+    r.tk_seq = 0;
+    r.tk_offset_ns = 0;
+    r.tk_wall_ns = 0;
+    if (tk_on && !invalid_cfg) {
+      r.tk_seq = g.seq;
+      r.tk_offset_ns = g.offset;
+      r.tk_wall_ns = g.wall;
+    }
+    r.status = status;
+    r.pred_code = pred_code;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_system();
+      p.res[c] = r;
+      if (q.stats) {
+        int32_t* st = q.stats + 8 * (int64_t)c;
+        st[0] = W;
+        st[1] = n_joined;
+        st[2] = n_serial;
+        st[3] = n_tkfail;
+        st[4] = n_ovf;
+        st[5] = n_noconv;
+        st[6] = 0;
+        st[7] = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+int sim_seg_prepare(int threads, size_t smem, int* per_sm) {
+  cudaFuncSetAttribute(k_sim_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_sim_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg, threads, smem);
+}
+void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
+                    int join_grid) {
+  k_seg_plan<<<(p.n_cfg + 3) / 4, 128, 0, s>>>(p, q);
+  k_sim_seg<<<grid, threads, smem, s>>>(p, q);
+  const int64_t items = (int64_t)p.n_cfg * q.wmax;
+  k_seg_tk<<<(int)std::min<int64_t>((items + 3) / 4, 148 * 16), 128, 0, s>>>(p, q);
+  k_sim_join<<<join_grid, threads, smem, s>>>(p, q);
+}
+}  // namespace twb
+#elif defined(TWB_SIM_TPUT_TU)
 // sim_tput.cu compiles this file a second time for the throughput variant alone: with
 // both variants in one translation unit the shared helpers stop being inlined into the
 // latency variant, whose blob reads then turn from LDS into generic loads (164 -> 173
@@ -1205,7 +1941,52 @@ int sim_big_prepare(int threads, int* per_sm);  // sim_big.cu
 void sim_big_launch(int grid, int threads, cudaStream_t s, const SimParams& p);
 int sim_check_prepare(int threads, size_t smem, int* per_sm);  // sim_check.cu
 void sim_check_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
+int sim_seg_prepare(int threads, size_t smem, int* per_sm);  // sim_seg.cu
+void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
+                    int join_grid);
 static thread_local int32_t* g_checks = nullptr;
+
+// ---- busy-period segments (latency regime): scratch layout ----------------------------
+// [64 B counters | nseg[n_cfg] | seg_a0[n_cfg*W] | summ[n_cfg*W] |
+//  regpos[R] | reg[R] | log[kSegLogPerReq*(R+X)] | side[8*(R+X)]], X = xtra * segments,
+//  R (request capacity) = what the rest of scratch holds
+constexpr int kSegMinReq = 16;
+constexpr int64_t kSegPerReqBytes =
+    (int64_t)sizeof(int32_t) + (int64_t)sizeof(SegRegen) + 8 * (int64_t)sizeof(int64_t) +
+    kSegLogPerReq * (int64_t)sizeof(TkLog);
+static int64_t align256(int64_t x) { return (x + 255) & ~255LL; }
+static int seg_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+static bool seg_enabled_for(int32_t n_cfg, int sms) {
+  const char* e = getenv("TWB_SIM_SEG");
+  if (e && e[0] == '0') return false;
+  return n_cfg >= 1 && (int64_t)n_cfg <= (int64_t)kLatencyConfigsPerSm * sms;
+}
+static int seg_wmax(int32_t n_cfg, int sms) {
+  const char* e = getenv("TWB_SIM_SEG_W");
+  int64_t w = e ? atoll(e) : 0;
+  if (w <= 0) w = ((int64_t)sms * 16 * 7 + n_cfg - 1) / n_cfg;  // ~7 segments per resident warp
+  if (w > 256) w = 256;
+  if (w < 1) w = 1;
+  return (int)w;
+}
+static int64_t seg_xtra(int32_t n_cfg, int wmax) {  // ~256 MB of overrun room in all
+  const int64_t per = kSegLogPerReq * (int64_t)sizeof(TkLog) + 64;
+  int64_t x = (256LL << 20) / (per * (int64_t)n_cfg * wmax);
+  return x < 64 ? 64 : (x > 4096 ? 4096 : x);
+}
+static int64_t seg_header_bytes(int32_t n_cfg, int wmax) {  // counters, plan, summaries
+  return align256(64 + align256(4LL * n_cfg) + align256(4LL * n_cfg * wmax) +
+                  align256((int64_t)sizeof(SegSummary) * n_cfg * wmax));
+}
+static int64_t seg_fixed_bytes(int32_t n_cfg, int wmax) {  // plus every segment's extra room
+  return seg_header_bytes(n_cfg, wmax) +
+         seg_xtra(n_cfg, wmax) * n_cfg * wmax * (kSegLogPerReq * (int64_t)sizeof(TkLog) + 64);
+}
 
 // bytes of scratch tw_sim_many needs: the 64-byte work counter, plus the global slot state
 // of every resident warp when the capacity exceeds what shared memory holds
@@ -1220,6 +2001,7 @@ static int64_t sim_scratch_bytes(int32_t n_cfg, int cap, int sms, int per_sm, in
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
 static thread_local int64_t* g_prof = nullptr;
+static thread_local int32_t* g_seg_stats = nullptr;
 
 }  // namespace twb
 
@@ -1301,6 +2083,76 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   }
   // slot state is 7 int32 arrays of cap per warp: large capacities get fewer warps per CTA
   const size_t per_warp = 7 * sizeof(int32_t) * (size_t)cap;
+  // latency regime: busy-period segments when the caller gave per-request bases and the
+  // scratch for the segment records (tw_sim_seg_scratch_bytes); not with event dumps,
+  // profiling or the invariant build, which run the serial loop
+  if (req_base && !ev && !g_checks && !g_prof && seg_enabled_for(n_cfg, sms) &&
+      128 + 4 * per_warp <= (size_t)max_optin) {
+    const int wmax = seg_wmax(n_cfg, sms);
+    const int64_t fixed = seg_fixed_bytes(n_cfg, wmax);
+    if (scratch_bytes >= fixed + kSegPerReqBytes + 4 * 256) {
+      const int64_t r_max = (scratch_bytes - fixed - 4 * 256) / kSegPerReqBytes;
+      char* b = static_cast<char*>(scratch);
+      SegParams q;
+      q.wmax = wmax;
+      q.min_req = kSegMinReq;
+      q.counter = reinterpret_cast<int32_t*>(b);
+      int64_t o = 64;
+      q.nseg = reinterpret_cast<int32_t*>(b + o);
+      o += align256(4LL * n_cfg);
+      q.seg_a0 = reinterpret_cast<int32_t*>(b + o);
+      o += align256(4LL * n_cfg * wmax);
+      q.summ = reinterpret_cast<SegSummary*>(b + o);
+      o = seg_header_bytes(n_cfg, wmax);
+      q.regpos = reinterpret_cast<int32_t*>(b + o);
+      o += align256(4 * r_max);
+      q.reg = reinterpret_cast<SegRegen*>(b + o);
+      o += align256((int64_t)sizeof(SegRegen) * r_max);
+      q.xtra = seg_xtra(n_cfg, wmax);
+      const int64_t units = r_max + q.xtra * n_cfg * wmax;  // fixed part counted the xtra bytes
+      q.log = reinterpret_cast<TkLog*>(b + o);
+      o += align256((int64_t)sizeof(TkLog) * kSegLogPerReq * units);
+      q.side = reinterpret_cast<int64_t*>(b + o);
+      q.r_max = r_max;
+      const char* cd = getenv("TWB_SIM_SEG_CAPDIV");  // tests only: force the overflow path
+      q.cap_div = cd && atoi(cd) > 1 ? atoi(cd) : 1;
+      q.stats = g_seg_stats;
+      const int threads = kSimThreads;
+      const size_t smem = 128 + 4 * per_warp;
+      sim_seg_prepare(threads, smem, &per_sm);
+      if (per_sm < 1) per_sm = 1;
+      cudaMemsetAsync(scratch, 0, 64, s);
+      cudaMemsetAsync(q.regpos, 0xff, 4 * r_max, s);
+      p.pset = pset;
+      p.pset_bytes = (uint32_t)pset_bytes;
+      p.pset_smem = 0;
+      p.cfgs = cfgs;
+      p.n_cfg = n_cfg;
+      p.order = order;
+      p.wl_off = wl_off;
+      p.ts = req_offset_ns;
+      p.prompt = req_prompt;
+      p.output = req_output;
+      p.res = results;
+      p.req_base = req_base;
+      p.first = req_first_ns;
+      p.finish = req_finish_ns;
+      p.ev_off = nullptr;
+      p.ev = nullptr;
+      p.counter = q.counter;
+      p.cap = cap;
+      p.prof = nullptr;
+      const int grid = sms * per_sm;
+      const int join_grid = (int)std::min<int64_t>(((int64_t)n_cfg + kSimWarps - 1) / kSimWarps, (int64_t)grid);
+      sim_seg_launch(grid, threads, smem, s, p, q, join_grid);
+      for (int k = 0; k < 4; k++) count_launch();  // plan, segments, Timekeeper replays, join
+      g_last[0] = grid;
+      g_last[1] = threads;
+      g_last[2] = (int32_t)smem;
+      g_last[3] = cap;
+      return check_launch("tw_sim_many");
+    }
+  }
   // more configs than 8 per SM, or a blob too large to stage next to one warp's slot
   // state: the throughput variant (blob read from global memory)
   const uint32_t blob_smem = (uint32_t)((pset_bytes + 127) & ~127LL);
@@ -1370,8 +2222,20 @@ extern "C" int64_t tw_sim_scratch_bytes(int32_t n_cfg, int32_t slot_capacity) {
   return sim_scratch_bytes(n_cfg, cap, sms, per_sm, nullptr);
 }
 
+extern "C" int64_t tw_sim_seg_scratch_bytes(int32_t n_cfg, int64_t total_requests) {
+  const int sms = seg_sms();
+  if (!seg_enabled_for(n_cfg, sms) || total_requests < 0) return 0;
+  const int wmax = seg_wmax(n_cfg, sms);
+  return seg_fixed_bytes(n_cfg, wmax) + 4 * 256 + kSegPerReqBytes * (total_requests > 0 ? total_requests : 1);
+}
+
 extern "C" int tw_sim_set_checks(int32_t* per_config_8xi32) {
   g_checks = per_config_8xi32;
+  return TW_OK;
+}
+
+extern "C" int tw_sim_set_seg_stats(int32_t* per_config_8xi32) {
+  g_seg_stats = per_config_8xi32;
   return TW_OK;
 }
 

@@ -296,9 +296,14 @@ class DeviceSweep:
         self.d_prompt = to_device(workloads.prompt, dev)
         self.d_output = to_device(workloads.output, dev)
         self.d_res = torch.zeros(self.n_cfg * SIM_RESULT_DTYPE.itemsize + 16, dtype=torch.uint8, device=dev)
-        scratch = int(_lib.load().tw_sim_scratch_bytes(self.n_cfg, self.slot_capacity)) if self.n_cfg else 64
-        self.d_scratch = torch.zeros(max(64, scratch), dtype=torch.uint8, device=dev)
         total_req = int(self.req_base[-1])
+        lib = _lib.load()
+        scratch = int(lib.tw_sim_scratch_bytes(self.n_cfg, self.slot_capacity)) if self.n_cfg else 64
+        # latency regime: records of the busy-period segments (tw_sim_seg_scratch_bytes; the
+        # library picks them when req_base is passed, i.e. with per-request stamps)
+        if per_request and self.n_cfg and not audit:
+            scratch = max(scratch, int(lib.tw_sim_seg_scratch_bytes(self.n_cfg, total_req)))
+        self.d_scratch = torch.zeros(max(64, scratch), dtype=torch.uint8, device=dev)
         self.per_request = per_request
         if per_request:
             self.d_req_base = to_device(self.req_base, dev)
