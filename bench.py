@@ -563,6 +563,9 @@ def configs_1_3(device):
         durs = time_kernel_steps(d.run, 5, 2, flush, torch.cuda.current_stream(device))
         ms = sum(durs) / len(durs)
         r = d.fetch().results
+        with _Env(TWB_SIM_SEG=0):  # the serial loop (one warp), for comparison
+            serial_ms = time_alone(sw, device)
+        stats = seg_stats(sw, device)
         vs = float(r["final_now_ns"][0] - sw.cfgs["epoch_ns"][0]) / 1e9
         t0 = time.perf_counter()
         cres, *_ = orc.sim_many(sw.pset.blob, sw.cfgs, sw.workloads.wl_off, sw.workloads.offset_ns,
@@ -570,6 +573,7 @@ def configs_1_3(device):
         c_s = time.perf_counter() - t0
         rec = {"label": sw.configs[0].label, "requests": int(sw.workloads.sizes()[0]), "steps": int(r["steps"][0]),
                "virtual_s": round(vs, 3), "gpu_ms": round(ms, 4), "gpu_virtual_s_per_wall_s": round(vs / (ms / 1e3), 1),
+               "gpu_serial_loop_ms": round(serial_ms, 4), "segments": stats,
                "c_port_one_thread_ms": round(c_s * 1e3, 2), "c_port_matches": bool((cres == r).all())}
         if os.path.isdir(os.path.join(REF_DIR, "timewarp")):
             t0 = time.perf_counter()
@@ -930,16 +934,94 @@ def main():
         torch.distributed.destroy_process_group()
 
 
+class _Env:
+    """Library switches for one measurement (read by libtwb200 at launch time)."""
+
+    def __init__(self, **env):
+        self.env = {k: str(v) for k, v in env.items()}
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.env}
+        os.environ.update(self.env)
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def seg_stats(sw, device):
+    """Busy-period segment statistics of one extra (untimed) launch (tw_sim_set_seg_stats)."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    d = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, device=device, per_request=True)
+    st = torch.zeros(8 * len(sw), dtype=torch.int32, device=device)
+    _lib.load().tw_sim_set_seg_stats(st.data_ptr())
+    try:
+        d.run()
+        torch.cuda.synchronize(device)
+    finally:
+        _lib.load().tw_sim_set_seg_stats(None)
+    path = _lib.last_sim_launch()["variant"]
+    s = st.view(-1, 8).cpu().numpy().astype(np.int64).sum(0)
+    del d
+    if path != "segments":
+        return {"path": path}
+    return {"path": path, "segments": int(s[0]), "joined_from_segment_runs": int(s[1]),
+            "serial_pieces_in_join": int(s[2]), "timekeeper_carry_refused": int(s[3]),
+            "segments_out_of_room": int(s[4]), "stops_not_regeneration_points": int(s[5])}
+
+
+def seg_roofline(sw, ms, device, sm_mhz, key):
+    """The segmented path's line (latency regime): the issue-slot roofline of its four kernels
+    together (k_seg_plan, k_sim_seg, k_seg_tk, k_sim_join; ncu instruction count of this code
+    version, profiles/traffic.json) over the live launch time, the segment statistics, and
+    the serial loop (one warp per config, TWB_SIM_SEG=0) timed beside it with its critical
+    chain (the heaviest config alone)."""
+    import torch
+
+    from paper_2601_00397_b200 import _lib
+
+    launch = _lib.last_sim_launch()
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    stats = seg_stats(sw, device)
+    with _Env(TWB_SIM_SEG=0):
+        serial_ms = time_alone(sw, device)
+        cyc, iters = ksim_profile(sw, device)
+        heavy = int(np.argmax(cyc))
+        heavy_serial = time_alone(sw.subset([heavy]), device)
+    heavy_seg = time_alone(sw.subset([heavy]), device)
+    extra = {"kernel": "k_seg_plan + k_sim_seg + k_seg_tk + k_sim_join", "launch": launch,
+             "segments": stats,
+             "serial_loop": {"ms": round(serial_ms, 4), "speedup": round(serial_ms / ms, 3),
+                             "cycles_per_iteration": round(float(cyc.sum() / max(iters.sum(), 1)), 1),
+                             "heaviest_config": heavy, "heaviest_label": sw.configs[heavy].label,
+                             "heaviest_alone_ms": round(heavy_serial, 4),
+                             "heaviest_alone_segmented_ms": round(heavy_seg, 4)},
+             "meaning": "each config's arrivals split into busy-period segments simulated in parallel and "
+                        "joined: the sweep is issue-bound instead of bound by its longest serial chain"}
+    return issue_roofline(key, ms, sm_mhz, sms, extra)
+
+
 def config4_block(args, device, cdev, peak_gbs):
     """BASELINE config 4 (the 1,024-config sweep on one B200): the same measurements as
     the headline at N = 1, reported beside it."""
-    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200 import _lib, presets
 
     sw = presets.sweep_1024(model="8b", seed=1)
     sw.global_ids = np.arange(len(sw), dtype=np.int64)
     sw.n_global = len(sw)
     r = measure_sweep(sw, args, 1, 0, device, cdev, False, "config 4")
-    roof = ksim_roofline(sw, r["dev"], r["ms"], device, peak_gbs, r["clocks"].get("sm_mhz"), "k_sim")
+    sm_mhz = r["clocks"].get("sm_mhz")
+    if _lib.last_sim_launch()["variant"] == "segments":
+        roof = seg_roofline(sw, r["ms"], device, sm_mhz, "k_sim_seg")
+    else:
+        roof = ksim_roofline(sw, r["dev"], r["ms"], device, peak_gbs, sm_mhz, "k_sim")
     return {"workload": "BASELINE config 4: 1,024 configs (Llama-3-8B tables, 1,000 requests, qps 8, seed 1)",
             "value": round(r["vsec"] / (r["ms_max"] / 1e3), 1), "unit": "virtual-s/wall-s",
             "ms_per_step": round(r["ms_max"], 4), "steps_per_s": round(r["steps"] / (r["ms_max"] / 1e3), 1),

@@ -369,6 +369,10 @@ int tw_sim_set_seg_stats(int32_t* per_config_8xi32);
  * (for the bench's roofline bookkeeping). */
 int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes,
                        int32_t* slot_capacity);
+/* Which event loop the last tw_sim_many on this thread ran: 0 latency variant (one warp
+ * per config), 1 throughput variant, 2 busy-period segments (plan, segments, Timekeeper
+ * replays, join; the geometry above is the segments kernel's), 3 slot state in scratch. */
+int tw_sim_last_path(void);
 
 /* Opt-in instrumentation for the next tw_sim_many calls on this thread: when set
  * (device pointer, 16 int64 per config; NULL disables), each config records

@@ -187,6 +187,7 @@ EXPORTED_SYMBOLS = (
     "tw_sim_set_seg_stats",
     "tw_sim_set_checks",
     "tw_sim_last_launch",
+    "tw_sim_last_path",
     "tw_sim_set_profile",
     "tw_metrics_many",
     "tw_metrics_scratch_bytes",
@@ -239,6 +240,7 @@ _SIGNATURES = {
     "tw_sim_set_seg_stats": (_I32, [_P]),
     "tw_sim_set_checks": (_I32, [_P]),
     "tw_sim_last_launch": (_I32, [_P, _P, _P, _P]),
+    "tw_sim_last_path": (_I32, []),
     "tw_sim_set_profile": (_I32, [_P]),
     "tw_metrics_many": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _I64, _P, _P]),
     "tw_metrics_scratch_bytes": (_I64, [_I32, _I32]),
@@ -296,6 +298,5 @@ def last_sim_launch() -> dict:
         "block": vals[1].value,
         "smem_bytes": vals[2].value,
         "slot_capacity": vals[3].value,
-        # the throughput variant keeps only slot state in shared memory (twb200.h)
-        "variant": "throughput" if vals[2].value == 128 + (vals[1].value // 32) * 7 * 4 * vals[3].value else "latency",
+        "variant": ("latency", "throughput", "segments", "global-slots")[load().tw_sim_last_path() & 3],
     }

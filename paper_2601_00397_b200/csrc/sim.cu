@@ -1554,11 +1554,15 @@ void seg_tk_replay(const SimParams& p, int c, int32_t a0, int32_t a1, int32_t n,
 }
 
 // Speculative segments: warps pull (config, segment) pairs, heaviest configs first.
-__global__ void __launch_bounds__(kSimThreads, TWB_SIM_TPUT_MIN_BLOCKS) k_sim_seg(SimParams p, SegParams q) {
+// kLat: the latency variant's geometry instead (blob staged in shared memory, registers
+// up to 3 CTAs per SM), an A/B alternative (TWB_SIM_SEG_LAT)
+template <bool kLat>
+__global__ void __launch_bounds__(kSimThreads, kLat ? 3 : TWB_SIM_TPUT_MIN_BLOCKS) k_sim_seg(SimParams p, SegParams q) {
   extern __shared__ __align__(128) char smem[];
-  const char* ps = static_cast<const char*>(p.pset);
+  const char* ps = kLat ? smem + 128 : static_cast<const char*>(p.pset);
+  if constexpr (kLat) tma_stage_to_smem(smem + 128, p.pset, p.pset_bytes, reinterpret_cast<uint64_t*>(smem));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* base = reinterpret_cast<int32_t*>(smem + 128) + (size_t)warp * 7 * p.cap;
+  int32_t* base = reinterpret_cast<int32_t*>(smem + 128 + p.pset_smem) + (size_t)warp * 7 * p.cap;
   Slots sl;
   sl.req = base;
   sl.prompt = base + p.cap;
@@ -1593,7 +1597,7 @@ __global__ void __launch_bounds__(kSimThreads, TWB_SIM_TPUT_MIN_BLOCKS) k_sim_se
     sx.reg = q.reg + rb;
     sx.g = nullptr;
     sx.sum = q.summ + (int64_t)c * q.wmax + w;
-    run_config<true, 1>(p, ps, sl, c, &sx);
+    run_config<!kLat, 1>(p, ps, sl, c, &sx);
     __syncwarp();
     if (lane == 0) sx.sum->log_len = sx.log_len;
     __syncwarp();
@@ -1890,18 +1894,26 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
   }
 }
 
-int sim_seg_prepare(int threads, size_t smem, int* per_sm) {
-  cudaFuncSetAttribute(k_sim_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+int sim_seg_prepare(int threads, size_t smem, int* per_sm, bool lat) {
+  if (lat) {
+    cudaFuncSetAttribute(k_sim_seg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg<true>, threads, smem);
+  }
+  cudaFuncSetAttribute(k_sim_seg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_sim_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg, threads, smem);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg<false>, threads, smem);
 }
 void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
-                    int join_grid) {
+                    int join_grid, bool lat, size_t join_smem, uint32_t join_pset_bytes) {
   k_seg_plan<<<(p.n_cfg + 3) / 4, 128, 0, s>>>(p, q);
-  k_sim_seg<<<grid, threads, smem, s>>>(p, q);
+  if (lat) k_sim_seg<true><<<grid, threads, smem, s>>>(p, q);
+  else k_sim_seg<false><<<grid, threads, smem, s>>>(p, q);
   const int64_t items = (int64_t)p.n_cfg * q.wmax;
   k_seg_tk<<<(int)std::min<int64_t>((items + 3) / 4, 148 * 16), 128, 0, s>>>(p, q);
-  k_sim_join<<<join_grid, threads, smem, s>>>(p, q);
+  SimParams pj = p;  // the join reads the whole blob from global memory
+  pj.pset_smem = 0;
+  pj.pset_bytes = join_pset_bytes;
+  k_sim_join<<<join_grid, threads, join_smem, s>>>(pj, q);
 }
 }  // namespace twb
 #elif defined(TWB_SIM_TPUT_TU)
@@ -1941,9 +1953,9 @@ int sim_big_prepare(int threads, int* per_sm);  // sim_big.cu
 void sim_big_launch(int grid, int threads, cudaStream_t s, const SimParams& p);
 int sim_check_prepare(int threads, size_t smem, int* per_sm);  // sim_check.cu
 void sim_check_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p);
-int sim_seg_prepare(int threads, size_t smem, int* per_sm);  // sim_seg.cu
+int sim_seg_prepare(int threads, size_t smem, int* per_sm, bool lat);  // sim_seg.cu
 void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
-                    int join_grid);
+                    int join_grid, bool lat, size_t join_smem, uint32_t join_pset_bytes);
 static thread_local int32_t* g_checks = nullptr;
 
 // ---- busy-period segments (latency regime): scratch layout ----------------------------
@@ -2000,6 +2012,7 @@ static int64_t sim_scratch_bytes(int32_t n_cfg, int cap, int sms, int per_sm, in
 }
 
 static thread_local int32_t g_last[4] = {0, 0, 0, 0};
+static thread_local int32_t g_last_path = 0;  // tw_sim_last_path
 static thread_local int64_t* g_prof = nullptr;
 static thread_local int32_t* g_seg_stats = nullptr;
 
@@ -2079,6 +2092,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
     g_last[1] = kSimThreads;
     g_last[2] = 128;
     g_last[3] = cap;
+    g_last_path = 3;
     return check_launch("tw_sim_many");
   }
   // slot state is 7 int32 arrays of cap per warp: large capacities get fewer warps per CTA
@@ -2118,14 +2132,33 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       q.cap_div = cd && atoi(cd) > 1 ? atoi(cd) : 1;
       q.stats = g_seg_stats;
       const int threads = kSimThreads;
-      const size_t smem = 128 + 4 * per_warp;
-      sim_seg_prepare(threads, smem, &per_sm);
+      // A/B only: TWB_SIM_SEG_LAT=1 stages the blob in shared memory (the latency variant's
+      // geometry), TWB_SIM_SEG_STAGE=<bytes> stages only that prefix (e.g. the core)
+      const char* lat_env = getenv("TWB_SIM_SEG_LAT");
+      const int lat = lat_env ? atoi(lat_env) : 0;
+      const size_t join_smem = 128 + 4 * per_warp;
+      size_t smem = join_smem;
+      sim_seg_prepare(threads, join_smem, &per_sm, false);
+      uint32_t seg_pset_bytes = (uint32_t)pset_bytes, seg_pset_smem = 0;
+      if (lat >= 1) {
+        const char* st_env = getenv("TWB_SIM_SEG_STAGE");
+        seg_pset_bytes = st_env ? (uint32_t)atoll(st_env) : (uint32_t)pset_bytes;
+        if (seg_pset_bytes < 64 || seg_pset_bytes > (uint32_t)pset_bytes) seg_pset_bytes = (uint32_t)pset_bytes;
+        seg_pset_smem = (seg_pset_bytes + 127) & ~127u;
+        smem = 128 + seg_pset_smem + 4 * per_warp;
+        if (smem <= (size_t)max_optin) sim_seg_prepare(threads, smem, &per_sm, true);
+        else {
+          smem = join_smem;
+          seg_pset_smem = 0;
+          seg_pset_bytes = (uint32_t)pset_bytes;
+        }
+      }
       if (per_sm < 1) per_sm = 1;
       cudaMemsetAsync(scratch, 0, 64, s);
       cudaMemsetAsync(q.regpos, 0xff, 4 * r_max, s);
       p.pset = pset;
-      p.pset_bytes = (uint32_t)pset_bytes;
-      p.pset_smem = 0;
+      p.pset_bytes = seg_pset_bytes;
+      p.pset_smem = seg_pset_smem;
       p.cfgs = cfgs;
       p.n_cfg = n_cfg;
       p.order = order;
@@ -2143,13 +2176,15 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       p.cap = cap;
       p.prof = nullptr;
       const int grid = sms * per_sm;
-      const int join_grid = (int)std::min<int64_t>(((int64_t)n_cfg + kSimWarps - 1) / kSimWarps, (int64_t)grid);
-      sim_seg_launch(grid, threads, smem, s, p, q, join_grid);
+      const int join_grid = (int)std::min<int64_t>(((int64_t)n_cfg + kSimWarps - 1) / kSimWarps, (int64_t)sms * 4);
+      sim_seg_launch(grid, threads, smem, s, p, q, join_grid, lat >= 1 && seg_pset_smem > 0, join_smem,
+                     (uint32_t)pset_bytes);
       for (int k = 0; k < 4; k++) count_launch();  // plan, segments, Timekeeper replays, join
       g_last[0] = grid;
       g_last[1] = threads;
       g_last[2] = (int32_t)smem;
       g_last[3] = cap;
+      g_last_path = 2;
       return check_launch("tw_sim_many");
     }
   }
@@ -2208,6 +2243,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   g_last[1] = threads;
   g_last[2] = (int32_t)smem;
   g_last[3] = cap;
+  g_last_path = tput ? 1 : 0;
   return check_launch("tw_sim_many");
 }
 
@@ -2243,6 +2279,8 @@ extern "C" int tw_sim_set_profile(int64_t* per_config_16xi64) {
   g_prof = per_config_16xi64;
   return TW_OK;
 }
+
+extern "C" int tw_sim_last_path(void) { return g_last_path; }
 
 extern "C" int tw_sim_last_launch(int32_t* grid, int32_t* block, int32_t* smem_bytes, int32_t* slot_capacity) {
   if (grid) *grid = g_last[0];

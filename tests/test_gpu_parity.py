@@ -830,18 +830,27 @@ def test_sim_blob_larger_than_shared_memory_equals_oracle():
         cfgs.append(SweepConfig(engine=eng, pred_id=int(rng.integers(0, 48)), workload_id=k, timekeeper=bool(k % 2)))
     wl = pack_arrays(arrays)
     ca = config_array(cfgs)
-    dev = DeviceSweep(pset, wl, ca, per_request=True)
-    dev.run()
-    out = dev.fetch()
-    assert _lib.last_sim_launch()["variant"] == "throughput"
-    for k in range(len(cfgs)):
-        ts, pr, op = wl.workload(k)
-        res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
-        assert res["status"] == 0
-        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
-            assert out.results[k][f] == res[f], (k, f)
-        lo, hi = out.req_base[k], out.req_base[k + 1]
-        assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
+    import os
+
+    # both loops that read the blob from global memory: the serial throughput variant and
+    # the busy-period segments (the default for a handful of configs)
+    for seg, variant in (("0", "throughput"), ("1", "segments")):
+        os.environ["TWB_SIM_SEG"] = seg
+        try:
+            dev = DeviceSweep(pset, wl, ca, per_request=True)
+            dev.run()
+            out = dev.fetch()
+        finally:
+            os.environ.pop("TWB_SIM_SEG", None)
+        assert _lib.last_sim_launch()["variant"] == variant
+        for k in range(len(cfgs)):
+            ts, pr, op = wl.workload(k)
+            res, first, finish, _ = orc.simulate_one(pset.blob, ca[k], ts, pr, op, want_events=False)
+            assert res["status"] == 0
+            for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+                assert out.results[k][f] == res[f], (k, f)
+            lo, hi = out.req_base[k], out.req_base[k + 1]
+            assert np.array_equal(out.first_ns[lo:hi], first) and np.array_equal(out.finish_ns[lo:hi], finish)
 
 
 def test_sweep_1024_equals_oracle_on_every_config():
