@@ -669,7 +669,8 @@ struct SegParams {
   int64_t xtra;          // extra requests of room per segment
   int32_t cap_div;       // test hook (TWB_SIM_SEG_CAPDIV): log / overrun room divided by this
   int32_t* stats;        // optional, 8 int32 per config (tw_sim_set_seg_stats)
-  int32_t* counter;      // [0..1] segment work counter (64-bit), [2] join work counter
+  int32_t* counter;      // [0..1] segment work counter (64-bit), [2] join work counter,
+                         // [4..5] Timekeeper replay work counter (64-bit)
 };
 
 __device__ __forceinline__ TkState tk_state(const TkGrid& g) {
@@ -1607,11 +1608,17 @@ __global__ void __launch_bounds__(kSimThreads, kLat ? 3 : TWB_SIM_TPUT_MIN_BLOCK
 // The segments' Timekeeper replays, one warp per (config, segment), in a kernel of their
 // own: inside k_sim_seg the replay loop next to the event loop pushed the kernel's code
 // past the instruction caches (ncu: stall_no_inst 46%, 7.3 ms vs 3.8 + this kernel).
-__global__ void __launch_bounds__(128) k_seg_tk(SimParams p, SegParams q) {
+#ifndef TWB_SEG_TK_BLOCKS
+#define TWB_SEG_TK_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(128, TWB_SEG_TK_BLOCKS) k_seg_tk(SimParams p, SegParams q) {
   const int lane = threadIdx.x & 31;
   const int64_t n_items = (int64_t)p.n_cfg * q.wmax;
-  for (int64_t idx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); idx < n_items;
-       idx += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+  for (;;) {  // persistent warps pull segments (their logs differ in length)
+    int64_t idx = 0;
+    if (lane == 0) idx = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(q.counter + 4), 1ULL);
+    idx = __shfl_sync(kFull, idx, 0);
+    if (idx >= n_items) break;
     const int32_t rank = (int32_t)(idx / q.wmax), w = (int32_t)(idx - (int64_t)rank * q.wmax);
     const int c = p.order ? p.order[rank] : rank;
     const int32_t W = q.nseg[c];
@@ -1909,7 +1916,11 @@ void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const Si
   if (lat) k_sim_seg<true><<<grid, threads, smem, s>>>(p, q);
   else k_sim_seg<false><<<grid, threads, smem, s>>>(p, q);
   const int64_t items = (int64_t)p.n_cfg * q.wmax;
-  k_seg_tk<<<(int)std::min<int64_t>((items + 3) / 4, 148 * 16), 128, 0, s>>>(p, q);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seg_tk, 128, 0);
+  k_seg_tk<<<(int)std::min<int64_t>((items + 3) / 4, (int64_t)sms * std::max(per_sm, 1)), 128, 0, s>>>(p, q);
   SimParams pj = p;  // the join reads the whole blob from global memory
   pj.pset_smem = 0;
   pj.pset_bytes = join_pset_bytes;
