@@ -9,6 +9,6 @@ run() {  # tool, extra flags, driver parts
 }
 run memcheck "--leak-check full"
 # the resident service kernel polls mapped host memory for its whole life: memcheck only
-run racecheck "--racecheck-report all" sim simtput bulk tk metrics wl single
-run synccheck "" sim simtput bulk tk metrics wl single
-run initcheck "" sim simtput bulk tk metrics wl single
+run racecheck "--racecheck-report all" sim seg simtput bulk tk metrics wl single
+run synccheck "" sim seg simtput bulk tk metrics wl single
+run initcheck "" sim seg simtput bulk tk metrics wl single

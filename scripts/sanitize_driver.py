@@ -2,6 +2,8 @@
 numpy, for compute-sanitizer (scripts/sanitize.sh; tests/test_sanitizer.py):
 
   k_sim<false>  latency variant, blob staged by TMA (8 configs, Timekeeper grid on, audit dump)
+  k_seg_plan, k_sim_seg, k_seg_tk, k_sim_join  busy-period segments (clean joins, overruns,
+                forced overflows and serial re-runs in the join)
   k_sim<true>   throughput variant (forced by a 367 KB predictor blob that cannot be staged)
   k_predict_features<true/false>, k_predict_batches<true/false> (mbarrier producer/consumer pipeline)
   k_tk_replay, k_tk_resolve_rows, k_metrics, k_generate_poisson, k_predict_single,
@@ -20,7 +22,7 @@ from paper_2601_00397_b200.sweep import DeviceSweep  # noqa: E402
 from paper_2601_00397_b200.timekeeper import OpStream, replay_many, resolve_round  # noqa: E402
 from paper_2601_00397_b200.workload import WorkloadSpec, generate_device, poisson_arrays  # noqa: E402
 
-which = set(sys.argv[1:]) or {"sim", "simtput", "bulk", "tk", "metrics", "wl", "single", "service"}
+which = set(sys.argv[1:]) or {"sim", "seg", "simtput", "bulk", "tk", "metrics", "wl", "single", "service"}
 rng = np.random.default_rng(0)
 
 
@@ -53,6 +55,39 @@ if "sim" in which or "metrics" in which:
                                  got.finish_ns[rb: rb + hi - lo], int(sub.cfgs[k]["epoch_ns"]))
             assert m[k].tobytes() == want_m.tobytes()
         print("k_metrics ok")
+
+if "seg" in which:
+    import os
+
+    def check_seg(sub, env):
+        os.environ.update(env)
+        try:
+            d = DeviceSweep(sub.pset, sub.workloads, sub.cfgs, per_request=True)
+            d.run()
+            torch.cuda.synchronize()
+            got = d.fetch()
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+        assert _lib.last_sim_launch()["variant"] == "segments"
+        want, _, first, finish = orc.sim_many(sub.pset.blob, sub.cfgs, sub.workloads.wl_off, sub.workloads.offset_ns,
+                                              sub.workloads.prompt, sub.workloads.output, per_request=True)
+        for f in ("status", "final_now_ns", "steps", "events", "digest", "tk_seq", "tk_offset_ns", "tk_wall_ns"):
+            assert np.array_equal(got.results[f], want[f]), f
+        assert np.array_equal(got.first_ns, first[: len(got.first_ns)])
+        assert np.array_equal(got.finish_ns, finish[: len(got.finish_ns)])
+        # hand the (large) segment scratch back at once, so later allocations are not carved
+        # out of its cached block (memcheck --leak-check would report the block as leaked)
+        del d, got
+        torch.cuda.empty_cache()
+
+    sw = presets.sweep_1024(n_requests=160)
+    sub = sw.subset(np.arange(0, len(sw), 128))
+    check_seg(sub, {"TWB_SIM_SEG_W": "8"})
+    check_seg(sub, {"TWB_SIM_SEG_W": "8", "TWB_SIM_SEG_CAPDIV": "1000"})  # every segment out of room
+    heavy = presets.single("heavy", "70b", 4, 2, 400, 4)  # long busy periods: overruns
+    check_seg(heavy, {"TWB_SIM_SEG_W": "25"})
+    print("k_seg_plan / k_sim_seg / k_seg_tk / k_sim_join ok")
 
 big = None
 if "simtput" in which or "bulk" in which:
