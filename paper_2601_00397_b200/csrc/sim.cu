@@ -1436,8 +1436,11 @@ __global__ void __launch_bounds__(kSimThreads, kTput ? TWB_SIM_TPUT_MIN_BLOCKS :
 // boundary moved (within +-15 arrivals) to the largest inter-arrival gap, where the
 // engine is most likely to be empty. One warp per config.
 __global__ void __launch_bounds__(128) k_seg_plan(SimParams p, SegParams q) {
+  // block (x = config, y = share of its boundaries); the warps of the grid's y dimension
+  // split the boundaries (a single config has up to 255 of them)
   const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int c = blockIdx.x;
+  const int wy = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5), ny = gridDim.y * (blockDim.x >> 5);
   if (c >= p.n_cfg) return;
   const tw_sim_cfg cfg = p.cfgs[c];
   const int64_t wl0 = p.wl_off[cfg.workload_id];
@@ -1446,14 +1449,14 @@ __global__ void __launch_bounds__(128) k_seg_plan(SimParams p, SegParams q) {
   int32_t W = n / q.min_req;
   W = W < 1 ? 1 : (W > q.wmax ? q.wmax : W);
   if (p.req_base[p.n_cfg] > q.r_max) W = 0;  // scratch too small for the per-request records
-  if (lane == 0) {
+  if (lane == 0 && wy == 0) {
     q.nseg[c] = W;
     q.seg_a0[(int64_t)c * q.wmax] = 0;
   }
   if (W <= 1) return;
   const int32_t len = n / W;
   const int32_t h = min(15, len / 2 - 1);
-  for (int k = 1; k < W; k++) {
+  for (int k = 1 + wy; k < W; k += ny) {
     const int32_t center = (int32_t)((int64_t)k * n / W);
     const int32_t j = center - h + lane;
     int64_t gap = -1;
@@ -1669,9 +1672,7 @@ __device__ __forceinline__ bool tk_compose(TkGrid& g, const TkState& E, const Tk
   g.last_bcast = T.last_bcast == INT64_MIN ? INT64_MIN : T.last_bcast + delta;
   g.offset = T.offset - delta;
   g.V = g.wall + g.offset;
-  g.disp = T.disp;
-  g.win.load(ts, n, epoch, T.disp);
-  g.disp_ts = T.disp < n ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
+  g.disp = T.disp;  // the dispatcher's window is reloaded only before a serial piece
   return true;
 }
 
@@ -1808,6 +1809,13 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
           if (s.j_stop > a1w) copy_side(w, a1w, s.j_stop);
           if (s.j_stop >= n) break;
           js = s.j_stop;
+          if (w + 1 < W && a0s[w + 1] == js) {  // the usual case: the next segment's start
+            w++;
+            e = SegRegen{0, 0, 0, 0, 0, TkState{0, 0, 0, 0, js, 0}};  // k_seg_tk's guess at a0
+            j_in = js;
+            exact = false;
+            continue;
+          }
           if (regpos[js] >= 0) {  // the owner's run was empty at js too: continue with it
             w = owner(js);
             e = reg[js];
@@ -1820,6 +1828,8 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
         }
       }
       // a serial piece from arrival js (the engine empty there), the true Timekeeper inline
+      g.win.load(ts, n, epoch, g.disp);
+      g.disp_ts = g.disp < n ? __shfl_sync(kFull, g.win.v, 0) : INT64_MAX;
       SegCtx sx;
       sx.a0 = js;
       sx.a1 = n;
@@ -1912,7 +1922,7 @@ int sim_seg_prepare(int threads, size_t smem, int* per_sm, bool lat) {
 }
 void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
                     int join_grid, bool lat, size_t join_smem, uint32_t join_pset_bytes) {
-  k_seg_plan<<<(p.n_cfg + 3) / 4, 128, 0, s>>>(p, q);
+  k_seg_plan<<<dim3((unsigned)p.n_cfg, (unsigned)std::min(64, (q.wmax + 3) / 4)), 128, 0, s>>>(p, q);
   if (lat) k_sim_seg<true><<<grid, threads, smem, s>>>(p, q);
   else k_sim_seg<false><<<grid, threads, smem, s>>>(p, q);
   const int64_t items = (int64_t)p.n_cfg * q.wmax;
