@@ -1983,7 +1983,16 @@ static thread_local int32_t* g_checks = nullptr;
 // [64 B counters | nseg[n_cfg] | seg_a0[n_cfg*W] | summ[n_cfg*W] |
 //  regpos[R] | reg[R] | log[kSegLogPerReq*(R+X)] | side[8*(R+X)]], X = xtra * segments,
 //  R (request capacity) = what the rest of scratch holds
-constexpr int kSegMinReq = 16;
+static int seg_min_req() {  // requests per segment at least (TWB_SIM_SEG_MINREQ: A/B only)
+  const char* e = getenv("TWB_SIM_SEG_MINREQ");
+  const int v = e ? atoi(e) : 16;
+  return v < 2 ? 2 : v;
+}
+static int seg_wcap() {  // segments per config at most (TWB_SIM_SEG_WCAP: A/B only)
+  const char* e = getenv("TWB_SIM_SEG_WCAP");
+  const int v = e ? atoi(e) : 256;
+  return v < 1 ? 1 : (v > 4096 ? 4096 : v);
+}
 constexpr int64_t kSegPerReqBytes =
     (int64_t)sizeof(int32_t) + (int64_t)sizeof(SegRegen) + 8 * (int64_t)sizeof(int64_t) +
     kSegLogPerReq * (int64_t)sizeof(TkLog);
@@ -2003,7 +2012,7 @@ static int seg_wmax(int32_t n_cfg, int sms) {
   const char* e = getenv("TWB_SIM_SEG_W");
   int64_t w = e ? atoll(e) : 0;
   if (w <= 0) w = ((int64_t)sms * 16 * 7 + n_cfg - 1) / n_cfg;  // ~7 segments per resident warp
-  if (w > 256) w = 256;
+  if (w > seg_wcap()) w = seg_wcap();
   if (w < 1) w = 1;
   return (int)w;
 }
@@ -2130,7 +2139,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       char* b = static_cast<char*>(scratch);
       SegParams q;
       q.wmax = wmax;
-      q.min_req = kSegMinReq;
+      q.min_req = seg_min_req();
       q.counter = reinterpret_cast<int32_t*>(b);
       int64_t o = 64;
       q.nseg = reinterpret_cast<int32_t*>(b + o);
