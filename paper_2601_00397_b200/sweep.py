@@ -302,7 +302,12 @@ class DeviceSweep:
         # latency regime: records of the busy-period segments (tw_sim_seg_scratch_bytes; the
         # library picks them when req_base is passed, i.e. with per-request stamps)
         if per_request and self.n_cfg and not audit:
-            scratch = max(scratch, int(lib.tw_sim_seg_scratch_bytes(self.n_cfg, total_req)))
+            seg = int(lib.tw_sim_seg_scratch_bytes(self.n_cfg, total_req))
+            # bounded: past a quarter of free device memory the serial loop runs instead (the
+            # library falls back to it when the scratch is too small for the segments)
+            free, _ = torch.cuda.mem_get_info(self.device)
+            if seg <= free // 4:
+                scratch = max(scratch, seg)
         self.d_scratch = torch.zeros(max(64, scratch), dtype=torch.uint8, device=dev)
         self.per_request = per_request
         if per_request:
