@@ -668,6 +668,7 @@ struct SegParams {
   int64_t r_max;
   int64_t xtra;          // extra requests of room per segment
   int32_t cap_div;       // test hook (TWB_SIM_SEG_CAPDIV): log / overrun room divided by this
+  int32_t epoch;         // launch number: a segment's summary is complete when its pad == epoch
   int32_t* stats;        // optional, 8 int32 per config (tw_sim_set_seg_stats)
   int32_t* counter;      // [0..1] segment work counter (64-bit), [2] join work counter,
                          // [4..5] Timekeeper replay work counter (64-bit)
@@ -1603,9 +1604,39 @@ __global__ void __launch_bounds__(kSimThreads, kLat ? 3 : TWB_SIM_TPUT_MIN_BLOCK
     sx.sum = q.summ + (int64_t)c * q.wmax + w;
     run_config<!kLat, 1>(p, ps, sl, c, &sx);
     __syncwarp();
-    if (lane == 0) sx.sum->log_len = sx.log_len;
+    if (lane == 0) {
+      sx.sum->log_len = sx.log_len;
+      __threadfence();
+      *reinterpret_cast<volatile int32_t*>(&sx.sum->pad) = q.epoch;  // the segment is done
+    }
     __syncwarp();
   }
+#ifdef TWB_SEG_TAIL_REPLAY
+  // A/B: with the segments handed out, the warps replay the Timekeeper logs themselves
+  // (waiting for segments still running), filling the kernel's tail
+  for (;;) {
+    int64_t idx = 0;
+    if (lane == 0) idx = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(q.counter + 4), 1ULL);
+    idx = __shfl_sync(kFull, idx, 0);
+    if (idx >= n_items) break;
+    const int32_t rank = (int32_t)(idx / q.wmax), w = (int32_t)(idx - (int64_t)rank * q.wmax);
+    const int c = p.order ? p.order[rank] : rank;
+    const int32_t W = q.nseg[c];
+    if (w >= W) continue;
+    const tw_sim_cfg& cfg = p.cfgs[c];
+    if (!(cfg.flags & TW_SIM_TIMEKEEPER)) continue;
+    SegSummary* sum = q.summ + (int64_t)c * q.wmax + w;
+    while (*reinterpret_cast<volatile int32_t*>(&sum->pad) != q.epoch) __nanosleep(256);
+    __threadfence();
+    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY) continue;
+    const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - p.wl_off[cfg.workload_id]);
+    const int64_t rb = p.req_base[c];
+    const int32_t a0 = q.seg_a0[(int64_t)c * q.wmax + w];
+    const int32_t a1 = (w + 1 < W) ? q.seg_a0[(int64_t)c * q.wmax + w + 1] : n;
+    seg_tk_replay(p, c, a0, a1, n, q.log + (int64_t)kSegLogPerReq * (rb + a0 + q.xtra * ((int64_t)c * q.wmax + w)),
+                  sum->log_len, q.regpos + rb, q.reg + rb, sum);
+  }
+#endif
 }
 
 // The segments' Timekeeper replays, one warp per (config, segment), in a kernel of their
@@ -2161,6 +2192,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       const char* cd = getenv("TWB_SIM_SEG_CAPDIV");  // tests only: force the overflow path
       q.cap_div = cd && atoi(cd) > 1 ? atoi(cd) : 1;
       q.stats = g_seg_stats;
+      static thread_local int32_t seg_epoch = 0;
+      q.epoch = ++seg_epoch;
       const int threads = kSimThreads;
       // A/B only: TWB_SIM_SEG_LAT=1 stages the blob in shared memory (the latency variant's
       // geometry), TWB_SIM_SEG_STAGE=<bytes> stages only that prefix (e.g. the core)
