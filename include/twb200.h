@@ -424,17 +424,20 @@ typedef struct tw_run_metrics {
  * compensated TPOT sum; NULL = the engine's (stable-sorted) order, which is the
  * caller's order for sorted arrival lists such as generate_arrivals produces.
  * max_requests: an upper bound on any workload's size. Up to ~28,000 requests the
- * per-request keys (8 B each) live in shared memory and scratch may be NULL; above
- * that they live in the caller's global scratch (scratch_bytes >=
- * tw_metrics_scratch_bytes(n_cfg, max_requests); less, down to one slice of
- * 8*max_requests bytes, runs fewer CTAs; none gives TW_ENOSMEM). */
+ * per-request keys (8 B each) live in shared memory; above that they live in the
+ * caller's global scratch (less than tw_metrics_scratch_bytes, down to one slice of
+ * 8*max_requests bytes, runs fewer CTAs; none gives TW_ENOSMEM). With the full
+ * tw_metrics_scratch_bytes the scratch also holds each config's TPOT values (8 B per
+ * request) and a second kernel sums them one lane per config (CPython's compensated
+ * sum, same order); with less, one thread of the config's CTA sums them. */
 int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int64_t* wl_off,
                     const int64_t* req_offset_ns, const int32_t* req_output,
                     const int64_t* req_base, const int64_t* req_first_ns,
                     const int64_t* req_finish_ns, const tw_sim_result* sim,
                     const int32_t* sum_order, int32_t max_requests, void* scratch,
                     int64_t scratch_bytes, tw_run_metrics* out, void* stream);
-/* bytes of global scratch tw_metrics_many wants for these sizes (0: shared memory suffices) */
+/* bytes of global scratch tw_metrics_many wants for these sizes (the TPOT rows, plus the
+ * keys above ~28,000 requests) */
 int64_t tw_metrics_scratch_bytes(int32_t n_cfg, int32_t max_requests);
 
 /* ---- native BarrierCore for the live Timekeeper --------- */

@@ -16,6 +16,7 @@
 //     MSD radix selection over 8-bit digits, all three ranks per pass, starting
 //     below the bits every key shares. A bitonic sort of the keys was
 //     shared-memory-bandwidth-bound: 0.185 -> 0.123 ms for 1,024 x 1,000.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -80,7 +81,36 @@ struct MetParams {
   int32_t cap;  // keys capacity
   uint64_t* gkeys;  // global-memory keys (cap per CTA) for workloads shared memory cannot hold
   tw_run_metrics* out;
+  // TPOT values in caller order, cap per config (k_metrics_tpot sums them one lane per
+  // config); nullptr: one thread of the config's CTA sums them (scratch too small)
+  double* tpot_vals;
 };
+
+// CPython's sum of one config's TPOT values per lane: 32 configs per warp, each lane running
+// the same Neumaier recurrence as neumaier_sum over its config's row (caller order), then
+// mean = sum / count. Inside k_metrics the sum was one thread's serial loop while the CTA
+// waited: ~22% of the kernel's instructions (ncu, config 5).
+__global__ void __launch_bounds__(128) k_metrics_tpot(MetParams p) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= p.n_cfg) return;
+  tw_run_metrics* o = p.out + c;
+  if (o->status != TW_METRICS_OK || o->tpot.count <= 0) return;
+  const tw_sim_cfg& cfg = p.cfgs[c];
+  const int n = (int)(p.wl_off[cfg.workload_id + 1] - p.wl_off[cfg.workload_id]);
+  const double* v = p.tpot_vals + (int64_t)c * p.cap;
+  double f = 0.0, cc = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < n; i++) {
+    double x = __ldg(v + i);
+    x = isnan(x) ? 0.0 : x;
+    const double t = __dadd_rn(f, x);
+    const double e = fabs(f) >= fabs(x) ? __dadd_rn(__dsub_rn(f, t), x) : __dadd_rn(__dsub_rn(x, t), f);
+    cc = __dadd_rn(cc, e);
+    f = t;
+  }
+  if (cc != 0.0 && isfinite(cc)) f = __dadd_rn(f, cc);
+  o->tpot.mean = __ddiv_rn(f, (double)o->tpot.count);
+}
 
 struct BlockRed {
   int64_t miss, tokens, maxfin, s_ttft, s_e2e, n_tpot;
@@ -338,14 +368,16 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
       stats_from_keys(keys, n, n, n > 0 ? __ddiv_rn(sum, (double)n) : 0.0, m == 0 ? res.ttft : res.e2e);
     }
     // ---- TPOT over requests with more than one output token (metrics.py:54-60, 100-101)
+    double* tv = p.tpot_vals ? p.tpot_vals + (int64_t)c * p.cap : nullptr;
     for (int i = tid; i < n; i += kMetThreads) {
       const int32_t op = p.output[wl0 + i];
       double t = __longlong_as_double(0x7ff8000000000000LL);
       if (op > 1) t = __ddiv_rn((double)(p.finish[rb + i] - p.first[rb + i]), (double)(op - 1));
       vals[pos ? pos[i] : i] = t;
+      if (tv) tv[pos ? pos[i] : i] = t;  // summed by k_metrics_tpot
     }
     __syncthreads();
-    if (tid == 0) sh_mean = n_tpot > 0 ? __ddiv_rn(neumaier_sum(vals, n), (double)n_tpot) : 0.0;
+    if (tid == 0) sh_mean = (n_tpot > 0 && !tv) ? __ddiv_rn(neumaier_sum(vals, n), (double)n_tpot) : 0.0;
     __syncthreads();
     for (int i = tid; i < n; i += kMetThreads) {
       const double t = vals[i];
@@ -389,6 +421,19 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
   const bool global = max_requests > limit;
   int64_t grid;
   size_t smem = 0;
+  // the TPOT rows (n_cfg x cap doubles) take the end of the scratch when it holds them
+  const int64_t tpot_bytes = (int64_t)n_cfg * cap * (int64_t)sizeof(double);
+  int64_t key_budget = scratch ? scratch_bytes : 0;
+  bool tpot_ok = false;
+  if (global) {
+    const int64_t want = ((int64_t)std::min<int64_t>(4LL * sms, n_cfg) * cap * (int64_t)sizeof(uint64_t) + 255) & ~255LL;
+    if (key_budget >= want + tpot_bytes) {
+      key_budget -= tpot_bytes;
+      tpot_ok = true;
+    }
+  } else {
+    tpot_ok = key_budget >= tpot_bytes;
+  }
   if (!global) {
     smem = (size_t)cap * sizeof(uint64_t);
     cudaFuncSetAttribute(k_metrics<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -397,7 +442,7 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
     grid = (int64_t)sms * per_sm;
   } else {
     // keys in global scratch: one cap-sized slice per CTA, as many CTAs as the scratch holds
-    const int64_t slices = scratch ? scratch_bytes / ((int64_t)cap * (int64_t)sizeof(uint64_t)) : 0;
+    const int64_t slices = key_budget / ((int64_t)cap * (int64_t)sizeof(uint64_t));
     if (slices < 1) {
       set_error("tw_metrics_many: max_requests %d above the %d requests shared memory holds and no scratch "
                 "(%lld bytes; tw_metrics_scratch_bytes gives the size)", max_requests, limit,
@@ -422,9 +467,22 @@ extern "C" int tw_metrics_many(const tw_sim_cfg* cfgs, int32_t n_cfg, const int6
   p.cap = cap;
   p.gkeys = static_cast<uint64_t*>(scratch);
   p.out = out;
+  // scratch layout: [global keys (workloads above what shared memory holds)] [TPOT values]
+  const int64_t keys_bytes = global ? (int64_t)grid * cap * (int64_t)sizeof(uint64_t) : 0;
+  const int64_t keys_room = (keys_bytes + 255) & ~255LL;
+  // lane-per-config sums pay off once each resident CTA has several configs to summarise
+  // (65,536 configs: 6.84 -> 4.72 ms); with few configs the 1,000-step chains of a handful
+  // of warps are slower than the in-CTA sums (1,024 configs: 0.113 -> 0.222 ms)
+  p.tpot_vals = (tpot_ok && n_cfg >= 4096 && scratch_bytes >= keys_room + tpot_bytes)
+                    ? reinterpret_cast<double*>(static_cast<char*>(scratch) + keys_room)
+                    : nullptr;
   if (global) k_metrics<true><<<(int)grid, kMetThreads, 0, (cudaStream_t)stream>>>(p);
   else k_metrics<false><<<(int)grid, kMetThreads, smem, (cudaStream_t)stream>>>(p);
   count_launch();
+  if (p.tpot_vals) {
+    k_metrics_tpot<<<(n_cfg + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+    count_launch();
+  }
   return check_launch("tw_metrics_many");
 }
 
@@ -433,7 +491,10 @@ extern "C" int64_t tw_metrics_scratch_bytes(int32_t n_cfg, int32_t max_requests)
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (max_requests <= (max_optin - kMetStaticSmem) / (int)sizeof(uint64_t) || n_cfg <= 0) return 0;
+  if (n_cfg <= 0) return 0;
+  const int cap = max_requests > 0 ? max_requests : 1;
+  const int64_t tpot = (int64_t)n_cfg * cap * (int64_t)sizeof(double);  // k_metrics_tpot's rows
+  if (max_requests <= (max_optin - kMetStaticSmem) / (int)sizeof(uint64_t)) return tpot;
   const int64_t ctas = n_cfg < 4 * sms ? n_cfg : 4 * sms;
-  return ctas * (int64_t)max_requests * (int64_t)sizeof(uint64_t);
+  return ((ctas * (int64_t)cap * (int64_t)sizeof(uint64_t) + 255) & ~255LL) + tpot;
 }
