@@ -1037,6 +1037,33 @@ def test_device_metrics_equal_oracle_on_sweep_1024():
         assert got[c].tobytes() == want.tobytes(), c
 
 
+def test_device_metrics_lane_sums_on_a_large_sweep_equal_oracle():
+    """At >= 4,096 configs the TPOT means are summed one lane per config (k_metrics_tpot):
+    every record equals the in-CTA path's and, on a sample, the C oracle's."""
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.sweep import DeviceSweep
+
+    sw = presets.sweep_65536(seeds=(3, 4), models=("8b", "70b")).subset(range(0, 4096))
+    assert len(sw) == 4096
+    dev = DeviceSweep(sw.pset, sw.workloads, sw.cfgs, per_request=True)
+    dev.run()
+    dev.run_metrics()
+    lanes = dev.fetch_metrics().copy()
+    dev.d_met_scratch = None  # no scratch: the CTA sums its own config
+    dev.run_metrics()
+    cta = dev.fetch_metrics()
+    assert lanes.tobytes() == cta.tobytes()
+    out = dev.fetch()
+    for c in range(0, len(sw), 97):
+        w = int(sw.cfgs[c]["workload_id"])
+        lo, hi = int(sw.workloads.wl_off[w]), int(sw.workloads.wl_off[w + 1])
+        rb = int(out.req_base[c])
+        want = orc.metrics(sw.workloads.offset_ns[lo:hi], sw.workloads.output[lo:hi],
+                           out.first_ns[rb : rb + hi - lo], out.finish_ns[rb : rb + hi - lo], int(sw.cfgs[c]["epoch_ns"]))
+        assert lanes[c].tobytes() == want.tobytes(), c
+
+
 def test_drop_in_simulate_matches_reference_timeline():
     """pkg/tests/test_oracle.py:35-43 through sweep.simulate (full event dicts)."""
     from paper_2601_00397_b200.predictor import ConstantPredictor
