@@ -146,10 +146,14 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 // ascending order, without sorting: MSD radix selection, 8-bit digits below the bits
 // every valid key shares, all three ranks per pass. Keys equal to ~0 (no value) are
 // never selected and sit above every valid key, so they are skipped.
+// After the first digit, the keys still matching one of the three prefixes (usually a few
+// dozen of ~1,000) are compacted into a small buffer and the later passes scan only those.
+constexpr int kMetCand = 448;
 __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t out[3]) {
   __shared__ uint32_t hist[3][256];
   __shared__ uint64_t pre[3], red_mn[kMetWarps], red_mx[kMetWarps];
-  __shared__ int rem[3], sh_shift;
+  __shared__ uint64_t cand[kMetCand];
+  __shared__ int rem[3], sh_shift, ncand;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint64_t mn = ~0ULL, mx = 0;
   for (int i = tid; i < n; i += kMetThreads) {
@@ -184,12 +188,15 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
     }
   }
   __syncthreads();
+  const uint64_t* src = keys;
+  int nsrc = n;
+  bool compacted = false;
   for (int shift = sh_shift; shift >= 0; shift -= 8) {
     for (int i = tid; i < 3 * 256; i += kMetThreads) (&hist[0][0])[i] = 0;
     __syncthreads();
     const uint64_t p0 = pre[0], p1 = pre[1], p2 = pre[2];
-    for (int i = tid; i < n; i += kMetThreads) {
-      const uint64_t k = keys[i];
+    for (int i = tid; i < nsrc; i += kMetThreads) {
+      const uint64_t k = src[i];
       if (k == ~0ULL) continue;
       const uint32_t dg = (uint32_t)(k >> shift) & 255u;
       if (shift >= 56) {
@@ -233,7 +240,25 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
         pre[t] |= (uint64_t)d << shift;
       }
     }
+    if (tid == 0) ncand = 0;
     __syncthreads();
+    if (!compacted && shift > 0) {  // keep the keys that can still be selected
+      const uint64_t q0 = pre[0], q1 = pre[1], q2 = pre[2];
+      for (int i = tid; i < nsrc; i += kMetThreads) {
+        const uint64_t k = src[i];
+        if (k != ~0ULL && (((k ^ q0) >> shift) == 0 || ((k ^ q1) >> shift) == 0 || ((k ^ q2) >> shift) == 0)) {
+          const int j = atomicAdd(&ncand, 1);
+          if (j < kMetCand) cand[j] = k;
+        }
+      }
+      __syncthreads();
+      if (ncand <= kMetCand) {
+        src = cand;
+        nsrc = ncand;
+        compacted = true;
+      }
+      __syncthreads();
+    }
   }
   out[0] = pre[0];
   out[1] = pre[1];
