@@ -830,7 +830,8 @@ __device__ void run_config(const SimParams& p, const char* ps, Slots sl, int c, 
   int overflow = 0;
   int32_t last_regen = a0, j_stop = n, log_len = 0;
   if constexpr (kMode != 0) {
-    if (kMode == 1 && lane == 0) {  // the segment's start is its first regeneration point
+    // (a0 < n: an empty workload's slot 0 is the next config's first request)
+    if (kMode == 1 && lane == 0 && a0 < n) {  // the segment's start is its first regeneration point
       sx->reg[a0] = SegRegen{0, 0, 0, 0, 0, TkState{}};
       sx->regpos[a0] = 0;
     }
@@ -1628,8 +1629,8 @@ __global__ void __launch_bounds__(kSimThreads, kLat ? 3 : TWB_SIM_TPUT_MIN_BLOCK
     SegSummary* sum = q.summ + (int64_t)c * q.wmax + w;
     while (*reinterpret_cast<volatile int32_t*>(&sum->pad) != q.epoch) __nanosleep(256);
     __threadfence();
-    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY) continue;
     const int32_t n = (int32_t)(p.wl_off[cfg.workload_id + 1] - p.wl_off[cfg.workload_id]);
+    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY || n == 0) continue;
     const int64_t rb = p.req_base[c];
     const int32_t a0 = q.seg_a0[(int64_t)c * q.wmax + w];
     const int32_t a1 = (w + 1 < W) ? q.seg_a0[(int64_t)c * q.wmax + w + 1] : n;
@@ -1664,7 +1665,7 @@ __global__ void __launch_bounds__(128, TWB_SEG_TK_BLOCKS) k_seg_tk(SimParams p, 
     const int32_t a0 = q.seg_a0[(int64_t)c * q.wmax + w];
     const int32_t a1 = (w + 1 < W) ? q.seg_a0[(int64_t)c * q.wmax + w + 1] : n;
     SegSummary* sum = q.summ + (int64_t)c * q.wmax + w;
-    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY) continue;
+    if (sum->status == TW_SIM_BAD_CONFIG || sum->status == TW_SIM_CAPACITY || a0 >= n) continue;
     seg_tk_replay(p, c, a0, a1, n, q.log + (int64_t)kSegLogPerReq * (rb + a0 + q.xtra * ((int64_t)c * q.wmax + w)),
                   sum->log_len, q.regpos + rb,
                   q.reg + rb, sum);
@@ -1684,6 +1685,11 @@ __device__ __forceinline__ bool tk_compose(TkGrid& g, const TkState& E, const Tk
                                            int64_t d_hi, bool exact, int32_t j, const int64_t* __restrict__ ts,
                                            int32_t n, int64_t epoch) {
   int64_t delta = 0;
+  if (!exact && T.seq == E.seq) {
+    // no broadcast in the piece: it is empty (entry = exit, e.g. a segment out of room at
+    // its entry) and the true state stands; anything else cannot be shown to carry over
+    return T.wall == E.wall && T.offset == E.offset && T.last_bcast == E.last_bcast && T.disp == E.disp;
+  }
   if (!exact) {
     if (g.disp != j || E.disp != j) return false;
     const bool set_t = g.last_bcast != INT64_MIN, set_e = E.last_bcast != INT64_MIN;
@@ -1808,7 +1814,7 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
           invalid_cfg = true;
           break;
         }
-        if (exact) e = reg[0];
+        if (exact) e = SegRegen{};  // the config's start: zero counters, Timekeeper seq 0
         if (s.status == kSegOverflow) {
           // valid from the entry up to its last regeneration point, serial from there
           n_ovf++;

@@ -142,3 +142,42 @@ def test_segmented_timekeeper_off_and_mixed_workloads_equal_oracle():
         assert np.array_equal(out.results[f], res[f]), f
     k = len(out.first_ns)
     assert np.array_equal(out.first_ns, first[:k]) and np.array_equal(out.finish_ns, finish[:k])
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_segmented_random_sweeps_equal_serial(seed):
+    """Random engine configs (chunk, budget, max_running, KV capacity down to stalls, both
+    policies, TP x PP, Timekeeper on/off, cooldown 0 to 2 ms), random workloads (0-600
+    requests, qps 1-64, short and long prompts), Table / Linear / Constant predictors, and
+    random segment counts and room divisors: the segmented run equals the serial loop."""
+    from paper_2601_00397_b200 import presets
+    from paper_2601_00397_b200.predictor import ConstantPredictor, LinearPredictor, PredictorSet
+    from paper_2601_00397_b200.sweep import EngineConfig, SchedulingPolicy, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import WorkloadSpec, pack_arrays, poisson_arrays
+
+    rng = np.random.default_rng(1000 + seed)
+    docs = []
+    for w in range(6):
+        lo = int(rng.choice([1, 16, 64, 512]))
+        docs.append({"source": "poisson", "qps": float(rng.choice([1, 4, 16, 64])), "seed": int(rng.integers(1, 10**6)),
+                     "num_requests": int(rng.choice([0, 1, 37, 200, 600])),
+                     "prompt_tokens": {"kind": "uniform", "low": lo, "high": lo + int(rng.integers(1, 3000))},
+                     "output_tokens": {"kind": "uniform", "low": 1, "high": int(rng.integers(2, 400))}})
+    wl = pack_arrays([poisson_arrays(WorkloadSpec.from_doc(d)) for d in docs])
+    tables = presets.calibration_set().predictors
+    pset = PredictorSet(list(tables) + [LinearPredictor(3000.0, 2.5, 40.0), ConstantPredictor(9000)])
+    cfgs = []
+    for k in range(192):
+        chunk = int(rng.choice([32, 128, 512, 2048]))
+        eng = EngineConfig(chunk_size=chunk, max_batch_tokens=chunk * int(rng.choice([1, 2, 8])),
+                           max_running=int(rng.choice([1, 4, 32, 256])), kv_block_tokens=int(rng.choice([8, 16])),
+                           kv_capacity_blocks=int(rng.choice([300, 4000, 1 << 20])),
+                           policy=SchedulingPolicy.MIXED if rng.random() < 0.5 else SchedulingPolicy.PREFILL_PRIORITIZED,
+                           workers_per_replica=int(rng.choice([1, 2, 8])), pp_stages=int(rng.choice([1, 2, 3])))
+        cfgs.append(SweepConfig(engine=eng, pred_id=int(rng.integers(0, len(pset.predictors))),
+                                workload_id=int(rng.integers(0, len(docs))), timekeeper=bool(rng.random() < 0.8),
+                                tk_cooldown_ns=int(rng.choice([0, 1, 500_000, 2_000_000])),
+                                epoch_ns=int(rng.choice([0, 1_790_000_000_000_000_000]))))
+    ca = config_array(cfgs)
+    env = {"TWB_SIM_SEG_W": int(rng.choice([1, 2, 5, 17, 64])), "TWB_SIM_SEG_CAPDIV": int(rng.choice([1, 1, 3, 1000]))}
+    _serial_and_segmented(pset, wl, ca, **env)
