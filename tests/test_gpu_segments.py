@@ -179,5 +179,6 @@ def test_segmented_random_sweeps_equal_serial(seed):
                                 tk_cooldown_ns=int(rng.choice([0, 1, 500_000, 2_000_000])),
                                 epoch_ns=int(rng.choice([0, 1_790_000_000_000_000_000]))))
     ca = config_array(cfgs)
+    ca["chunk_size"][rng.random(len(ca)) < 0.03] = 0  # a few invalid configs (TW_SIM_BAD_CONFIG)
     env = {"TWB_SIM_SEG_W": int(rng.choice([1, 2, 5, 17, 64])), "TWB_SIM_SEG_CAPDIV": int(rng.choice([1, 1, 3, 1000]))}
     _serial_and_segmented(pset, wl, ca, **env)
