@@ -291,7 +291,8 @@ typedef struct tw_sim_cfg {
 #define TW_SIM_STALLED_KV 2      /* oracle.py:189-193 */
 #define TW_SIM_PRED_ERROR 3      /* predictor raised; pred_code holds TW_PRED_* */
 #define TW_SIM_CAPACITY 4        /* max_running exceeds the launch's slot capacity */
-#define TW_SIM_BAD_CONFIG 5      /* EngineConfig validation failed (engine.py:109-120) */
+#define TW_SIM_BAD_CONFIG 5      /* EngineConfig validation failed (engine.py:109-120); the
+                                    config never ran: final_now_ns = epoch, counters 0 */
 #define TW_SIM_EVENT_OVERFLOW 6  /* flag bit (status |= 1<<8) when the dump was truncated */
 
 typedef struct tw_sim_result {

@@ -144,12 +144,11 @@ def test_segmented_timekeeper_off_and_mixed_workloads_equal_oracle():
     assert np.array_equal(out.first_ns, first[:k]) and np.array_equal(out.finish_ns, finish[:k])
 
 
-@pytest.mark.parametrize("seed", range(24))
-def test_segmented_random_sweeps_equal_serial(seed):
-    """Random engine configs (chunk, budget, max_running, KV capacity down to stalls, both
-    policies, TP x PP, Timekeeper on/off, cooldown 0 to 2 ms), random workloads (0-600
-    requests, qps 1-64, short and long prompts), Table / Linear / Constant predictors, and
-    random segment counts and room divisors: the segmented run equals the serial loop."""
+def _random_sweep(seed):
+    """A random sweep: engine configs (chunk, budget, max_running, KV capacity down to
+    stalls, both policies, TP x PP, Timekeeper on/off, cooldown 0 to 2 ms, live epochs, a
+    few invalid configs), workloads of 0-600 requests at qps 1-64 with short and long
+    prompts, Table / Linear / Constant predictors; plus random segment-path knobs."""
     from paper_2601_00397_b200 import presets
     from paper_2601_00397_b200.predictor import ConstantPredictor, LinearPredictor, PredictorSet
     from paper_2601_00397_b200.sweep import EngineConfig, SchedulingPolicy, SweepConfig, config_array
@@ -181,4 +180,38 @@ def test_segmented_random_sweeps_equal_serial(seed):
     ca = config_array(cfgs)
     ca["chunk_size"][rng.random(len(ca)) < 0.03] = 0  # a few invalid configs (TW_SIM_BAD_CONFIG)
     env = {"TWB_SIM_SEG_W": int(rng.choice([1, 2, 5, 17, 64])), "TWB_SIM_SEG_CAPDIV": int(rng.choice([1, 1, 3, 1000]))}
+    return pset, wl, ca, env
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_segmented_random_sweeps_equal_serial(seed):
+    """Random sweeps (_random_sweep) with random segment counts and room divisors: the
+    segmented run equals the serial loop."""
+    pset, wl, ca, env = _random_sweep(seed)
     _serial_and_segmented(pset, wl, ca, **env)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_sweeps_equal_oracle_in_every_loop(seed):
+    """The same random sweeps against the C oracle through each event loop: the segments
+    (default), the serial latency variant (TWB_SIM_SEG=0) and, with the configs repeated
+    past 8 per SM, the throughput variant."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_00397_b200 import _lib
+
+    pset, wl, ca, _ = _random_sweep(seed)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    big = np.tile(ca, (8 * sms) // len(ca) + 1)
+    for cfgs, env, variant in ((ca, {}, "segments"), (ca, {"TWB_SIM_SEG": "0"}, "latency"), (big, {}, "throughput")):
+        out, _ = _run(pset, wl, cfgs, env)
+        assert _lib.last_sim_launch()["variant"] == variant
+        res, _, first, finish = orc.sim_many(pset.blob, cfgs, wl.wl_off, wl.offset_ns, wl.prompt, wl.output,
+                                             per_request=True)
+        for f in FIELDS:
+            assert np.array_equal(out.results[f], res[f]), (variant, f)
+        ok = (res["status"] & 0xFF) == 0
+        for c in np.flatnonzero(ok):  # stamps of runs that completed (stopped runs leave theirs unset)
+            lo, hi = out.req_base[c], out.req_base[c + 1]
+            assert np.array_equal(out.first_ns[lo:hi], first[lo:hi]) and np.array_equal(out.finish_ns[lo:hi], finish[lo:hi]), (variant, c)
