@@ -159,6 +159,12 @@ typedef struct tw_service tw_service;
 int tw_service_start(const void* pset, int64_t pset_bytes, int32_t max_slots, tw_service** out);
 int tw_service_predict(tw_service* service, const int32_t* host_slots, int32_t n_slots,
                        int32_t desc_id, int64_t* out_ns);
+/* The same request with the batch's features extracted on the host (P = total prefill
+ * tokens, D = number of decodes, C = total context; predictor.py:69-84; each < 2^48):
+ * one 32-byte mailbox read on the device, no slot transfer. The caller answers an empty
+ * batch itself (EmptyBatch): (P, D, C) of a non-empty batch are predicted as given. */
+int tw_service_predict_features(tw_service* service, int64_t total_prefill_tokens, int64_t num_decodes,
+                                int64_t total_context, int32_t desc_id, int64_t* out_ns);
 int tw_service_stop(tw_service* service);
 
 /* Device self-test of the predictor's reciprocal-based exact division against the

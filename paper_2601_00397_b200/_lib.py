@@ -175,6 +175,7 @@ EXPORTED_SYMBOLS = (
     "tw_predict_one_sync",
     "tw_service_start",
     "tw_service_predict",
+    "tw_service_predict_features",
     "tw_service_stop",
     "tw_selftest_division",
     "tw_tk_replay",
@@ -225,6 +226,7 @@ _SIGNATURES = {
     "tw_predict_one_sync": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _P]),
     "tw_service_start": (_I32, [_P, _I64, _I32, _P]),
     "tw_service_predict": (_I32, [_P, _P, _I32, _I32, _P]),
+    "tw_service_predict_features": (_I32, [_P, _I64, _I64, _I64, _I32, _P]),
     "tw_service_stop": (_I32, [_P]),
     "tw_selftest_division": (_I32, [_I64, ctypes.c_uint64, _P, _P]),
     "tw_tk_replay": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -605,45 +605,81 @@ extern "C" int tw_predict_one_sync(const void* pset, int64_t pset_bytes, const i
 // then bounded by PCIe latency (a few microseconds) instead of kernel launch + sync.
 // ---------------------------------------------------------------------------------
 struct tw_service_mailbox {
-  // host -> device, one 8-byte word written last: request counter (bits 40-63), descriptor
-  // (bits 24-39; 0xffff = stop) and slot count (bits 0-23). One word means one PCIe read
-  // tells the warp everything but the slots, which its lanes then read in one round.
-  volatile uint64_t req;
+  // host -> device, 32 bytes read by one PCIe round trip of four lanes: q[0] is the request
+  // word, written last: request counter (bits 40-63), descriptor (bits 24-39; 0xffff = stop)
+  // and slot count (bits 0-23; 0xffffff = a features request). A features request carries
+  // P, D, C in q[1..3], each tagged with the counter's low 16 bits in bits 48-63, so a read
+  // torn against the host's writes is recognised and repeated.
+  volatile uint64_t q[4];
   volatile int64_t result;  // device -> host: ns or a TW_PRED_* code
-  volatile uint64_t ack;    // device -> host: the request word answered (written last)
+  volatile uint64_t ack;    // device -> host: the request word answered (ordered after result)
   volatile int32_t cap, pad;
-  volatile int32_t slots[1];  // tok[n] then ctx[n]
+  volatile int32_t slots[1];  // tok[n] then ctx[n] (slot requests)
 };
+constexpr uint32_t kSvcFeatures = 0xffffffu;
+constexpr uint64_t kSvcTagMask = 0xffffULL << 48;
 
-__global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__ pset, uint32_t pset_bytes,
-                                                       tw_service_mailbox* mb) {
+// TWB_SVC_SLEEP_NS: back-off between polls (A/B; 0 = spin)
+#ifndef TWB_SVC_SLEEP_NS
+#define TWB_SVC_SLEEP_NS 0
+#endif
+__global__ void __launch_bounds__(32) k_predict_service(const char* __restrict__ pset_g, uint32_t pset_bytes,
+                                                       uint32_t staged, tw_service_mailbox* mb) {
+  extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x;
+  // the blob stays in shared memory for the service's life when it fits (one lookup is a
+  // chain of dependent reads: shared memory instead of L2 on every step)
+  if (staged) tma_stage_to_smem(smem + 128, pset_g, pset_bytes, reinterpret_cast<uint64_t*>(smem));
+  const char* ps = staged ? static_cast<const char*>(smem + 128) : pset_g;
+  const tw_pset_header* h = reinterpret_cast<const tw_pset_header*>(ps);
+  const bool fast = h->fast_off > 0 && pset_bytes >= (uint32_t)h->total_bytes;
+  const int n_desc = pset_ndesc(ps);
   uint64_t seen = 0;
   for (;;) {
-    uint64_t w = 0;
-    if (lane == 0) {
-      do {
-        w = mb->req;
-        if (w == seen) __nanosleep(32);
-      } while (w == seen);
+    uint64_t v = 0, w = 0;
+    for (;;) {
+      if (lane < 4) v = mb->q[lane];  // one 32-byte read
+      w = __shfl_sync(kFull, v, 0);
+      if (w == seen) {
+#if TWB_SVC_SLEEP_NS > 0
+        __nanosleep(TWB_SVC_SLEEP_NS);
+#endif
+        continue;
+      }
+      if ((w & 0xffffffu) != kSvcFeatures) break;
+      const uint64_t tag = (w >> 40) << 48;  // the counter's low 16 bits
+      if (__all_sync(kFull, lane < 1 || lane >= 4 || (v & kSvcTagMask) == tag)) break;  // not torn
     }
-    w = __shfl_sync(kFull, w, 0);
     const int32_t desc = (int32_t)((w >> 24) & 0xffffu);
     if (desc == 0xffff) return;  // stop
-    const int32_t n = (int32_t)(w & 0xffffffu);
+    const uint32_t n = (uint32_t)(w & 0xffffffu);
     int64_t Pt = 0, Dn = 0, Ct = 0;
-    for (int i = lane; i < n; i += 32) {
-      const int32_t x = mb->slots[i], c = mb->slots[n + i];  // one round of PCIe reads
-      if (x >= 0) Pt += x; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
-      Ct += c;
+    if (n == kSvcFeatures) {  // P, D, C extracted on the host (the batch's three sums)
+      Pt = (int64_t)(__shfl_sync(kFull, v, 1) & ~kSvcTagMask);
+      Dn = (int64_t)(__shfl_sync(kFull, v, 2) & ~kSvcTagMask);
+      Ct = (int64_t)(__shfl_sync(kFull, v, 3) & ~kSvcTagMask);
+    } else {
+      for (uint32_t i = lane; i < n; i += 32) {
+        const int32_t x = mb->slots[i], c = mb->slots[n + i];  // one round of PCIe reads
+        if (x >= 0) Pt += x; else Dn += 1;  // PrefillChunk / DecodeSlot (predictor.py:69-81)
+        Ct += c;
+      }
+      Pt = warp_sum_i64(Pt);
+      Dn = warp_sum_i64(Dn);
+      Ct = warp_sum_i64(Ct);
     }
-    Pt = warp_sum_i64(Pt);
-    Dn = warp_sum_i64(Dn);
-    Ct = warp_sum_i64(Ct);
     if (lane == 0) {
-      mb->result = n == 0 ? (int64_t)TW_PRED_EMPTY_BATCH : predict_one_global(pset, pset_bytes, desc, Pt, Dn, Ct);
-      __threadfence_system();  // the result lands before the acknowledgement
-      mb->ack = w;
+      int64_t r;
+      if (n == 0) r = TW_PRED_EMPTY_BATCH;
+      else if (fast && ((Pt | Dn) >> 31) == 0 && Ct >= 0 &&
+               (staged ? predict_fast<true>(ps, pset_qhdr(ps), n_desc, (int32_t)Pt, (int32_t)Dn, desc, r)
+                       : predict_fast<false>(ps, pset_qhdr(ps), n_desc, (int32_t)Pt, (int32_t)Dn, desc, r))) {
+      } else {
+        r = predict_scalar(ps, desc, Pt, Dn, Ct);
+      }
+      mb->result = r;
+      // the result before the acknowledgement, system-wide (a release store: no full fence)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&mb->ack), "l"(w) : "memory");
     }
     seen = w;
     __syncwarp();
@@ -680,7 +716,14 @@ extern "C" int tw_service_start(const void* pset, int64_t pset_bytes, int32_t ma
   sv->seq = 0;
   sv->cap = max_slots;
   cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking);
-  k_predict_service<<<1, 32, 0, sv->stream>>>(static_cast<const char*>(pset), (uint32_t)pset_bytes, sv->dev);
+  int dev = 0, max_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t stage_bytes = 128 + (((size_t)pset_bytes + 127) & ~(size_t)127);
+  const uint32_t staged = ((pset_bytes & 15) == 0 && stage_bytes <= (size_t)max_optin) ? 1u : 0u;
+  if (staged) cudaFuncSetAttribute(k_predict_service, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_bytes);
+  k_predict_service<<<1, 32, staged ? stage_bytes : 0, sv->stream>>>(static_cast<const char*>(pset),
+                                                                     (uint32_t)pset_bytes, staged, sv->dev);
   count_launch();
   const int rc = check_launch("tw_service_start");
   if (rc != TW_OK) {
@@ -707,7 +750,7 @@ extern "C" int tw_service_predict(tw_service* sv, const int32_t* host_slots, int
   for (int i = 0; i < 2 * n_slots; i++) mb->slots[i] = host_slots[i];
   __sync_synchronize();  // the slots before the request word
   const uint64_t w = ((uint64_t)(++sv->seq & 0xffffff) << 40) | ((uint64_t)desc_id << 24) | (uint64_t)n_slots;
-  mb->req = w;
+  mb->q[0] = w;
   for (int64_t spins = 0; mb->ack != w; spins++) {
     if ((spins & 0xfffff) == 0xfffff && cudaStreamQuery(sv->stream) != cudaErrorNotReady) {
       set_error("tw_service_predict: the service kernel is not running");
@@ -719,10 +762,37 @@ extern "C" int tw_service_predict(tw_service* sv, const int32_t* host_slots, int
   return TW_OK;
 }
 
+extern "C" int tw_service_predict_features(tw_service* sv, int64_t total_prefill_tokens, int64_t num_decodes,
+                                           int64_t total_context, int32_t desc_id, int64_t* out_ns) {
+  if (!sv || !out_ns || desc_id < 0 || desc_id >= 0xffff || total_prefill_tokens < 0 || num_decodes < 0 ||
+      total_context < 0 || ((total_prefill_tokens | num_decodes | total_context) >> 48) != 0) {
+    set_error("tw_service_predict_features: bad arguments");
+    return TW_EINVAL;
+  }
+  tw_service_mailbox* mb = sv->host;
+  const uint64_t seq = ++sv->seq & 0xffffff;
+  const uint64_t tag = (seq & 0xffff) << 48;
+  mb->q[1] = tag | (uint64_t)total_prefill_tokens;
+  mb->q[2] = tag | (uint64_t)num_decodes;
+  mb->q[3] = tag | (uint64_t)total_context;
+  __sync_synchronize();  // the features before the request word
+  const uint64_t w = (seq << 40) | ((uint64_t)desc_id << 24) | (uint64_t)kSvcFeatures;
+  mb->q[0] = w;
+  for (int64_t spins = 0; mb->ack != w; spins++) {
+    if ((spins & 0xfffff) == 0xfffff && cudaStreamQuery(sv->stream) != cudaErrorNotReady) {
+      set_error("tw_service_predict_features: the service kernel is not running");
+      return TW_ECUDA;
+    }
+  }
+  __sync_synchronize();
+  *out_ns = mb->result;
+  return TW_OK;
+}
+
 extern "C" int tw_service_stop(tw_service* sv) {
   if (!sv) return TW_OK;
   __sync_synchronize();
-  sv->host->req = ((uint64_t)(++sv->seq & 0xffffff) << 40) | (0xffffULL << 24);  // stop
+  sv->host->q[0] = ((uint64_t)(++sv->seq & 0xffffff) << 40) | (0xffffULL << 24);  // stop
   const cudaError_t e = cudaStreamSynchronize(sv->stream);
   cudaStreamDestroy(sv->stream);
   cudaFreeHost(sv->host);

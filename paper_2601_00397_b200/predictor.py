@@ -173,7 +173,7 @@ class _DevicePredictor:
         slots in pinned memory, which a one-warp kernel reads and answers in place
         (zero-copy); the call polls the answer word (~20 us on a B200 box through
         Python, launch-bound). A process that only predicts can use the resident service instead
-        (``predictor_set.service()``, ~14.5 us, no launch on the round trip)."""
+        (``predictor_set.service()``, ~6.5 us, no launch on the round trip)."""
         code = self.predictor_set.live().predict_one(batch)
         if code < 0:
             raise_for_code(code, _describe(batch))
@@ -668,9 +668,29 @@ class PredictorService:
         self._out = ctypes.c_int64()
         self._out_ref = ctypes.byref(self._out)
         self._fn = _lib.load().tw_service_predict
+        self._ffn = _lib.load().tw_service_predict_features
         atexit.register(self.close)
 
     def predict_one(self, batch, desc_id: int = 0) -> int:
+        """One batch: its three feature sums (predictor.py:69-84, the reference's own
+        properties) go to the device in one 32-byte mailbox write; the lookup runs there."""
+        chunks, decodes = batch.prefill_chunks, batch.decodes
+        if not chunks and not decodes:
+            return TW_PRED_EMPTY_BATCH
+        P = C = 0
+        for c in chunks:
+            P += c.chunk_tokens
+            C += c.context_len_before
+        for dslot in decodes:
+            C += dslot.context_len
+        D = len(decodes)
+        if min(P, C) < 0 or max(P, D, C) >= 1 << 48:  # outside the mailbox's fields: slot request
+            return self.predict_slots(batch, desc_id)
+        _lib.check(self._ffn(self._h, P, D, C, desc_id, self._out_ref), "tw_service_predict_features")
+        return int(self._out.value)
+
+    def predict_slots(self, batch, desc_id: int = 0) -> int:
+        """The same through the slot request: the device reads the slots and sums them."""
         chunks, decodes = batch.prefill_chunks, batch.decodes
         n = len(chunks) + len(decodes)
         if n > self.max_slots:

@@ -25,6 +25,25 @@ t = time.perf_counter()
 for _ in range(2000):
     sv.predict_one(batch)
 res["resident_service_us"] = round((time.perf_counter() - t) / 2000 * 1e6, 2)
+t = time.perf_counter()
+for _ in range(2000):
+    sv.predict_slots(batch)
+res["resident_service_slots_us"] = round((time.perf_counter() - t) / 2000 * 1e6, 2)
+sys.path.insert(0, "baseline/_ref")
+try:  # the reference's own predict() on the same batch, for scale
+    from timewarp.predictor import BatchComposition as RB, DecodeSlot as RD, PrefillChunk as RC
+    from timewarp.predictor import TablePredictor as RT
+
+    from paper_2601_00397_b200 import calibration
+    rp = RT.from_csv(calibration.csv_path("8b", 1, 1), allow_extrapolation=True)
+    rbatch = RB(prefill_chunks=(RC("p", 384, 0),), decodes=tuple(RD(f"d{i}", 500 + i) for i in range(5)))
+    assert rp.predict(rbatch) == res["value_ns"]
+    t = time.perf_counter()
+    for _ in range(2000):
+        rp.predict(rbatch)
+    res["reference_python_predict_us"] = round((time.perf_counter() - t) / 2000 * 1e6, 2)
+except ImportError:
+    pass
 assert sv.predict_one(batch) == res["value_ns"] == int(pred.predictor_set.predict_batches([batch], [0])[0])
 sv.close()
 print(json.dumps(res))
