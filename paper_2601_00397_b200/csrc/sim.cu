@@ -2053,18 +2053,34 @@ static int seg_wmax(int32_t n_cfg, int sms) {
   if (w < 1) w = 1;
   return (int)w;
 }
-static int64_t seg_xtra(int32_t n_cfg, int wmax) {  // ~256 MB of overrun room in all
+// Extra requests of room per segment: ~256 MB of overrun room in all, at most 4,096 and at
+// most an eighth of the launch's requests (an overrun past the room re-runs serially from the
+// segment's last regeneration point, so the bound trades memory for rare serial pieces)
+static int64_t seg_xtra(int32_t n_cfg, int wmax, int64_t total_requests) {
   const int64_t per = kSegLogPerReq * (int64_t)sizeof(TkLog) + 64;
   int64_t x = (256LL << 20) / (per * (int64_t)n_cfg * wmax);
-  return x < 64 ? 64 : (x > 4096 ? 4096 : x);
+  x = x > 4096 ? 4096 : x;
+  x = std::min(x, total_requests / 8);
+  return x < 64 ? 64 : x;
 }
 static int64_t seg_header_bytes(int32_t n_cfg, int wmax) {  // counters, plan, summaries
   return align256(64 + align256(4LL * n_cfg) + align256(4LL * n_cfg * wmax) +
                   align256((int64_t)sizeof(SegSummary) * n_cfg * wmax));
 }
-static int64_t seg_fixed_bytes(int32_t n_cfg, int wmax) {  // plus every segment's extra room
-  return seg_header_bytes(n_cfg, wmax) +
-         seg_xtra(n_cfg, wmax) * n_cfg * wmax * (kSegLogPerReq * (int64_t)sizeof(TkLog) + 64);
+// the scratch the segments need for R requests (tw_sim_seg_scratch_bytes)
+static int64_t seg_bytes(int32_t n_cfg, int wmax, int64_t R) {
+  return seg_header_bytes(n_cfg, wmax) + 4 * 256 + kSegPerReqBytes * R +
+         seg_xtra(n_cfg, wmax, R) * n_cfg * wmax * (kSegLogPerReq * (int64_t)sizeof(TkLog) + 64);
+}
+// the largest request count whose segment records fit in `bytes` (seg_bytes is increasing)
+static int64_t seg_r_max(int32_t n_cfg, int wmax, int64_t bytes) {
+  int64_t lo = 0, hi = bytes / kSegPerReqBytes + 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (seg_bytes(n_cfg, wmax, mid) <= bytes) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 // bytes of scratch tw_sim_many needs: the 64-byte work counter, plus the global slot state
@@ -2170,9 +2186,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
   if (req_base && !ev && !g_checks && !g_prof && seg_enabled_for(n_cfg, sms) &&
       128 + 4 * per_warp <= (size_t)max_optin) {
     const int wmax = seg_wmax(n_cfg, sms);
-    const int64_t fixed = seg_fixed_bytes(n_cfg, wmax);
-    if (scratch_bytes >= fixed + kSegPerReqBytes + 4 * 256) {
-      const int64_t r_max = (scratch_bytes - fixed - 4 * 256) / kSegPerReqBytes;
+    const int64_t r_max = seg_r_max(n_cfg, wmax, scratch_bytes);
+    if (r_max >= 1) {
       char* b = static_cast<char*>(scratch);
       SegParams q;
       q.wmax = wmax;
@@ -2189,8 +2204,8 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       o += align256(4 * r_max);
       q.reg = reinterpret_cast<SegRegen*>(b + o);
       o += align256((int64_t)sizeof(SegRegen) * r_max);
-      q.xtra = seg_xtra(n_cfg, wmax);
-      const int64_t units = r_max + q.xtra * n_cfg * wmax;  // fixed part counted the xtra bytes
+      q.xtra = seg_xtra(n_cfg, wmax, r_max);
+      const int64_t units = r_max + q.xtra * n_cfg * wmax;
       q.log = reinterpret_cast<TkLog*>(b + o);
       o += align256((int64_t)sizeof(TkLog) * kSegLogPerReq * units);
       q.side = reinterpret_cast<int64_t*>(b + o);
@@ -2331,7 +2346,7 @@ extern "C" int64_t tw_sim_seg_scratch_bytes(int32_t n_cfg, int64_t total_request
   const int sms = seg_sms();
   if (!seg_enabled_for(n_cfg, sms) || total_requests < 0) return 0;
   const int wmax = seg_wmax(n_cfg, sms);
-  return seg_fixed_bytes(n_cfg, wmax) + 4 * 256 + kSegPerReqBytes * (total_requests > 0 ? total_requests : 1);
+  return seg_bytes(n_cfg, wmax, total_requests > 0 ? total_requests : 1);
 }
 
 extern "C" int tw_sim_set_checks(int32_t* per_config_8xi32) {
