@@ -724,8 +724,9 @@ def ksim_roofline(sw, dev, ms, device, peak_gbs, sm_mhz, key, heavy_alone=True):
     heavy = int(np.argmax(cyc))
     chain = {"heaviest_config": heavy, "heaviest_label": sw.configs[heavy].label,
              "heaviest_cycles_in_sweep": int(cyc[heavy]), "sweep_ms": round(ms, 4)}
-    if heavy_alone:
-        chain["heaviest_alone_ms"] = round(time_alone(sw.subset([heavy]), device), 4)
+    if heavy_alone:  # the serial loop (one warp), as the sweep runs it
+        with _Env(TWB_SIM_SEG=0):
+            chain["heaviest_alone_ms"] = round(time_alone(sw.subset([heavy]), device), 4)
     extra = {
         "kernel": "k_sim", "launch": launch, "traffic": measured_traffic(key),
         "cycles_per_iteration": round(float(cyc.sum() / max(iters.sum(), 1)), 1),
