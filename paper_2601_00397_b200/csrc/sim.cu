@@ -1682,8 +1682,7 @@ __global__ void __launch_bounds__(128, TWB_SEG_TK_BLOCKS) k_seg_tk(SimParams p, 
 // -delta), provided delta keeps every wall decision. Returns false when that cannot be
 // shown (the caller re-runs the piece serially); `exact` (the config's own start) copies.
 __device__ __forceinline__ bool tk_compose(TkGrid& g, const TkState& E, const TkState& T, int64_t d_lo,
-                                           int64_t d_hi, bool exact, int32_t j, const int64_t* __restrict__ ts,
-                                           int32_t n, int64_t epoch) {
+                                           int64_t d_hi, bool exact, int32_t j, int64_t tj) {
   int64_t delta = 0;
   if (!exact && T.seq == E.seq) {
     // no broadcast in the piece: it is empty (entry = exit, e.g. a segment out of room at
@@ -1699,7 +1698,6 @@ __device__ __forceinline__ bool tk_compose(TkGrid& g, const TkState& E, const Tk
       const int64_t wait = g.last_bcast + g.cooldown - g.wall;
       if (wait > 0) slp = (wait == g.cooldown) ? g.conv_cooldown : cold_fake_sleep(wait);
     }
-    const int64_t tj = epoch + __ldg(ts + j);
     if (!(g.wall + g.offset < tj - slp) || !(E.wall + E.offset < tj - slp)) return false;
     delta = g.wall - E.wall;
     if (delta < d_lo || delta >= d_hi) return false;
@@ -1746,7 +1744,17 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
     const bool tk_on = (cfg.flags & TW_SIM_TIMEKEEPER) != 0;
     const int64_t rb = p.req_base[c];
     const int32_t W = q.nseg[c];
-    const int32_t* a0s = q.seg_a0 + (int64_t)c * q.wmax;
+    // the segment starts and their arrival times in shared memory (the chain reads them at
+    // every piece), and the next segment's summary loaded ahead of its turn
+    int64_t* ta0 = reinterpret_cast<int64_t*>(smem + 128 + (size_t)(blockDim.x >> 5) * 7 * 4 * p.cap) +
+                   (size_t)warp * 2 * q.wmax;
+    int32_t* a0s = reinterpret_cast<int32_t*>(ta0 + q.wmax);
+    for (int32_t k = lane; k < W; k += 32) {
+      const int32_t a = q.seg_a0[(int64_t)c * q.wmax + k];
+      a0s[k] = a;
+      ta0[k] = a < n ? epoch + __ldg(ts + a) : INT64_MAX;
+    }
+    __syncwarp();
     const SegSummary* sm = q.summ + (int64_t)c * q.wmax;
     int32_t* regpos = q.regpos + rb;
     SegRegen* reg = q.reg + rb;
@@ -1805,10 +1813,17 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
     SegRegen e{};
     bool exact = true;     // the chain's first piece starts with the config (no guess)
     bool serial = W == 0;  // not segmented: the whole config serially from arrival 0
+    SegSummary s_next;
+    int32_t w_next = -1;
     for (;;) {
       if (!serial) {
-        const SegSummary s = sm[w];
+        const SegSummary s = (w == w_next) ? s_next : sm[w];
+        if (w + 1 < W) {  // the usual successor, fetched while this piece is joined
+          s_next = sm[w + 1];
+          w_next = w + 1;
+        }
         const int32_t a1w = (w + 1 < W) ? a0s[w + 1] : n;
+        const int64_t tj = (j_in == a0s[w]) ? ta0[w] : epoch + __ldg(ts + j_in);
         if (s.status == TW_SIM_BAD_CONFIG || s.status == TW_SIM_CAPACITY) {
           status = s.status;
           invalid_cfg = true;
@@ -1820,7 +1835,7 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
           n_ovf++;
           const int32_t jr = s.last_regen;
           const SegRegen E = reg[jr];
-          if (!tk_on || tk_compose(g, e.tk, E.tk, s.d_lo, s.d_hi, exact, j_in, ts, n, epoch)) {
+          if (!tk_on || tk_compose(g, e.tk, E.tk, s.d_lo, s.d_hi, exact, j_in, tj)) {
             add(E.events, E.dig, E.msum, E.steps, e);
             js = jr;
           } else {
@@ -1828,7 +1843,7 @@ __global__ void __launch_bounds__(kSimThreads, 1) k_sim_join(SimParams p, SegPar
             n_tkfail++;
           }
           serial = true;
-        } else if (tk_on && !tk_compose(g, e.tk, s.tk, s.d_lo, s.d_hi, exact, j_in, ts, n, epoch)) {
+        } else if (tk_on && !tk_compose(g, e.tk, s.tk, s.d_lo, s.d_hi, exact, j_in, tj)) {
           js = j_in;  // the Timekeeper guess does not carry over: this piece serially
           serial = true;
           n_tkfail++;
@@ -1954,7 +1969,6 @@ int sim_seg_prepare(int threads, size_t smem, int* per_sm, bool lat) {
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg<true>, threads, smem);
   }
   cudaFuncSetAttribute(k_sim_seg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_sim_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_sim_seg<false>, threads, smem);
 }
 void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const SimParams& p, const SegParams& q,
@@ -1968,6 +1982,7 @@ void sim_seg_launch(int grid, int threads, size_t smem, cudaStream_t s, const Si
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seg_tk, 128, 0);
   k_seg_tk<<<(int)std::min<int64_t>((items + 3) / 4, (int64_t)sms * std::max(per_sm, 1)), 128, 0, s>>>(p, q);
+  cudaFuncSetAttribute(k_sim_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem);
   SimParams pj = p;  // the join reads the whole blob from global memory
   pj.pset_smem = 0;
   pj.pset_bytes = join_pset_bytes;
@@ -2187,7 +2202,9 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       128 + 4 * per_warp <= (size_t)max_optin) {
     const int wmax = seg_wmax(n_cfg, sms);
     const int64_t r_max = seg_r_max(n_cfg, wmax, scratch_bytes);
-    if (r_max >= 1) {
+    // the join adds each warp's segment starts and their arrival times (12 B per segment)
+    const size_t join_smem = 128 + 4 * per_warp + (size_t)kSimWarps * 16 * wmax;
+    if (r_max >= 1 && join_smem <= (size_t)max_optin) {
       char* b = static_cast<char*>(scratch);
       SegParams q;
       q.wmax = wmax;
@@ -2220,9 +2237,9 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
       // geometry), TWB_SIM_SEG_STAGE=<bytes> stages only that prefix (e.g. the core)
       const char* lat_env = getenv("TWB_SIM_SEG_LAT");
       const int lat = lat_env ? atoi(lat_env) : 0;
-      const size_t join_smem = 128 + 4 * per_warp;
-      size_t smem = join_smem;
-      sim_seg_prepare(threads, join_smem, &per_sm, false);
+      const size_t seg_smem = 128 + 4 * per_warp;
+      size_t smem = seg_smem;
+      sim_seg_prepare(threads, seg_smem, &per_sm, false);
       uint32_t seg_pset_bytes = (uint32_t)pset_bytes, seg_pset_smem = 0;
       if (lat >= 1) {
         const char* st_env = getenv("TWB_SIM_SEG_STAGE");
@@ -2232,7 +2249,7 @@ extern "C" int tw_sim_many(const void* pset, int64_t pset_bytes, const tw_sim_cf
         smem = 128 + seg_pset_smem + 4 * per_warp;
         if (smem <= (size_t)max_optin) sim_seg_prepare(threads, smem, &per_sm, true);
         else {
-          smem = join_smem;
+          smem = seg_smem;
           seg_pset_smem = 0;
           seg_pset_bytes = (uint32_t)pset_bytes;
         }
