@@ -150,7 +150,7 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 // dozen of ~1,000) are compacted into a small buffer and the later passes scan only those.
 constexpr int kMetCand = 448;
 __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t out[3]) {
-  __shared__ uint32_t hist[3][256];
+  __shared__ __align__(16) uint32_t hist[3][256];
   __shared__ uint64_t pre[3], red_mn[kMetWarps], red_mx[kMetWarps];
   __shared__ uint64_t cand[kMetCand];
   __shared__ int rem[3], sh_shift, ncand;
@@ -192,17 +192,18 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
   int nsrc = n;
   bool compacted = false;
   for (int shift = sh_shift; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 3 * 256; i += kMetThreads) (&hist[0][0])[i] = 0;
+    // the first digit: every target still shares the prefix, one histogram serves all three
+    const bool one = shift == sh_shift;
+    for (int i = tid; i < (one ? 256 : 3 * 256) / 4; i += kMetThreads)
+      reinterpret_cast<uint4*>(&hist[0][0])[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     const uint64_t p0 = pre[0], p1 = pre[1], p2 = pre[2];
     for (int i = tid; i < nsrc; i += kMetThreads) {
       const uint64_t k = src[i];
       if (k == ~0ULL) continue;
       const uint32_t dg = (uint32_t)(k >> shift) & 255u;
-      if (shift >= 56) {
+      if (one) {
         atomicAdd(&hist[0][dg], 1u);
-        atomicAdd(&hist[1][dg], 1u);
-        atomicAdd(&hist[2][dg], 1u);
       } else {
         const int hs = shift + 8;
         if (((k ^ p0) >> hs) == 0) atomicAdd(&hist[0][dg], 1u);
@@ -216,7 +217,7 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
       uint32_t c[8], sl = 0;
 #pragma unroll
       for (int b = 0; b < 8; b++) {
-        c[b] = hist[t][8 * lane + b];
+        c[b] = hist[one ? 0 : t][8 * lane + b];
         sl += c[b];
       }
       uint32_t incl = sl;
@@ -266,7 +267,13 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
   __syncthreads();
 }
 
+constexpr uint64_t kSignBit = 0x8000000000000000ULL;
+
 // nearest-rank p50 / p90 / p99 of the count valid keys among keys[0, n) (metrics.py:62-79)
+// kInt: keys are int64 values with the sign bit flipped (TTFT, e2e: the reference's float(t)
+// is monotone in t, so the order statistics of the floats are the floats of the int64 order
+// statistics, and integer keys share more high bits: fewer radix passes than float keys)
+template <bool kInt>
 __device__ void stats_from_keys(const uint64_t* keys, int n, int count, double mean, tw_latency_stats& st) {
   if (count > 0) {
     const int r[3] = {nearest_rank_index(50, count), nearest_rank_index(90, count), nearest_rank_index(99, count)};
@@ -274,9 +281,9 @@ __device__ void stats_from_keys(const uint64_t* keys, int n, int count, double m
     select3(keys, n, r, v);
     if (threadIdx.x == 0) {
       st.count = count;
-      st.p50 = dval(v[0]);
-      st.p90 = dval(v[1]);
-      st.p99 = dval(v[2]);
+      st.p50 = kInt ? (double)(int64_t)(v[0] ^ kSignBit) : dval(v[0]);
+      st.p90 = kInt ? (double)(int64_t)(v[1] ^ kSignBit) : dval(v[1]);
+      st.p99 = kInt ? (double)(int64_t)(v[2] ^ kSignBit) : dval(v[2]);
       st.mean = mean;
     }
   } else if (threadIdx.x == 0) {
@@ -387,10 +394,10 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
       }
       for (int i = tid; i < n; i += kMetThreads) {
         const int64_t t = (m == 0 ? p.first[rb + i] : p.finish[rb + i]) - epoch - p.ts[wl0 + i];
-        keys[i] = dkey((double)t);
+        keys[i] = (uint64_t)t ^ kSignBit;  // t < INT64_MAX, so never the no-value key ~0
       }
       const double sum = exact ? (double)s : sh_mean;
-      stats_from_keys(keys, n, n, n > 0 ? __ddiv_rn(sum, (double)n) : 0.0, m == 0 ? res.ttft : res.e2e);
+      stats_from_keys<true>(keys, n, n, n > 0 ? __ddiv_rn(sum, (double)n) : 0.0, m == 0 ? res.ttft : res.e2e);
     }
     // ---- TPOT over requests with more than one output token (metrics.py:54-60, 100-101)
     double* tv = p.tpot_vals ? p.tpot_vals + (int64_t)c * p.cap : nullptr;
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
       const double t = vals[i];
       keys[i] = isnan(t) ? ~0ULL : dkey(t);
     }
-    stats_from_keys(keys, n, n_tpot, sh_mean, res.tpot);
+    stats_from_keys<false>(keys, n, n_tpot, sh_mean, res.tpot);
     if (tid == 0) {
       res.status = TW_METRICS_OK;
       p.out[c] = res;
