@@ -178,10 +178,11 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
     mn = red_mn[0] < mn ? red_mn[0] : mn;
     mx = red_mx[0] > mx ? red_mx[0] : mx;
     const uint64_t diff = mn ^ mx;
-    // highest differing bit -> first digit; -8: every valid key is the same (mn)
-    sh_shift = diff ? ((63 - __clzll((long long)diff)) / 8) * 8 : -8;
-    const uint64_t keep = (sh_shift >= 56 || sh_shift < 0) ? (sh_shift < 0 ? ~0ULL : 0ULL)
-                                                            : ~((1ULL << (sh_shift + 8)) - 1);
+    // the first digit is the 8 bits from the highest differing bit h down (all of it split
+    // 256 ways, not the few bits of an aligned digit); -8: every valid key is the same (mn)
+    const int h = diff ? 63 - __clzll((long long)diff) : -1;
+    sh_shift = h < 0 ? -8 : (h >= 7 ? h - 7 : 0);
+    const uint64_t keep = h < 0 ? ~0ULL : (h >= 63 ? 0ULL : ~((2ULL << h) - 1));
     for (int t = 0; t < 3; t++) {
       pre[t] = mn & keep;
       rem[t] = r[t];
@@ -191,9 +192,13 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
   const uint64_t* src = keys;
   int nsrc = n;
   bool compacted = false;
-  for (int shift = sh_shift; shift >= 0; shift -= 8) {
+  // digits of 8 bits from sh_shift down, the last one (at bit 0) narrower
+  for (int shift = sh_shift, width = sh_shift >= 0 ? min(8, 64 - sh_shift) : 0, top = shift + width; shift >= 0;
+       top = shift, width = min(8, shift), shift -= width) {
+    if (width == 0) break;
     // the first digit: every target still shares the prefix, one histogram serves all three
     const bool one = shift == sh_shift;
+    const uint32_t dmask = (1u << width) - 1u;
     for (int i = tid; i < (one ? 256 : 3 * 256) / 4; i += kMetThreads)
       reinterpret_cast<uint4*>(&hist[0][0])[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
@@ -201,11 +206,11 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
     for (int i = tid; i < nsrc; i += kMetThreads) {
       const uint64_t k = src[i];
       if (k == ~0ULL) continue;
-      const uint32_t dg = (uint32_t)(k >> shift) & 255u;
+      const uint32_t dg = (uint32_t)(k >> shift) & dmask;
       if (one) {
         atomicAdd(&hist[0][dg], 1u);
       } else {
-        const int hs = shift + 8;
+        const int hs = top;  // < 64: not the first digit
         if (((k ^ p0) >> hs) == 0) atomicAdd(&hist[0][dg], 1u);
         if (((k ^ p1) >> hs) == 0) atomicAdd(&hist[1][dg], 1u);
         if (((k ^ p2) >> hs) == 0) atomicAdd(&hist[2][dg], 1u);
@@ -296,10 +301,10 @@ __device__ void stats_from_keys(const uint64_t* keys, int n, int count, double m
 // kGlobal: the keys live in a caller-provided global scratch (cap per CTA) instead of
 // dynamic shared memory: workloads above ~28,000 requests (metrics.py has no limit)
 template <bool kGlobal>
-__global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
+__global__ void __launch_bounds__(kMetThreads, 10) k_metrics(MetParams p) {
   extern __shared__ __align__(16) uint64_t skeys[];
   uint64_t* keys = kGlobal ? p.gkeys + (size_t)blockIdx.x * (size_t)p.cap : skeys;
-  __shared__ int64_t red[6][kMetWarps];
+  __shared__ int64_t red[7][kMetWarps];
   __shared__ tw_run_metrics res;
   __shared__ double sh_mean;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -327,6 +332,11 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
     }
     // ---- pass 1: per-request reductions (collect_metrics, metrics.py:213-247)
     BlockRed r = {0, 0, INT64_MIN, 0, 0, 0};
+    // the int64 sums stand for the reference's float sums only when every partial sum is an
+    // exact float: all values in [0, (2^53 - 1) / n] (else, e.g. past 2^63 or with
+    // negative values, the CPython-order float sum below)
+    const uint64_t lim = (uint64_t)(((1LL << 53) - 1) / (n > 0 ? n : 1));
+    int32_t big = 0;  // bit 0: a TTFT value past the bound, bit 1: an e2e value
     for (int i = tid; i < n; i += kMetThreads) {
       const int64_t fin = p.finish[rb + i], fst = p.first[rb + i];
       const int64_t off = p.ts[wl0 + i];
@@ -338,20 +348,23 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
       r.tokens += op;
       const int64_t fr = fin - epoch;
       r.maxfin = fr > r.maxfin ? fr : r.maxfin;
-      r.s_ttft += fst - epoch - off;
-      r.s_e2e += fin - epoch - off;
+      const int64_t a = fst - epoch - off, b = fin - epoch - off;
+      r.s_ttft += a;
+      r.s_e2e += b;
+      big |= ((uint64_t)a > lim) | (((uint64_t)b > lim) << 1);
       r.n_tpot += op > 1;
     }
-    int64_t v[6] = {r.miss, r.tokens, r.maxfin, r.s_ttft, r.s_e2e, r.n_tpot};
+    // the flags as two counts, 20 bits apart (at most 128 per CTA)
+    int64_t v[7] = {r.miss, r.tokens, r.maxfin, r.s_ttft, r.s_e2e, r.n_tpot, (big & 1) + ((int64_t)(big >> 1) << 20)};
 #pragma unroll
-    for (int k = 0; k < 6; k++) {
+    for (int k = 0; k < 7; k++) {
       const int64_t w = (k == 2) ? warp_max_i64(v[k]) : warp_sum_i64(v[k]);
       if (lane == 0) red[k][warp] = w;
     }
     __syncthreads();
     if (tid < 32) {
 #pragma unroll
-      for (int k = 0; k < 6; k++) {
+      for (int k = 0; k < 7; k++) {
         int64_t w = lane < kMetWarps ? red[k][lane] : (k == 2 ? INT64_MIN : 0);
         w = (k == 2) ? warp_max_i64(w) : warp_sum_i64(w);
         if (lane == 0) red[k][0] = w;
@@ -361,6 +374,7 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
     const int64_t miss = red[0][0], tokens = red[1][0], maxfin = red[2][0];
     const int64_t s_ttft = red[3][0], s_e2e = red[4][0];
     const int n_tpot = (int)red[5][0];
+    const bool big_sum[2] = {(red[6][0] & 0xfffff) != 0, (red[6][0] >> 20) != 0};
     if (miss > 0) {  // IncompleteLog (metrics.py:236-240)
       if (tid == 0) {
         res.status = TW_METRICS_INCOMPLETE;
@@ -382,7 +396,7 @@ __global__ void __launch_bounds__(kMetThreads) k_metrics(MetParams p) {
     // ---- TTFT, e2e: exact integer sums unless they could round, then the CPython sum
     for (int m = 0; m < 2; m++) {
       const int64_t s = m == 0 ? s_ttft : s_e2e;
-      const bool exact = s >= 0 && s < (1LL << 53);
+      const bool exact = !big_sum[m] && s >= 0 && s < (1LL << 53);
       if (!exact) {
         for (int i = tid; i < n; i += kMetThreads) {
           const int64_t t = (m == 0 ? p.first[rb + i] : p.finish[rb + i]) - epoch - p.ts[wl0 + i];

@@ -1017,6 +1017,57 @@ def test_device_metrics_beyond_shared_memory_equal_oracle():
         assert int(got[w]["status"]) == 0 and got[w].tobytes() == want.tobytes(), w
 
 
+def test_device_metrics_radix_digit_edges_equal_oracle():
+    """The percentile selection splits keys on 8-bit digits from the highest bit where the
+    keys differ down: stamps written straight into the device buffers with latency spreads of
+    0 to 2^62 ns, spreads just below and above digit boundaries, heavy ties, and TPOT values
+    from tiny to huge, every record equal to the C oracle's."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_00397_b200.predictor import ConstantPredictor, PredictorSet
+    from paper_2601_00397_b200.sweep import DeviceSweep, EngineConfig, SweepConfig, config_array
+    from paper_2601_00397_b200.workload import pack_arrays
+
+    rng = np.random.default_rng(77)
+    spreads = [0, 1, 3, 127, 128, 255, 256, 257, 2**15 - 1, 2**16, 2**31 + 5, 2**33, 2**40 - 1, 2**52, 2**62]
+    arrays, lat = [], []
+    for i, sp in enumerate(spreads * 2):
+        n = int(rng.integers(1, 1500))
+        ts = np.sort(rng.integers(0, 10**9, n)).astype(np.int64)
+        op = rng.integers(1, 50, n).astype(np.int32)
+        base = int(rng.integers(0, 10**6))
+        if i >= len(spreads):  # heavy ties: a handful of distinct latencies
+            ttft = base + rng.choice(np.array([0, sp // 2, sp], np.int64), n)
+        else:
+            ttft = base + (rng.integers(0, sp + 1, n, dtype=np.int64) if sp else np.zeros(n, np.int64))
+        dec = rng.integers(0, max(sp, 1), n, dtype=np.int64) // 3
+        arrays.append((ts, rng.integers(1, 900, n).astype(np.int32), op))
+        lat.append((ttft, dec))
+    eng = EngineConfig(chunk_size=512, max_batch_tokens=2048, max_running=256, kv_block_tokens=16,
+                       kv_capacity_blocks=1 << 20)
+    cfgs = config_array([SweepConfig(engine=eng, pred_id=0, workload_id=w, epoch_ns=13 * w)
+                         for w in range(len(arrays))])
+    dev = DeviceSweep(PredictorSet([ConstantPredictor(900)]), pack_arrays(arrays), cfgs, per_request=True)
+    dev.run()
+    out = dev.fetch()
+    first = np.zeros(dev.d_first.numel(), np.int64)
+    finish = np.zeros(dev.d_finish.numel(), np.int64)
+    for w, (ts, pr, op) in enumerate(arrays):
+        rb, n = int(out.req_base[w]), len(ts)
+        ttft, dec = lat[w]
+        first[rb : rb + n] = 13 * w + ts + ttft
+        finish[rb : rb + n] = first[rb : rb + n] + dec
+    dev.d_first.copy_(torch.from_numpy(first))
+    dev.d_finish.copy_(torch.from_numpy(finish))
+    dev.run_metrics()
+    got = dev.fetch_metrics()
+    for w, (ts, pr, op) in enumerate(arrays):
+        rb, n = int(out.req_base[w]), len(ts)
+        want = orc.metrics(ts, op, first[rb : rb + n], finish[rb : rb + n], 13 * w)
+        assert got[w].tobytes() == want.tobytes(), (w, spreads[w % len(spreads)])
+
+
 def test_device_metrics_equal_oracle_on_sweep_1024():
     from oracle import oracle as orc
     from paper_2601_00397_b200 import presets
