@@ -232,6 +232,7 @@ __device__ void select3(const uint64_t* keys, int n, const int r[3], uint64_t ou
         if (lane >= o) incl += w;
       }
       const int target = rem[t];
+      __syncwarp();  // every lane has read rem[t] before one of them rewrites it
       const unsigned hit = __ballot_sync(kFull, (int)incl > target);
       if (lane == __ffs(hit) - 1) {
         int cum = (int)(incl - sl);
