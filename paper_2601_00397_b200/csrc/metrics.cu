@@ -302,7 +302,7 @@ __device__ void stats_from_keys(const uint64_t* keys, int n, int count, double m
 // kGlobal: the keys live in a caller-provided global scratch (cap per CTA) instead of
 // dynamic shared memory: workloads above ~28,000 requests (metrics.py has no limit)
 template <bool kGlobal>
-__global__ void __launch_bounds__(kMetThreads, 10) k_metrics(MetParams p) {
+__global__ void __launch_bounds__(kMetThreads, 12) k_metrics(MetParams p) {
   extern __shared__ __align__(16) uint64_t skeys[];
   uint64_t* keys = kGlobal ? p.gkeys + (size_t)blockIdx.x * (size_t)p.cap : skeys;
   __shared__ int64_t red[7][kMetWarps];
